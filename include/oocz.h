@@ -1,0 +1,177 @@
+/*
+ * oocz.h -- C ABI of liboocz.so: out-of-core 25-point stencil time stepping
+ * with on-the-fly ZFP-style fixed-rate compression, B200 (sm_100a).
+ *
+ * Method: Shen, Wu, Okita, Ino, "Accelerating GPU-Based Out-of-Core Stencil
+ * Computation with On-the-Fly Compression", arXiv 2109.05410.
+ * The calls follow the paper's problem statement (Sec. VI):
+ * given two read-write time levels u^t, u^{t-1}, a read-only model m, a
+ * 25-point stencil and a compression rate, advance n steps and read back.
+ *
+ * Conventions
+ *  - Every call returns oocz_status: 0 = OK, < 0 = error.  A failed call
+ *    leaves the context unchanged unless it returns OOCZ_ECUDA / OOCZ_ENCCL,
+ *    which poison the context (every later call returns OOCZ_ESTATE).
+ *  - Fields are fp32, x fastest then y then z ("C order" [z][y][x]).
+ *  - A context is used by one host thread at a time.
+ *  - Pointers named d_* are device pointers on the context's device; all
+ *    others are host pointers.  The caller owns every pointer it passes; the
+ *    library never keeps one past the call (except the stream handles passed
+ *    to the codec / kernel calls, used only during the call).
+ *  - No torch types, no C++ types: plain pointers, sizes, and PODs.
+ */
+#ifndef OOCZ_H
+#define OOCZ_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OOCZ_ABI_VERSION 1
+
+typedef enum {
+    OOCZ_OK = 0,
+    OOCZ_EINVAL = -1,      /* bad value: P < 2h, P does not divide nz/world, rate > 64, ... */
+    OOCZ_EALIGN = -2,      /* nx, ny, nz, P or h not a multiple of 4 (ZFP blocks are 4^3) */
+    OOCZ_ECFL = -3,        /* max m exceeds the leapfrog stability bound m_max(c), or m < 0 */
+    OOCZ_ECAPACITY = -4,   /* device (or pinned host) memory budget too small */
+    OOCZ_ENONFINITE = -5,  /* NaN or Inf in a field passed to set_field */
+    OOCZ_ESTATE = -6,      /* step before all fields were set, or poisoned context */
+    OOCZ_ECUDA = -7,       /* CUDA runtime / driver failure (poisons the context) */
+    OOCZ_ENCCL = -8        /* NCCL failure (poisons the context) */
+} oocz_status;
+
+/* field ids ("two read-write datasets ... and a read-only dataset") */
+enum { OOCZ_U = 0,        /* u^t       (read-write) */
+       OOCZ_UPREV = 1,    /* u^{t-1}   (read-write) */
+       OOCZ_M = 2 };      /* m = (v dt / dx)^2 (read-only) */
+
+/* where the per-field store lives */
+enum { OOCZ_STORE_HOST = 0,    /* pinned host DRAM: the paper's out-of-core path */
+       OOCZ_STORE_DEVICE = 1 };/* resident in HBM: same pipeline, no host link (measures the kernels) */
+
+typedef struct {
+    int32_t  nx, ny, nz;   /* GLOBAL interior extent; multiples of 4.  Rank r of `world`
+                              owns planes [r*nz/world, (r+1)*nz/world).                   */
+    float    c[5];         /* 1-D second-derivative weights c0..c4 (radius 4);
+                              oocz_default_config fills the 8th-order set (R1). */
+    int32_t  tb;           /* temporal blocking depth T >= 1 (PAPER.md:217 uses 12); halo h = 4T */
+    int32_t  block_planes; /* P: z-planes per block; multiple of 4, P >= 2h, P | nz/world     */
+    int32_t  rate[3];      /* bits per value for {U, UPREV, M}: 0 = raw fp32, 1..64 = fixed-rate
+                              ZFP ("the number of bits to preserve a value") */
+    int32_t  store;        /* OOCZ_STORE_HOST or OOCZ_STORE_DEVICE                             */
+    int32_t  slots;        /* staging slots per direction (>= 2); host store only             */
+    int32_t  profile;      /* 1: record per-stage CUDA events (oocz_get_events)               */
+    uint64_t device_bytes; /* device memory budget; 0 = whatever cudaMemGetInfo reports free  */
+} oocz_config;
+
+typedef struct {
+    uint64_t steps, sweeps;           /* totals since create                                */
+    uint64_t h2d_bytes, d2h_bytes;    /* host<->device bytes moved by oocz_step             */
+    uint64_t halo_bytes;              /* bytes sent to neighbour ranks by oocz_step          */
+    uint64_t kernel_launches;         /* this library's kernel launches in oocz_step         */
+    uint64_t device_bytes_used;       /* device memory held by the context                   */
+    uint64_t host_bytes_pinned;       /* pinned host memory held by the context              */
+    double   step_ms;                 /* host wall time spent inside oocz_step               */
+    /* per-stage device time summed over blocks (profile = 1 only), ms */
+    double   h2d_ms, decode_ms, stencil_ms, encode_ms, d2h_ms, copy_ms, halo_ms;
+} oocz_stats;
+
+/* one pipeline stage of one block (profile = 1), times relative to the
+ * first event of the last oocz_step call (SPEC.md:282-287 StageEvent) */
+enum { OOCZ_ST_H2D = 0, OOCZ_ST_DECODE = 1, OOCZ_ST_STENCIL = 2, OOCZ_ST_ENCODE = 3,
+       OOCZ_ST_D2H = 4, OOCZ_ST_HALO = 5 };
+typedef struct {
+    int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute, 2 = d2h, 3 = comm */
+    double   start_ms, end_ms;
+    uint64_t bytes;
+} oocz_event;
+
+typedef struct oocz_ctx oocz_ctx;
+
+/* ---------------------------------------------------------------- library */
+int32_t     oocz_abi_version(void);
+const char* oocz_status_string(oocz_status s);
+/* fills defaults: 8th-order c, tb = 4, rates 16, host store, 2 slots */
+void        oocz_default_config(oocz_config* cfg, int32_t nx, int32_t ny, int32_t nz);
+/* m_max(c) = 4 / (3 max_theta |S(theta)|), S = c0 + 2 sum c_k cos(k theta); 105/512 for
+ * the default c (R2).  oocz_set_field(M) rejects larger m with OOCZ_ECFL. */
+double      oocz_cfl_limit(const float c[5]);
+/* validate a config for (rank, world) without allocating; msg (may be NULL) receives
+ * the violated constraint, e.g. "P (36) < 2h (40)" */
+oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char* msg, size_t msg_len);
+
+/* ---------------------------------------------------------------- stepper
+ * Multi-GPU (world > 1): one process per GPU; z-slabs of nz/world planes; the
+ * 128-byte NCCL unique id comes from oocz_get_nccl_id on rank 0 and is
+ * broadcast by the caller (e.g. torch.distributed).  oocz_create and
+ * oocz_step are collective over the world. */
+oocz_status oocz_get_nccl_id(uint8_t id[128]);
+oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world,
+                        const uint8_t* nccl_id /* NULL if world == 1 */,
+                        int32_t device, oocz_ctx** out);
+/* Copy this rank's slab (count = nx*ny*nz/world floats) of field f into the
+ * store, compressing it on the GPU (the initial round trip).
+ * Rejects NaN/Inf (OOCZ_ENONFINITE) and, for OOCZ_M, m < 0 or m > m_max (OOCZ_ECFL). */
+oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const float* src, size_t count);
+oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const float* d_src, size_t count);
+/* Advance n steps: floor(n/T) sweeps of T steps, then one sweep of n mod T.
+ * Every sweep streams each z-block through decode -> T cone-limited stencil
+ * steps -> encode (Fig. 4), with copies, codec and stencil on
+ * separate CUDA streams (Fig. 5).  Blocks until done.
+ * Results depend on how n is split across calls (each sweep ends with a
+ * re-encode); R16. */
+oocz_status oocz_step(oocz_ctx* ctx, int64_t nsteps);
+/* Decode this rank's slab of field f into dst (count floats). */
+oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, float* dst, size_t count);
+oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float* d_dst, size_t count);
+oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out);
+/* In-process z-partitioned group on ONE device: `world` contexts (ranks 0..world-1)
+ * that exchange their halos with device copies instead of NCCL, stepped in
+ * lockstep by oocz_step_local_group.  Same engine, same halo protocol as the
+ * multi-process path; used to check on a single GPU that a partitioned run is
+ * bit-identical to world = 1.  Each context is destroyed with oocz_destroy. */
+oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t world, int32_t device, oocz_ctx** outs);
+oocz_status oocz_step_local_group(oocz_ctx* const* ctxs, int32_t world, int64_t nsteps);
+/* copy up to cap events of the last oocz_step (profile = 1) into evs; *n = total */
+oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, size_t cap, size_t* n);
+const char* oocz_last_error(const oocz_ctx* ctx);  /* owned by ctx; valid until the next call */
+void        oocz_destroy(oocz_ctx* ctx);
+
+/* ---------------------------------------------------------------- codec / kernels
+ * Stateless entry points used by the parity tests and the benchmark.  All
+ * pointers are device pointers, caller-owned; `stream` is a cudaStream_t (NULL
+ * = legacy default stream).  The call enqueues work and returns; errors in
+ * argument checking are returned synchronously. */
+
+/* exact compressed size: (nx/4)(ny/4)(nz/4) * 8 * rate bytes (fixed rate) */
+size_t      oocz_zfp_bytes(int32_t nx, int32_t ny, int32_t nz, int32_t rate);
+/* ZFP fixed-rate fp32 3-D encode: 4^3 blocks in order bz, by, bx; block b occupies
+ * words [rate*b, rate*b + rate) of d_out (little-endian uint64, bits LSB first).
+ * Format: DESIGN.md "Codec" (zfp 0.5.5 fixed-rate layout).  rate in 1..64. */
+oocz_status oocz_zfp_encode(const float* d_in, int32_t nx, int32_t ny, int32_t nz,
+                            int32_t rate, uint64_t* d_out, void* stream);
+oocz_status oocz_zfp_decode(const uint64_t* d_in, int32_t nx, int32_t ny, int32_t nz,
+                            int32_t rate, float* d_out, void* stream);
+/* nsteps in-core leapfrog steps on a whole nx*ny*nz grid with a zero Dirichlet ghost of
+ * depth 4: (u, uprev) <- (2u - uprev + m L(u), u), arithmetic order of DESIGN.md R5.
+ * On return d_u holds the newest level and d_uprev the one before. */
+oocz_status oocz_stencil_steps(float* d_u, float* d_uprev, const float* d_m,
+                               int32_t nx, int32_t ny, int32_t nz, const float c[5],
+                               int32_t nsteps, void* stream);
+/* one step restricted to planes [z0, z1) of an nz-plane array: d_uprev[z] <- u+ there,
+ * nothing else written; planes outside [zv0, zv1) of d_u are read as zero (ghost).
+ * This is the engine's cone-limited primitive (temporal blocking). */
+oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev, const float* d_m,
+                                     int32_t nx, int32_t ny, int32_t nz, const float c[5],
+                                     int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
+                                     void* stream);
+/* number of this library's kernels launched by this process so far */
+uint64_t    oocz_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOCZ_H */

@@ -1,0 +1,38 @@
+// common.cuh -- shared plumbing of liboocz.so (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstddef>
+
+#include "../../include/oocz.h"
+
+#if defined(__CUDACC__)
+#define OOCZ_HD __host__ __device__ __forceinline__
+#else
+#define OOCZ_HD inline
+#endif
+
+namespace oocz {
+
+// count of this library's kernel launches (oocz_kernel_launch_count)
+void note_launches(uint64_t n);
+
+// launch-configuration helpers
+constexpr int kNumSMs = 148;  // B200
+
+inline const char* cuda_str(cudaError_t e) { return cudaGetErrorString(e); }
+
+// internal launchers (stream-ordered, no synchronisation)
+cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
+                              uint64_t* out, cudaStream_t s);
+cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int rate,
+                              float* out, cudaStream_t s);
+// one cone-limited step: planes [z0, z1) of uprev <- u+; u planes outside
+// [zv0, zv1) read as zero
+cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m,
+                                int nx, int ny, int nz, const float c[5],
+                                int z0, int z1, int zv0, int zv1, cudaStream_t s);
+// checks used by set_field: flags[0] |= non-finite seen; flags[1] = max(bits of m) (m >= 0)
+cudaError_t launch_scan_field(const float* in, size_t n, unsigned int* flags, cudaStream_t s);
+
+}  // namespace oocz

@@ -1,0 +1,841 @@
+// engine.cu -- out-of-core sweep engine behind the C ABI (include/oocz.h).
+//
+// The paper's method (PAPER.md:112-113 Sec. III, :130-179 Sec. V):
+//  * the datasets are split along z into blocks of P planes that are streamed
+//    host -> GPU -> host; each residency advances T steps (temporal blocking,
+//    halo h = 4T);
+//  * contiguous blocks share their common region C_i = [(i+1)P-h, (i+1)P+h) on
+//    the GPU (region sharing, Fig. 3), so each plane crosses the host link once
+//    per direction per sweep;
+//  * remainders and common regions are compressed separately (Fig. 4): with
+//    h a multiple of 4, every region boundary is a ZFP block-row boundary, so
+//    the per-field store is one fixed-rate stream of 4-plane block-rows and any
+//    region is one contiguous byte range.  Block i reads [iP+h, (i+1)P+h)
+//    (block 0: [0, P+h)) and writes back its own planes [iP, (i+1)P), which
+//    are exactly "the i-th remainder and the (i-1)-th common region" halves it
+//    owns (reading R13);
+//  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
+//  * copies, codec and stencil overlap on three CUDA streams (Fig. 5).
+//
+// Device-side data layout (per rank):
+//   slab[f]   : (P + 2h) planes of nx*ny fp32, slab plane 0 = rank plane iP - h
+//   ccopy[f]  : 2h planes, time-t copy of C_i (u, u-, m)
+//   in[slot]  : H2D staging of one read unit (3 fields), `slots` deep
+//   out[slot] : D2H staging of one write unit (2 read-write fields)
+//   store[f]  : pinned host (OOCZ_STORE_HOST) or device (OOCZ_STORE_DEVICE)
+//               stream of S/4 block-rows
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdarg>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "halo.h"
+
+namespace oocz {
+
+static std::atomic<uint64_t> g_launches{0};
+void note_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+namespace {
+
+__global__ void scan_field_kernel(const float* __restrict__ in, size_t n, unsigned int* flags)
+{
+    unsigned int nonfinite = 0, neg = 0, mx = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned int b = __float_as_uint(in[i]);
+        const unsigned int a = b & 0x7fffffffu;
+        nonfinite |= a >= 0x7f800000u;
+        neg |= (b >> 31) && a;                // negative and not -0.0
+        mx = max(mx, a);
+    }
+    nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+    neg = __reduce_or_sync(0xffffffffu, neg);
+    mx = __reduce_max_sync(0xffffffffu, mx);
+    if ((threadIdx.x & 31) == 0) {
+        if (nonfinite) atomicOr(&flags[0], 1u);
+        if (neg) atomicOr(&flags[0], 2u);
+        atomicMax(&flags[1], mx);
+    }
+}
+
+}  // namespace
+
+cudaError_t launch_scan_field(const float* in, size_t n, unsigned int* flags, cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    size_t blocks = std::min<size_t>((n + 255) / 256, (size_t)kNumSMs * 8);
+    scan_field_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, n, flags);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace oocz
+
+using namespace oocz;
+
+// ------------------------------------------------------------------ context
+struct Geom {
+    int rd0, rd1;      // read unit, rank-local planes
+    int own0, own1;    // write unit
+    int slab0;         // rank-local plane of slab plane 0 (= iP - h)
+    int vlo, vhi;      // slab planes holding data (others read as zero ghost)
+};
+
+struct oocz_ctx {
+    oocz_config cfg{};
+    int rank = 0, world = 1, device = 0;
+    int S = 0, P = 0, D = 0, h = 0, T = 0, L = 0;   // slab planes, block, blocks, halo, depth, slab len
+    int nx = 0, ny = 0;
+    size_t plane_elems = 0;
+    size_t row_bytes[3] = {0, 0, 0};       // bytes per 4-plane block-row in the store
+    bool field_set[3] = {false, false, false};
+    bool poisoned = false;
+    std::string err;
+
+    std::vector<Geom> geom;
+    // device buffers
+    float* slab[3] = {nullptr, nullptr, nullptr};
+    float* ccopy[3] = {nullptr, nullptr, nullptr};
+    std::vector<uint8_t*> in_slot, out_slot;
+    size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
+    size_t in_slot_bytes = 0, out_slot_bytes = 0;
+    unsigned int* d_flags = nullptr;
+    // store
+    uint8_t* store[3] = {nullptr, nullptr, nullptr};
+    size_t store_bytes[3] = {0, 0, 0};
+    // streams / events
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written;
+    long long seq = 0;                      // global block sequence number
+    // halo exchange (world > 1)
+    HaloComm* halo = nullptr;
+    // profiling
+    struct Prof { int sweep, block, stage, lane; cudaEvent_t a, b; uint64_t bytes; };
+    std::vector<Prof> prof;
+    std::vector<oocz_event> events;
+    oocz_stats stats{};
+};
+
+namespace {
+
+oocz_status fail(oocz_ctx* c, oocz_status s, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+oocz_status fail(oocz_ctx* c, oocz_status s, const char* fmt, ...)
+{
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    if (c) {
+        c->err = buf;
+        if (s == OOCZ_ECUDA || s == OOCZ_ENCCL) c->poisoned = true;
+    }
+    return s;
+}
+
+#define CK(call)                                                                        \
+    do {                                                                                \
+        cudaError_t e_ = (call);                                                        \
+        if (e_ != cudaSuccess)                                                          \
+            return fail(ctx, OOCZ_ECUDA, "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), \
+                        __FILE__, __LINE__);                                            \
+    } while (0)
+
+size_t row_bytes_for(int nx, int ny, int rate)
+{
+    return rate == 0 ? (size_t)nx * ny * 4 * sizeof(float) : (size_t)(nx / 4) * (ny / 4) * 8u * (size_t)rate;
+}
+
+double cfl_limit(const float c[5])
+{
+    // m_max = 4 / (3 max_theta |S(theta)|), S = c0 + 2 sum c_k cos(k theta) (R2)
+    double mx = 0.0;
+    const int N = 20000;
+    for (int i = 0; i <= N; i++) {
+        const double th = M_PI * i / N;
+        double s = c[0];
+        for (int k = 1; k <= 4; k++) s += 2.0 * c[k] * std::cos(k * th);
+        mx = std::max(mx, std::fabs(s));
+    }
+    return mx > 0 ? 4.0 / (3.0 * mx) : INFINITY;
+}
+
+// one 4-aligned plane range of a field's store as a byte range
+inline size_t rows_off(const oocz_ctx* c, int f, int plane) { return (size_t)(plane / 4) * c->row_bytes[f]; }
+
+cudaError_t encode_or_copy(oocz_ctx* c, int f, const float* src, int nplanes, uint8_t* dst, cudaStream_t s)
+{
+    const int rate = c->cfg.rate[f];
+    if (rate == 0)
+        return cudaMemcpyAsync(dst, src, (size_t)nplanes * c->plane_elems * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s);
+    return launch_zfp_encode(src, c->nx, c->ny, nplanes, rate, reinterpret_cast<uint64_t*>(dst), s);
+}
+
+cudaError_t decode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, float* dst, cudaStream_t s)
+{
+    const int rate = c->cfg.rate[f];
+    if (rate == 0)
+        return cudaMemcpyAsync(dst, src, (size_t)nplanes * c->plane_elems * sizeof(float),
+                               cudaMemcpyDeviceToDevice, s);
+    return launch_zfp_decode(reinterpret_cast<const uint64_t*>(src), c->nx, c->ny, nplanes, rate, dst, s);
+}
+
+void prof_begin(oocz_ctx* c, int sweep, int block, int stage, int lane, cudaStream_t s, uint64_t bytes)
+{
+    if (!c->cfg.profile) return;
+    oocz_ctx::Prof p{sweep, block, stage, lane, nullptr, nullptr, bytes};
+    cudaEventCreate(&p.a);
+    cudaEventCreate(&p.b);
+    cudaEventRecord(p.a, s);
+    c->prof.push_back(p);
+}
+void prof_end(oocz_ctx* c, cudaStream_t s)
+{
+    if (!c->cfg.profile) return;
+    cudaEventRecord(c->prof.back().b, s);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ library
+extern "C" int32_t oocz_abi_version(void) { return OOCZ_ABI_VERSION; }
+
+extern "C" uint64_t oocz_kernel_launch_count(void) { return g_launches.load(); }
+
+extern "C" const char* oocz_status_string(oocz_status s)
+{
+    switch (s) {
+        case OOCZ_OK: return "ok";
+        case OOCZ_EINVAL: return "invalid argument";
+        case OOCZ_EALIGN: return "extent not a multiple of 4";
+        case OOCZ_ECFL: return "stability (CFL) bound violated";
+        case OOCZ_ECAPACITY: return "memory budget too small";
+        case OOCZ_ENONFINITE: return "non-finite value in field";
+        case OOCZ_ESTATE: return "invalid state";
+        case OOCZ_ECUDA: return "CUDA error";
+        case OOCZ_ENCCL: return "NCCL error";
+    }
+    return "unknown status";
+}
+
+extern "C" void oocz_default_config(oocz_config* cfg, int32_t nx, int32_t ny, int32_t nz)
+{
+    std::memset(cfg, 0, sizeof *cfg);
+    cfg->nx = nx; cfg->ny = ny; cfg->nz = nz;
+    cfg->c[0] = (float)(-205.0 / 72.0);
+    cfg->c[1] = (float)(8.0 / 5.0);
+    cfg->c[2] = (float)(-1.0 / 5.0);
+    cfg->c[3] = (float)(8.0 / 315.0);
+    cfg->c[4] = (float)(-1.0 / 560.0);
+    cfg->tb = 4;
+    cfg->block_planes = nz;
+    cfg->rate[0] = cfg->rate[1] = cfg->rate[2] = 16;
+    cfg->store = OOCZ_STORE_HOST;
+    cfg->slots = 2;
+}
+
+extern "C" double oocz_cfl_limit(const float c[5]) { return c ? cfl_limit(c) : 0.0; }
+
+extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char* msg, size_t msg_len)
+{
+    char buf[256] = "";
+    oocz_status st = OOCZ_OK;
+#define BAD(code, ...) do { snprintf(buf, sizeof buf, __VA_ARGS__); st = code; goto done; } while (0)
+    if (!cfg) BAD(OOCZ_EINVAL, "null config");
+    if (world < 1) BAD(OOCZ_EINVAL, "world (%d) < 1", world);
+    if (cfg->nx <= 0 || cfg->ny <= 0 || cfg->nz <= 0)
+        BAD(OOCZ_EINVAL, "extents must be positive (%d, %d, %d)", cfg->nx, cfg->ny, cfg->nz);
+    if (cfg->nx % 4 || cfg->ny % 4 || cfg->nz % 4)
+        BAD(OOCZ_EALIGN, "nx, ny, nz (%d, %d, %d) must be multiples of 4", cfg->nx, cfg->ny, cfg->nz);
+    if (cfg->nz % world) BAD(OOCZ_EINVAL, "world (%d) does not divide nz (%d)", world, cfg->nz);
+    {
+        const int S = cfg->nz / world;
+        if (S % 4) BAD(OOCZ_EALIGN, "nz/world (%d) must be a multiple of 4", S);
+        if (cfg->tb < 1) BAD(OOCZ_EINVAL, "tb (%d) < 1", cfg->tb);
+        const int h = 4 * cfg->tb;
+        const int P = cfg->block_planes;
+        if (P <= 0 || P % 4) BAD(OOCZ_EALIGN, "P (%d) must be a positive multiple of 4", P);
+        if (P < 2 * h) BAD(OOCZ_EINVAL, "P (%d) < 2h (%d)", P, 2 * h);
+        if (S % P) BAD(OOCZ_EINVAL, "P (%d) does not divide nz/world (%d)", P, S);
+    }
+    for (int f = 0; f < 3; f++)
+        if (cfg->rate[f] < 0 || cfg->rate[f] > 64) BAD(OOCZ_EINVAL, "rate[%d] (%d) outside [0, 64]", f, cfg->rate[f]);
+    if (cfg->store != OOCZ_STORE_HOST && cfg->store != OOCZ_STORE_DEVICE)
+        BAD(OOCZ_EINVAL, "store (%d) unknown", cfg->store);
+    if (cfg->store == OOCZ_STORE_HOST && cfg->slots < 2) BAD(OOCZ_EINVAL, "slots (%d) < 2", cfg->slots);
+    for (int k = 0; k < 5; k++)
+        if (!std::isfinite(cfg->c[k])) BAD(OOCZ_EINVAL, "c[%d] not finite", k);
+#undef BAD
+done:
+    if (msg && msg_len) snprintf(msg, msg_len, "%s", buf);
+    return st;
+}
+
+extern "C" oocz_status oocz_get_nccl_id(uint8_t id[128])
+{
+    return halo_get_unique_id(id) ? OOCZ_OK : OOCZ_ENCCL;
+}
+
+static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                               int32_t device, HaloComm* preset_halo, oocz_ctx** out)
+{
+    if (!out) return OOCZ_EINVAL;
+    *out = nullptr;
+    char msg[256];
+    oocz_status st = oocz_validate(cfg, world, msg, sizeof msg);
+    if (st != OOCZ_OK) {
+        fprintf(stderr, "oocz_create: %s\n", msg);
+        return st;
+    }
+    if (rank < 0 || rank >= world || (world > 1 && !nccl_id && !preset_halo)) return OOCZ_EINVAL;
+    oocz_ctx* ctx = new oocz_ctx;
+    ctx->cfg = *cfg;
+    ctx->rank = rank; ctx->world = world; ctx->device = device;
+    ctx->nx = cfg->nx; ctx->ny = cfg->ny;
+    ctx->S = cfg->nz / world;
+    ctx->T = cfg->tb; ctx->h = 4 * cfg->tb; ctx->P = cfg->block_planes;
+    ctx->D = ctx->S / ctx->P;
+    ctx->L = ctx->P + 2 * ctx->h;
+    ctx->plane_elems = (size_t)cfg->nx * cfg->ny;
+    for (int f = 0; f < 3; f++) ctx->row_bytes[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f]);
+
+    auto cleanup_fail = [&](oocz_status s) { oocz_destroy(ctx); return s; };
+#define CKC(call)                                                                                 \
+    do {                                                                                          \
+        cudaError_t e_ = (call);                                                                  \
+        if (e_ != cudaSuccess) {                                                                  \
+            fprintf(stderr, "oocz_create: %s: %s\n", #call, cudaGetErrorString(e_));              \
+            return cleanup_fail(e_ == cudaErrorMemoryAllocation ? OOCZ_ECAPACITY : OOCZ_ECUDA);   \
+        }                                                                                         \
+    } while (0)
+
+    CKC(cudaSetDevice(device));
+    // block geometry (rank-local planes)
+    const int S = ctx->S, P = ctx->P, h = ctx->h, D = ctx->D;
+    const bool has_up = rank > 0, has_down = rank < world - 1;
+    for (int i = 0; i < D; i++) {
+        Geom g;
+        g.slab0 = i * P - h;
+        g.rd0 = i == 0 ? 0 : i * P + h;
+        g.rd1 = std::min((i + 1) * P + h, S);
+        g.own0 = i * P;
+        g.own1 = (i + 1) * P;
+        const int lo = (i == 0 && !has_up) ? 0 : i * P - h;
+        const int hi = (i == D - 1 && !has_down) ? S : (i + 1) * P + h;
+        g.vlo = lo - g.slab0;
+        g.vhi = hi - g.slab0;
+        ctx->geom.push_back(g);
+    }
+    // memory plan and budget check
+    const size_t pb = ctx->plane_elems * sizeof(float);
+    size_t need = 3 * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
+    const bool host = cfg->store == OOCZ_STORE_HOST;
+    const int rd_max_planes = std::min(P + h, S);
+    if (host) {
+        for (int f = 0; f < 3; f++) {
+            ctx->in_off[f] = ctx->in_slot_bytes;
+            ctx->in_slot_bytes += (size_t)(rd_max_planes / 4) * ctx->row_bytes[f];
+        }
+        for (int f = 0; f < 2; f++) {
+            ctx->out_off[f] = ctx->out_slot_bytes;
+            ctx->out_slot_bytes += (size_t)(P / 4) * ctx->row_bytes[f];
+        }
+        need += (size_t)cfg->slots * (ctx->in_slot_bytes + ctx->out_slot_bytes);
+    }
+    for (int f = 0; f < 3; f++) ctx->store_bytes[f] = (size_t)(S / 4) * ctx->row_bytes[f];
+    if (!host) need += ctx->store_bytes[0] + ctx->store_bytes[1] + ctx->store_bytes[2];
+    if (world > 1) need += halo_device_bytes(ctx->plane_elems, h, cfg->rate, ctx->row_bytes);
+    {
+        size_t fr = 0, tot = 0;
+        CKC(cudaMemGetInfo(&fr, &tot));
+        const size_t budget = cfg->device_bytes ? cfg->device_bytes : fr;
+        if (need > budget) {
+            fprintf(stderr, "oocz_create: device memory %zu B needed > budget %zu B\n", need, budget);
+            return cleanup_fail(OOCZ_ECAPACITY);
+        }
+    }
+    for (int f = 0; f < 3; f++) {
+        CKC(cudaMalloc(&ctx->slab[f], (size_t)ctx->L * pb));
+        CKC(cudaMemset(ctx->slab[f], 0, (size_t)ctx->L * pb));
+        CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
+    }
+    CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
+    if (host) {
+        for (int s = 0; s < cfg->slots; s++) {
+            uint8_t* a = nullptr;
+            uint8_t* b = nullptr;
+            CKC(cudaMalloc(&a, ctx->in_slot_bytes));
+            CKC(cudaMalloc(&b, ctx->out_slot_bytes));
+            ctx->in_slot.push_back(a);
+            ctx->out_slot.push_back(b);
+        }
+        for (int f = 0; f < 3; f++) {
+            CKC(cudaHostAlloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1), cudaHostAllocDefault));
+            ctx->stats.host_bytes_pinned += ctx->store_bytes[f];
+        }
+    } else {
+        for (int f = 0; f < 3; f++) CKC(cudaMalloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1)));
+    }
+    ctx->stats.device_bytes_used = need;
+    CKC(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    const int nslots = host ? cfg->slots : 1;
+    auto mk = [&](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
+        for (int k = 0; k < n; k++) {
+            cudaEvent_t e;
+            cudaError_t r = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+            if (r != cudaSuccess) return r;
+            v.push_back(e);
+        }
+        return cudaSuccess;
+    };
+    CKC(mk(ctx->ev_in_ready, nslots));
+    CKC(mk(ctx->ev_in_free, nslots));
+    CKC(mk(ctx->ev_out_ready, nslots));
+    CKC(mk(ctx->ev_out_free, nslots));
+    CKC(mk(ctx->ev_written, D));
+    if (preset_halo) {
+        ctx->halo = preset_halo;
+    } else if (world > 1) {
+        std::string herr;
+        ctx->halo = halo_create(rank, world, nccl_id, device, ctx->plane_elems, h, cfg->rate,
+                                ctx->row_bytes, &herr);
+        if (!ctx->halo) {
+            fprintf(stderr, "oocz_create: %s\n", herr.c_str());
+            return cleanup_fail(OOCZ_ENCCL);
+        }
+    }
+#undef CKC
+    *out = ctx;
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                                   int32_t device, oocz_ctx** out)
+{
+    return create_impl(cfg, rank, world, nccl_id, device, nullptr, out);
+}
+
+extern "C" oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t world, int32_t device,
+                                               oocz_ctx** outs)
+{
+    if (!outs || world < 1) return OOCZ_EINVAL;
+    char msg[256];
+    oocz_status st = oocz_validate(cfg, world, msg, sizeof msg);
+    if (st != OOCZ_OK) {
+        fprintf(stderr, "oocz_create_local_group: %s\n", msg);
+        return st;
+    }
+    if (cudaSetDevice(device) != cudaSuccess) return OOCZ_ECUDA;
+    size_t rb[3];
+    for (int f = 0; f < 3; f++) rb[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f]);
+    HaloComm** hs = nullptr;
+    if (world > 1) {
+        std::string herr;
+        hs = halo_create_local_group(world, device, (size_t)cfg->nx * cfg->ny, 4 * cfg->tb, cfg->rate, rb, &herr);
+        if (!hs) {
+            fprintf(stderr, "oocz_create_local_group: %s\n", herr.c_str());
+            return OOCZ_ECAPACITY;
+        }
+    }
+    std::vector<HaloComm*> halos(world, nullptr);
+    for (int r = 0; r < world && hs; r++) halos[r] = hs[r];
+    for (int r = 0; r < world; r++) {
+        st = create_impl(cfg, r, world, nullptr, device, halos[r], &outs[r]);
+        if (st != OOCZ_OK) {
+            for (int k = 0; k < r; k++) { oocz_destroy(outs[k]); outs[k] = nullptr; }
+            for (int k = r; k < world; k++) if (halos[k]) halo_destroy(halos[k]);
+            return st;
+        }
+        halos[r] = nullptr;   // owned by the context now
+    }
+    return OOCZ_OK;
+}
+
+extern "C" void oocz_destroy(oocz_ctx* ctx)
+{
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d);
+    if (ctx->s_comp) cudaStreamSynchronize(ctx->s_comp);
+    if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h);
+    if (ctx->halo) halo_destroy(ctx->halo);
+    for (int f = 0; f < 3; f++) {
+        cudaFree(ctx->slab[f]);
+        cudaFree(ctx->ccopy[f]);
+        if (ctx->cfg.store == OOCZ_STORE_HOST) cudaFreeHost(ctx->store[f]);
+        else cudaFree(ctx->store[f]);
+    }
+    for (auto p : ctx->in_slot) cudaFree(p);
+    for (auto p : ctx->out_slot) cudaFree(p);
+    cudaFree(ctx->d_flags);
+    for (auto* v : {&ctx->ev_in_ready, &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free, &ctx->ev_written})
+        for (auto e : *v) cudaEventDestroy(e);
+    for (auto& p : ctx->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
+    if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
+    if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
+    delete ctx;
+}
+
+extern "C" const char* oocz_last_error(const oocz_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+extern "C" oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out)
+{
+    if (!ctx || !out) return OOCZ_EINVAL;
+    *out = ctx->stats;
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, size_t cap, size_t* n)
+{
+    if (!ctx || !n) return OOCZ_EINVAL;
+    *n = ctx->events.size();
+    if (evs) std::memcpy(evs, ctx->events.data(), std::min(cap, ctx->events.size()) * sizeof(oocz_event));
+    return OOCZ_OK;
+}
+
+// ------------------------------------------------------------------ set / get
+static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src, size_t count, bool on_device)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+    if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
+    if (!src && count) return fail(ctx, OOCZ_EINVAL, "null source");
+    const size_t want = ctx->plane_elems * (size_t)ctx->S;
+    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
+    CK(cudaSetDevice(ctx->device));
+    ctx->field_set[field] = false;
+    cudaStream_t s = ctx->s_comp;
+    const int chunk = ctx->P;                       // planes per pass, <= slab capacity
+    const double mmax = cfl_limit(ctx->cfg.c);
+    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
+    CK(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(unsigned int), s));
+    for (int z = 0; z < ctx->S; z += chunk) {
+        const int np = std::min(chunk, ctx->S - z);
+        const size_t n = (size_t)np * ctx->plane_elems;
+        float* buf = ctx->slab[field];
+        CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->plane_elems, n * sizeof(float),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
+        CK(launch_scan_field(buf, n, ctx->d_flags, s));
+        const size_t off = rows_off(ctx, field, z);
+        const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
+        if (host) {
+            uint8_t* dev = ctx->in_slot[0];         // device staging of the encoded rows
+            CK(encode_or_copy(ctx, field, buf, np, dev, s));
+            CK(cudaMemcpyAsync(ctx->store[field] + off, dev, bytes, cudaMemcpyDeviceToHost, s));
+        } else {
+            CK(encode_or_copy(ctx, field, buf, np, ctx->store[field] + off, s));
+        }
+    }
+    unsigned int flags[2] = {0, 0};
+    CK(cudaMemcpyAsync(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (flags[0] & 1u) return fail(ctx, OOCZ_ENONFINITE, "field %d contains NaN or Inf", field);
+    if (field == OOCZ_M) {
+        float mx;
+        std::memcpy(&mx, &flags[1], sizeof mx);
+        if (flags[0] & 2u) return fail(ctx, OOCZ_ECFL, "m has negative values");
+        if ((double)mx > mmax)
+            return fail(ctx, OOCZ_ECFL, "max m (%.9g) > m_max(c) (%.9g)", (double)mx, mmax);
+    }
+    ctx->field_set[field] = true;
+    if (field != OOCZ_M && ctx->halo) {
+        std::string herr;
+        if (!halo_capture_store(ctx->halo, field, ctx->store[field], host, ctx->S, ctx->row_bytes[field], s, &herr) ||
+            cudaStreamSynchronize(s) != cudaSuccess)
+            return fail(ctx, OOCZ_ENCCL, "halo capture: %s", herr.c_str());
+    }
+    if (field == OOCZ_M && ctx->halo) {
+        // m halos are read-only: exchange them once (compressed form, reading R20)
+        std::string herr;
+        if (!halo_exchange_m(ctx->halo, ctx->store[OOCZ_M], host, ctx->S, ctx->row_bytes[OOCZ_M], s, &herr))
+            return fail(ctx, OOCZ_ENCCL, "m halo exchange: %s", herr.c_str());
+    }
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const float* src, size_t count)
+{
+    return set_field_impl(ctx, field, src, count, false);
+}
+extern "C" oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const float* d_src, size_t count)
+{
+    return set_field_impl(ctx, field, d_src, count, true);
+}
+
+static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, float* dst, size_t count, bool on_device)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+    if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
+    if (!ctx->field_set[field]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", field);
+    const size_t want = ctx->plane_elems * (size_t)ctx->S;
+    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
+    if (!dst && count) return fail(ctx, OOCZ_EINVAL, "null destination");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->s_comp;
+    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
+    const int chunk = ctx->P;
+    for (int z = 0; z < ctx->S; z += chunk) {
+        const int np = std::min(chunk, ctx->S - z);
+        const size_t n = (size_t)np * ctx->plane_elems;
+        const size_t off = rows_off(ctx, field, z);
+        const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
+        float* buf = ctx->slab[field];
+        if (host) {
+            uint8_t* dev = ctx->in_slot[0];
+            CK(cudaMemcpyAsync(dev, ctx->store[field] + off, bytes, cudaMemcpyHostToDevice, s));
+            CK(decode_or_copy(ctx, field, dev, np, buf, s));
+        } else {
+            CK(decode_or_copy(ctx, field, ctx->store[field] + off, np, buf, s));
+        }
+        CK(cudaMemcpyAsync(dst + (size_t)z * ctx->plane_elems, buf, n * sizeof(float),
+                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaStreamSynchronize(s));
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, float* dst, size_t count)
+{
+    return get_field_impl(ctx, field, dst, count, false);
+}
+extern "C" oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float* d_dst, size_t count)
+{
+    return get_field_impl(ctx, field, d_dst, count, true);
+}
+
+// ------------------------------------------------------------------ step
+// Enqueue one block of one sweep (ts steps).
+static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
+{
+    const Geom& g = ctx->geom[i];
+    const int h = ctx->h, P = ctx->P, D = ctx->D;
+    const size_t pb = ctx->plane_elems * sizeof(float);
+    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
+    const int nslots = (int)ctx->ev_in_ready.size();
+    const int slot = (int)(ctx->seq % nslots);
+    const int rd_planes = g.rd1 - g.rd0;
+    const uint8_t* src[3];
+    cudaStream_t sc = ctx->s_comp;
+
+    // ---- (a2) H2D of the read unit (u, u-, m) into a staging slot
+    if (host) {
+        cudaStream_t sh = ctx->s_h2d;
+        CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
+        // rows written back by blocks i and i+1 of the previous sweep must have landed
+        CK(cudaStreamWaitEvent(sh, ctx->ev_written[std::min(i + 1, D - 1)], 0));
+        uint64_t bytes = 0;
+        for (int f = 0; f < 3; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
+        prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
+        for (int f = 0; f < 3; f++) {
+            const size_t nbytes = (size_t)(rd_planes / 4) * ctx->row_bytes[f];
+            CK(cudaMemcpyAsync(ctx->in_slot[slot] + ctx->in_off[f], ctx->store[f] + rows_off(ctx, f, g.rd0),
+                               nbytes, cudaMemcpyHostToDevice, sh));
+            src[f] = ctx->in_slot[slot] + ctx->in_off[f];
+        }
+        prof_end(ctx, sh);
+        ctx->stats.h2d_bytes += bytes;
+        CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
+        CK(cudaStreamWaitEvent(sc, ctx->ev_in_ready[slot], 0));
+    } else {
+        for (int f = 0; f < 3; f++) src[f] = ctx->store[f] + rows_off(ctx, f, g.rd0);
+    }
+
+    // ---- (a4) slab assembly: time-t C_{i-1} from the previous block, halo from a neighbour rank
+    if (i > 0) {
+        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 1, sc, 0);
+        for (int f = 0; f < 3; f++)
+            CK(cudaMemcpyAsync(ctx->slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sc));
+        prof_end(ctx, sc);
+    }
+    if (ctx->halo) {
+        std::string herr;
+        if (!halo_insert(ctx->halo, i == 0, i == D - 1, ctx->slab, g.slab0, ctx->S, ctx->nx, ctx->ny, sc, &herr))
+            return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
+    }
+    // ---- (a3) decode the read unit into the slab
+    {
+        uint64_t bytes = 0;
+        for (int f = 0; f < 3; f++) bytes += (uint64_t)rd_planes * pb;
+        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 1, sc, bytes);
+        for (int f = 0; f < 3; f++)
+            CK(decode_or_copy(ctx, f, src[f], rd_planes, ctx->slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sc));
+        prof_end(ctx, sc);
+    }
+    if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sc));
+    // keep the time-t C_i for block i+1 (reading R14)
+    if (i < D - 1)
+        for (int f = 0; f < 3; f++)
+            CK(cudaMemcpyAsync(ctx->ccopy[f], ctx->slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
+                               cudaMemcpyDeviceToDevice, sc));
+
+    // ---- (a5) T cone-limited steps, in place, roles swapping
+    float* cu = ctx->slab[OOCZ_U];
+    float* cp = ctx->slab[OOCZ_UPREV];
+    prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 0);
+    for (int s = 1; s <= ts; s++) {
+        const int z0 = std::max(4 * s, g.vlo);
+        const int z1 = std::min(ctx->L - 4 * s, g.vhi);
+        CK(launch_stencil_step(cu, cp, ctx->slab[OOCZ_M], ctx->nx, ctx->ny, ctx->L, ctx->cfg.c, z0, z1, g.vlo,
+                               g.vhi, sc));
+        std::swap(cu, cp);
+    }
+    prof_end(ctx, sc);
+
+    // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-
+    const float* own[2] = {cu + (size_t)h * ctx->plane_elems, cp + (size_t)h * ctx->plane_elems};
+    if (ctx->halo) {
+        std::string herr;
+        if (!halo_capture(ctx->halo, i == 0, i == D - 1, own, P, ctx->nx, ctx->ny, sc, &herr))
+            return fail(ctx, OOCZ_ENCCL, "halo capture: %s", herr.c_str());
+    }
+    if (host) {
+        CK(cudaStreamWaitEvent(sc, ctx->ev_out_free[slot], 0));
+        prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, 0);
+        for (int f = 0; f < 2; f++) CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], sc));
+        prof_end(ctx, sc);
+        CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
+        // ---- (a7) D2H into the store, in place
+        cudaStream_t sd = ctx->s_d2h;
+        CK(cudaStreamWaitEvent(sd, ctx->ev_out_ready[slot], 0));
+        uint64_t bytes = 0;
+        for (int f = 0; f < 2; f++) bytes += (uint64_t)(P / 4) * ctx->row_bytes[f];
+        prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, sd, bytes);
+        for (int f = 0; f < 2; f++)
+            CK(cudaMemcpyAsync(ctx->store[f] + rows_off(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
+                               (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, sd));
+        prof_end(ctx, sd);
+        ctx->stats.d2h_bytes += bytes;
+        CK(cudaEventRecord(ctx->ev_out_free[slot], sd));
+        CK(cudaEventRecord(ctx->ev_written[i], sd));
+    } else {
+        prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, 0);
+        for (int f = 0; f < 2; f++)
+            CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), sc));
+        prof_end(ctx, sc);
+    }
+    ctx->seq++;
+    return OOCZ_OK;
+}
+
+static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+    if (nsteps < 0) return fail(ctx, OOCZ_EINVAL, "nsteps (%lld) < 0", (long long)nsteps);
+    for (int f = 0; f < 3; f++)
+        if (!ctx->field_set[f]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", f);
+    CK(cudaSetDevice(ctx->device));
+    for (auto& p : ctx->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    ctx->prof.clear();
+    ctx->events.clear();
+    *base = nullptr;
+    if (ctx->cfg.profile) {
+        CK(cudaEventCreate(base));
+        CK(cudaEventRecord(*base, ctx->s_h2d));
+        CK(cudaStreamWaitEvent(ctx->s_comp, *base, 0));
+        CK(cudaStreamWaitEvent(ctx->s_d2h, *base, 0));
+    }
+    return OOCZ_OK;
+}
+
+static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
+{
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaStreamSynchronize(ctx->s_h2d));
+    CK(cudaStreamSynchronize(ctx->s_comp));
+    CK(cudaStreamSynchronize(ctx->s_d2h));
+    ctx->stats.steps += (uint64_t)nsteps;
+    ctx->stats.halo_bytes = halo_bytes_sent(ctx->halo);
+    if (ctx->cfg.profile && base) {
+        for (auto& p : ctx->prof) {
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, base, p.a));
+            CK(cudaEventElapsedTime(&b, base, p.b));
+            ctx->events.push_back(oocz_event{p.sweep, p.block, p.stage, p.lane, a, b, p.bytes});
+            const double d = b - a;
+            switch (p.stage) {
+                case OOCZ_ST_H2D: ctx->stats.h2d_ms += d; break;
+                case OOCZ_ST_DECODE: ctx->stats.decode_ms += d; break;
+                case OOCZ_ST_STENCIL: ctx->stats.stencil_ms += d; break;
+                case OOCZ_ST_ENCODE: ctx->stats.encode_ms += d; break;
+                case OOCZ_ST_D2H: ctx->stats.d2h_ms += d; break;
+                case OOCZ_ST_HALO: ctx->stats.halo_ms += d; break;
+            }
+        }
+        cudaEventDestroy(base);
+    }
+    return OOCZ_OK;
+}
+
+// Enqueue all sweeps of every context in lockstep (one context unless this is
+// an in-process local group), then wait.
+static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
+{
+    if (!ctxs || n < 1) return OOCZ_EINVAL;
+    const auto t0 = std::chrono::steady_clock::now();
+    const uint64_t launches0 = g_launches.load();
+    std::vector<cudaEvent_t> base(n, nullptr);
+    for (int r = 0; r < n; r++) {
+        oocz_status st = step_begin(ctxs[r], nsteps, &base[r]);
+        if (st != OOCZ_OK) return st;
+    }
+    const int T = ctxs[0]->T;
+    int64_t done = 0;
+    int sweep = 0;
+    while (done < nsteps) {
+        const int ts = (int)std::min<int64_t>(T, nsteps - done);
+        for (int r = 0; r < n; r++) {
+            oocz_ctx* ctx = ctxs[r];
+            if (ctx->halo) {
+                std::string herr;
+                CK(cudaSetDevice(ctx->device));
+                if (!halo_sweep_begin(ctx->halo, ctx->s_comp, &herr))
+                    return fail(ctx, OOCZ_ENCCL, "halo exchange: %s", herr.c_str());
+            }
+        }
+        for (int r = 0; r < n; r++) {
+            for (int i = 0; i < ctxs[r]->D; i++) {
+                oocz_status st = enqueue_block(ctxs[r], sweep, i, ts);
+                if (st != OOCZ_OK) return st;
+            }
+            ctxs[r]->stats.sweeps++;
+        }
+        done += ts;
+        sweep++;
+    }
+    for (int r = 0; r < n; r++) {
+        oocz_status st = step_end(ctxs[r], nsteps, base[r]);
+        if (st != OOCZ_OK) return st;
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    const uint64_t launched = g_launches.load() - launches0;
+    for (int r = 0; r < n; r++) {
+        ctxs[r]->stats.step_ms += ms;
+        ctxs[r]->stats.kernel_launches += launched;
+    }
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_step(oocz_ctx* ctx, int64_t nsteps)
+{
+    return step_group(&ctx, 1, nsteps);
+}
+
+extern "C" oocz_status oocz_step_local_group(oocz_ctx* const* ctxs, int32_t world, int64_t nsteps)
+{
+    if (!ctxs || world < 1) return OOCZ_EINVAL;
+    for (int r = 0; r < world; r++)
+        if (!ctxs[r] || ctxs[r]->rank != r || ctxs[r]->world != world) return OOCZ_EINVAL;
+    return step_group(ctxs, world, nsteps);
+}

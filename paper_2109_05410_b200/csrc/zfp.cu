@@ -1,0 +1,239 @@
+// zfp.cu -- fixed-rate ZFP-style encode / decode kernels for fp32 3-D fields (sm_100a).
+//
+// PAPER.md:120-125 (Sec. IV): a fixed-rate codec, so compressed sizes are known
+// in advance and device buffers are pre-allocated; PAPER.md:155-160 (Fig. 4):
+// blocks are decompressed on arrival and compressed before leaving the GPU.
+// Format: zfp 0.5.5 fixed-rate layout; per-block logic in
+// zfp_block.cuh.
+//
+// Kernel shape: one thread per 4^3 block, 128 threads per CTA; consecutive
+// threads own consecutive bx, so the 16 float4 row loads / stores of a warp are
+// coalesced.  The 32 bit-plane words of each thread live in shared memory in a
+// [plane][thread] layout (conflict-free).  Compressed words are staged through
+// shared memory so that global traffic is coalesced in both kernels.
+#include "common.cuh"
+#include "zfp_block.cuh"
+
+namespace oocz {
+namespace {
+
+constexpr int kThreads = 128;
+
+struct BlockPos { long long bx, by, bz; };
+
+__device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
+    BlockPos p;
+    p.bx = b % nbx;
+    long long r = b / nbx;
+    p.by = r % nby;
+    p.bz = r / nby;
+    return p;
+}
+
+__global__ void __launch_bounds__(kThreads)
+zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
+                  long long nblocks, int rate, uint64_t* __restrict__ out)
+{
+    extern __shared__ __align__(16) uint64_t smem[];
+    uint64_t* planes = smem;                       // [32][kThreads]
+    uint64_t* words = smem + 32 * kThreads;        // [kThreads][rate + 1]
+    const int t = threadIdx.x;
+    const int stride = rate + 1;
+    const long long b0 = (long long)blockIdx.x * kThreads;
+    const long long b = b0 + t;
+
+    if (b < nblocks) {
+        const BlockPos p = block_pos(b, nbx, nby);
+        const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+        uint32_t v[64];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+                v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
+                v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
+                v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
+                v[16 * k + 4 * j + 3] = __float_as_uint(f.w);
+            }
+        zb::BitWriter bw{words + (size_t)t * stride, 0ull, 0, 0};
+        const int Emax = zb::block_exponent(v);
+        if (Emax < 0) {
+            bw.put(0, 1);                          // all-zero block: one 0 bit
+        } else {
+            const uint32_t e = (uint32_t)Emax + 1u; // emax + 127, emax = Emax - 126
+            bw.put(2u * e + 1u, zb::kHeaderBits);
+            int32_t q[64];
+#pragma unroll
+            for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+            zb::fwd_xform(q);
+            constexpr int perm[64] = OOCZ_PERM3;
+            uint32_t lo[32], hi[32];
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
+                hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
+            }
+            zb::transpose32(lo);
+            zb::transpose32(hi);
+#pragma unroll
+            for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
+            zb::encode_planes([&](int k) { return planes[k * kThreads + t]; },
+                              64 * rate - zb::kHeaderBits, bw);
+        }
+        bw.finish(rate);
+    }
+    __syncthreads();
+    // coalesced copy-out of this CTA's contiguous word range
+    const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
+    const int total = (int)nb * rate;
+    uint64_t* dst = out + (size_t)b0 * rate;
+    for (int w = t; w < total; w += kThreads) {
+        const int tt = w / rate, ww = w - tt * rate;
+        dst[w] = words[tt * stride + ww];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
+                  long long nblocks, int rate, float* __restrict__ out)
+{
+    extern __shared__ __align__(16) uint64_t smem[];
+    uint64_t* planes = smem;                       // [32][kThreads]
+    uint64_t* words = smem + 32 * kThreads;        // [kThreads][rate + 1]
+    const int t = threadIdx.x;
+    const int stride = rate + 1;
+    const long long b0 = (long long)blockIdx.x * kThreads;
+    const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
+    {   // coalesced stage-in
+        const int total = (int)nb * rate;
+        const uint64_t* src = in + (size_t)b0 * rate;
+        for (int w = t; w < total; w += kThreads) {
+            const int tt = w / rate, ww = w - tt * rate;
+            words[tt * stride + ww] = __ldg(src + w);
+        }
+    }
+    __syncthreads();
+    if (t >= nb) return;
+
+    const BlockPos p = block_pos(b0 + t, nbx, nby);
+    float* base = out + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+    zb::BitReader br{words + (size_t)t * stride, 0};
+    if (!br.read(1)) {                             // zero block -> +0.0
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int j = 0; j < 4; j++)
+                *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) = make_float4(0.f, 0.f, 0.f, 0.f);
+        return;
+    }
+    const int emax = (int)br.read(zb::kEBits) - 127;
+    zb::decode_planes([&](int k, uint64_t x) { planes[k * kThreads + t] = x; },
+                      64 * rate - zb::kHeaderBits, br);
+    uint32_t lo[32], hi[32];
+#pragma unroll
+    for (int k = 0; k < 32; k++) {
+        const uint64_t x = planes[k * kThreads + t];
+        lo[k] = (uint32_t)x;
+        hi[k] = (uint32_t)(x >> 32);
+    }
+    zb::transpose32(lo);
+    zb::transpose32(hi);
+    constexpr int perm[64] = OOCZ_PERM3;
+    int32_t q[64];
+#pragma unroll
+    for (int i = 0; i < 32; i++) {
+        q[perm[i]] = (int32_t)((lo[i] ^ zb::kNBMask) - zb::kNBMask);
+        q[perm[i + 32]] = (int32_t)((hi[i] ^ zb::kNBMask) - zb::kNBMask);
+    }
+    zb::inv_xform(q);
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int l = 16 * k + 4 * j;
+            *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
+                make_float4(zb::dequantize(q[l], emax), zb::dequantize(q[l + 1], emax),
+                            zb::dequantize(q[l + 2], emax), zb::dequantize(q[l + 3], emax));
+        }
+}
+
+size_t codec_smem_bytes(int rate) {
+    return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * (rate + 1));
+}
+
+bool codec_args_ok(int nx, int ny, int nz, int rate) {
+    return nx >= 0 && ny >= 0 && nz >= 0 && nx % 4 == 0 && ny % 4 == 0 && nz % 4 == 0 &&
+           rate >= 1 && rate <= 64;
+}
+
+}  // namespace
+
+cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
+                              uint64_t* out, cudaStream_t s)
+{
+    if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
+    const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
+    if (nblocks == 0) return cudaSuccess;
+    const size_t smem = codec_smem_bytes(rate);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(zfp_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)codec_smem_bytes(64));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const long long grid = (nblocks + kThreads - 1) / kThreads;
+    zfp_encode_kernel<<<(unsigned)grid, kThreads, smem, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int rate,
+                              float* out, cudaStream_t s)
+{
+    if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
+    const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
+    if (nblocks == 0) return cudaSuccess;
+    const size_t smem = codec_smem_bytes(rate);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(zfp_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)codec_smem_bytes(64));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const long long grid = (nblocks + kThreads - 1) / kThreads;
+    zfp_decode_kernel<<<(unsigned)grid, kThreads, smem, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+}  // namespace oocz
+
+// ------------------------------------------------------------------ C ABI
+extern "C" size_t oocz_zfp_bytes(int32_t nx, int32_t ny, int32_t nz, int32_t rate)
+{
+    if (nx < 0 || ny < 0 || nz < 0 || rate < 0) return 0;
+    return (size_t)(nx / 4) * (size_t)(ny / 4) * (size_t)(nz / 4) * 8u * (size_t)rate;
+}
+
+extern "C" oocz_status oocz_zfp_encode(const float* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                       int32_t rate, uint64_t* d_out, void* stream)
+{
+    if (nx % 4 || ny % 4 || nz % 4) return OOCZ_EALIGN;
+    if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
+        return OOCZ_EINVAL;
+    cudaError_t e = oocz::launch_zfp_encode(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? OOCZ_OK : OOCZ_ECUDA;
+}
+
+extern "C" oocz_status oocz_zfp_decode(const uint64_t* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                       int32_t rate, float* d_out, void* stream)
+{
+    if (nx % 4 || ny % 4 || nz % 4) return OOCZ_EALIGN;
+    if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
+        return OOCZ_EINVAL;
+    cudaError_t e = oocz::launch_zfp_decode(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
+    return e == cudaSuccess ? OOCZ_OK : OOCZ_ECUDA;
+}

@@ -1,0 +1,237 @@
+// zfp_block.cuh -- per-4^3-block ZFP fixed-rate coder, word-parallel.
+//
+// Format (zfp 0.5.5 fixed-rate fp32 3-D, the layout of the
+// cuZFP 0.5.5 library the paper uses): 1 flag bit,
+// 8 exponent bits, group-tested bit planes 31..0 of the negabinary,
+// sequency-ordered coefficients of the lifted block-floating-point integers,
+// truncated at 64*rate bits.
+//
+// This is NOT a transcription of a bit-serial coder.  One thread owns one
+// block and works on whole 64-bit bit planes:
+//   * quantisation straight from the fp32 bit fields (integer ops, exact),
+//   * 32x32 bit-matrix transposes to turn 64 coefficients into 32 planes,
+//   * each group test emits/consumes a whole zero run at once (ctz on the
+//     plane word / on the next <=63 stream bits), so the coder's cost is
+//     O(planes + newly significant coefficients) instead of O(bits).
+// Functions are __host__ __device__ only so that a stand-alone CPU build of
+// this header (tests/native/zfp_host_check.cu) can exercise the same logic; the
+// library itself only calls them from CUDA kernels.
+#pragma once
+#include <cstdint>
+#include <cstring>
+
+#if defined(__CUDACC__)
+#define ZB_HD __host__ __device__ __forceinline__
+#define ZB_UNROLL _Pragma("unroll")
+#else
+#define ZB_HD inline
+#define ZB_UNROLL
+#endif
+
+namespace oocz {
+namespace zb {
+
+constexpr uint32_t kNBMask = 0xaaaaaaaau;
+constexpr int kEBits = 8;
+constexpr int kHeaderBits = 1 + kEBits;
+
+// sequency order of the 64 coefficients (by i+j+k, then i^2+j^2+k^2)
+#define OOCZ_PERM3                                                                  \
+    { 0, 1, 4, 16, 20, 17, 5, 2, 8, 32, 21, 6, 18, 24, 9, 33,                         \
+      36, 3, 12, 48, 22, 25, 37, 40, 34, 10, 7, 19, 28, 13, 49, 52,                   \
+      41, 38, 26, 23, 29, 53, 11, 35, 44, 14, 50, 56, 42, 27, 39, 45,                 \
+      30, 54, 57, 60, 51, 15, 43, 46, 58, 61, 55, 31, 62, 59, 47, 63 }
+
+ZB_HD int ctz64(uint64_t x) {
+#if defined(__CUDA_ARCH__)
+    return __ffsll((long long)x) - 1;
+#else
+    return __builtin_ctzll(x);
+#endif
+}
+
+ZB_HD uint64_t lowmask(int m) { return m >= 64 ? ~0ull : ((1ull << m) - 1ull); }
+ZB_HD uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
+
+// 32-bit two's-complement wraparound arithmetic with arithmetic >> (App. A)
+ZB_HD int32_t add(int32_t a, int32_t b) { return (int32_t)((uint32_t)a + (uint32_t)b); }
+ZB_HD int32_t sub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
+ZB_HD int32_t shl1(int32_t a) { return (int32_t)((uint32_t)a << 1); }
+ZB_HD int32_t asr1(int32_t a) { return a >> 1; }
+
+ZB_HD void fwd_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+    x = add(x, w); x = asr1(x); w = sub(w, x);
+    z = add(z, y); z = asr1(z); y = sub(y, z);
+    x = add(x, z); x = asr1(x); z = sub(z, x);
+    w = add(w, y); w = asr1(w); y = sub(y, w);
+    w = add(w, asr1(y)); y = sub(y, asr1(w));
+}
+
+ZB_HD void inv_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+    y = add(y, asr1(w)); w = sub(w, asr1(y));
+    y = add(y, w); w = shl1(w); w = sub(w, y);
+    z = add(z, x); x = shl1(x); x = sub(x, z);
+    y = add(y, z); z = shl1(z); z = sub(z, y);
+    w = add(w, x); x = shl1(x); x = sub(x, w);
+}
+
+// q[i + 4j + 16k]; lines along x, then y, then z
+ZB_HD void fwd_xform(int32_t q[64]) {
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = 4 * l; fwd_lift(q[b], q[b + 1], q[b + 2], q[b + 3]); }
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = (l & 3) + 16 * (l >> 2); fwd_lift(q[b], q[b + 4], q[b + 8], q[b + 12]); }
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = l; fwd_lift(q[b], q[b + 16], q[b + 32], q[b + 48]); }
+}
+
+ZB_HD void inv_xform(int32_t q[64]) {
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = l; inv_lift(q[b], q[b + 16], q[b + 32], q[b + 48]); }
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = (l & 3) + 16 * (l >> 2); inv_lift(q[b], q[b + 4], q[b + 8], q[b + 12]); }
+ZB_UNROLL
+    for (int l = 0; l < 16; l++) { int b = 4 * l; inv_lift(q[b], q[b + 1], q[b + 2], q[b + 3]); }
+}
+
+// In-place 32x32 bit transpose, LSB = column 0: afterwards bit i of a[k] is
+// the former bit k of a[i].  5 butterfly levels of 16 masked swaps.
+ZB_HD void transpose32(uint32_t a[32]) {
+    uint32_t m = 0x0000ffffu;
+ZB_UNROLL
+    for (int j = 16; j != 0; j >>= 1) {
+ZB_UNROLL
+        for (int k = 0; k < 32; k++) {
+            if ((k & j) == 0) {
+                uint32_t t = ((a[k] >> j) ^ a[k + j]) & m;
+                a[k + j] ^= t;
+                a[k] ^= t << j;
+            }
+        }
+        m ^= m << (j >> 1);
+    }
+}
+
+// Common exponent from fp32 bit patterns: returns the biased exponent E of the
+// largest magnitude (emax = E - 126, i.e. max(frexp exponent, -126); E = 0 for
+// an all-denormal block), or -1 for an all-zero block.
+ZB_HD int block_exponent(const uint32_t v[64]) {
+    uint32_t mx = 0;
+ZB_UNROLL
+    for (int i = 0; i < 64; i++) { uint32_t a = v[i] & 0x7fffffffu; mx = a > mx ? a : mx; }
+    return mx == 0 ? -1 : (int)(mx >> 23);
+}
+
+// q = trunc(x * 2^(30 - emax)), built from the bit fields: x = mant * 2^(max(E,1)-150)
+ZB_HD int32_t quantize(uint32_t bits, int Emax) {
+    int E = (int)((bits >> 23) & 0xffu);
+    uint32_t mant = (bits & 0x7fffffu) | (E ? 0x800000u : 0u);
+    int s = (E < 1 ? 1 : E) - Emax + 6;                       // <= 6
+    uint32_t a = s >= 0 ? (mant << s) : (s > -32 ? (mant >> (-s)) : 0u);
+    return (bits >> 31) ? -(int32_t)a : (int32_t)a;
+}
+
+// x = fl32(fl32(q) * 2^(emax-30)), one rounding of the exact product
+ZB_HD float dequantize(int32_t q, int emax) {
+    int64_t sb = (int64_t)(emax - 30 + 1023) << 52;
+#if defined(__CUDA_ARCH__)
+    double s = __longlong_as_double(sb);
+    return __double2float_rn(__dmul_rn((double)__int2float_rn(q), s));
+#else
+    double s;
+    std::memcpy(&s, &sb, sizeof s);
+    return (float)((double)(float)q * s);
+#endif
+}
+
+// ---------------------------------------------------------------- bit I/O
+struct BitWriter {
+    uint64_t* p;      // next output word
+    uint64_t acc;     // pending bits (LSB first)
+    int nb;           // number of pending bits, < 64
+    int words;        // words stored so far
+    ZB_HD void put(uint64_t v, int n) {        // 0 <= n <= 64, v < 2^n
+        if (n == 0) return;
+        acc |= v << nb;
+        nb += n;
+        if (nb >= 64) {
+            p[words++] = acc;
+            nb -= 64;
+            acc = nb ? (v >> (n - nb)) : 0ull;
+        }
+    }
+    ZB_HD void finish(int total_words) {       // zero padding to the fixed size
+        if (nb) { p[words++] = acc; acc = 0; nb = 0; }
+        while (words < total_words) p[words++] = 0ull;
+    }
+};
+
+struct BitReader {
+    const uint64_t* p;  // stream words of this block
+    int pos;            // bit position
+    ZB_HD uint64_t peek(int m) const {           // 0 <= m <= 64
+        if (m == 0) return 0ull;
+        int w = pos >> 6, o = pos & 63;
+        uint64_t v = p[w] >> o;
+        if (o + m > 64) v |= p[w + 1] << (64 - o);
+        return v & lowmask(m);
+    }
+    ZB_HD uint64_t read(int m) { uint64_t v = peek(m); pos += m; return v; }
+};
+
+// ---------------------------------------------------------------- plane coder
+// Encodes planes[31..0] (plane k: bit i = bit k of coefficient i) under a budget
+// of `bits` bits.  PlaneAt(k) returns plane k.
+template <class PlaneAt>
+ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
+    int n = 0;                                 // significant coefficients so far
+    for (int k = 31; k >= 0 && bits > 0; --k) {
+        uint64_t x = plane_at(k);
+        int m = n < bits ? n : bits;           // first n bits verbatim
+        bw.put(x & lowmask(m), m);
+        bits -= m;
+        x = shr64(x, m);
+        while (n < 64 && bits > 0) {           // group tests over the rest
+            if (x == 0) { bw.put(0, 1); bits -= 1; break; }
+            bw.put(1, 1); bits -= 1;
+            int tz = ctz64(x);                 // zero run up to the next one
+            int cnt; uint64_t pat;
+            if (n + tz < 63) { cnt = tz + 1; pat = 1ull << tz; }
+            else { cnt = tz; pat = 0; }        // position 63 is implied, never sent
+            int e = cnt < bits ? cnt : bits;
+            bw.put(pat & lowmask(e), e);
+            bits -= e;
+            n += tz + 1;
+            x = shr64(x, tz + 1);
+        }
+    }
+}
+
+// Decodes under a budget of `bits` bits; PlaneSet(k, x) stores plane k.
+template <class PlaneSet>
+ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br) {
+    int n = 0;
+    for (int k = 31; k >= 0; --k) {
+        uint64_t x = 0;
+        if (bits > 0) {
+            int m = n < bits ? n : bits;
+            x = br.read(m);
+            bits -= m;
+            while (n < 64 && bits > 0) {
+                bits -= 1;
+                if (!br.read(1)) break;        // group empty
+                int L = 63 - n < bits ? 63 - n : bits;
+                uint64_t w = br.peek(L);
+                if (w) { int tz = ctz64(w); br.pos += tz + 1; bits -= tz + 1; n += tz; }
+                else   { br.pos += L; bits -= L; n += L; }
+                // a one at n: found, implied (n = 63), or budget ran out (zfp's rule)
+                x += 1ull << n;
+                n += 1;
+            }
+        }
+        plane_set(k, x);
+    }
+}
+
+}  // namespace zb
+}  // namespace oocz

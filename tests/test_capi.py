@@ -1,0 +1,66 @@
+"""CPU-side checks of the C ABI (no GPU compute): the library loads, exports
+every function include/oocz.h declares, and its host-only calls (config
+validation, sizes, CFL bound) follow the contract."""
+import ctypes as C
+from fractions import Fraction
+
+import pytest
+
+
+@pytest.fixture(scope="module")
+def z():
+    import __graft_entry__ as g
+    g.build_library()
+    from paper_2109_05410_b200 import oocz
+    return oocz
+
+
+def test_every_header_symbol_is_exported(z):
+    names = z.header_functions()
+    assert len(names) >= 20
+    lib = C.CDLL(z.LIB_PATH)
+    missing = [n for n in names if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_abi_version(z):
+    assert z.oocz_abi_version() == 1
+
+
+def test_zfp_bytes_closed_form(z):
+    assert z.oocz_zfp_bytes(64, 64, 64, 16) == 524_288
+    assert z.oocz_zfp_bytes(512, 512, 512, 8) == 128 << 20
+    assert z.oocz_zfp_bytes(4096, 4096, 1536, 16) == 51_539_607_552
+
+
+def test_cfl_limit_default_coefficients(z):
+    assert abs(z.oocz_cfl_limit(z.default_coeffs()) - float(Fraction(105, 512))) < 1e-6
+
+
+@pytest.mark.parametrize("kw,world,code,msg", [
+    (dict(nx=62), 1, -2, "multiples of 4"),
+    (dict(block_planes=36, tb=5, nz=144), 1, -1, "P (36) < 2h (40)"),
+    (dict(block_planes=48, nz=144), 1, 0, ""),                       # SPEC.md:297 analogue
+    (dict(block_planes=144, tb=12, nz=1152), 1, 0, ""),             # paper: D = 8 -> P = 144, h = 48
+    (dict(block_planes=40, nz=128), 1, -1, "does not divide"),
+    (dict(block_planes=32, nz=128), 3, -1, "world (3) does not divide nz"),
+    (dict(rate=[16, 70, 16]), 1, -1, "rate[1] (70)"),
+    (dict(block_planes=30), 1, -2, "P (30)"),
+    (dict(slots=1), 1, -1, "slots"),
+    (dict(store=7), 1, -1, "store"),
+])
+def test_validate(z, kw, world, code, msg):
+    base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)
+    base.update(kw)
+    cfg = z.oocz_default_config(base.pop("nx"), base.pop("ny"), base.pop("nz"), **base)
+    rc, m = z.oocz_validate(cfg, world)
+    assert rc == code, m
+    assert msg in m
+
+
+def test_default_config(z):
+    cfg = z.oocz_default_config(16, 16, 64)
+    assert (cfg.nx, cfg.ny, cfg.nz, cfg.tb, cfg.block_planes) == (16, 16, 64, 4, 64)
+    assert list(cfg.rate) == [16, 16, 16] and cfg.store == 0 and cfg.slots == 2
+    import oracle
+    assert list(cfg.c) == list(oracle.default_coeffs())

@@ -1,0 +1,165 @@
+"""End-to-end parity of the out-of-core stepper (oocz_create / set_field /
+step / get_field) vs the oracle's reduced schedule: in-core
+steps plus a whole-field round trip after every sweep.  Bar: bit-exact."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2109_05410_b200 import synth
+from gpu_util import Z, bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _fields(nx, ny, nz, seed, kind="dense"):
+    if kind == "pulse":
+        u = synth.pulse(nx, ny, nz, sigma=4.0)
+        up = u.copy()
+    else:
+        u = synth.dense(nx, ny, nz, seed=seed)
+        up = (synth.dense(nx, ny, nz, seed=seed + 1) * np.float32(0.9)).astype(np.float32)
+    return u, up, synth.layered(nx, ny, nz)
+
+
+def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0):
+    z = Z()
+    nz, ny, nx = u.shape
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
+                                slots=slots, profile=profile)
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        for n in calls:
+            s.step(n)
+        return s.get(z.OOCZ_U), s.get(z.OOCZ_UPREV), s.stats(), (z.oocz_get_events(s.ctx) if profile else None)
+
+
+def _run_oracle(u, up, m, T, rates, calls):
+    a = oracle.roundtrip(u, rates[0])
+    b = oracle.roundtrip(up, rates[1])
+    mm = oracle.roundtrip(m, rates[2])
+    for n in calls:
+        a, b = oracle.advance(a, b, mm, T, rates, n)
+    return a, b
+
+
+CASES = [
+    # nx, ny, nz, T, P, rates, calls
+    (64, 64, 64, 2, 32, (16, 16, 16), [10]),          # C1 shape (BASELINE configs[0])
+    (32, 24, 64, 2, 16, (0, 0, 0), [10]),             # raw
+    (40, 16, 96, 3, 24, (8, 12, 24), [7]),            # mixed rates, n mod T != 0
+    (24, 28, 48, 1, 8, (16, 0, 4), [3, 2]),           # split calls
+    (32, 32, 32, 4, 32, (16, 16, 16), [8]),           # D = 1
+    (136, 12, 64, 2, 16, (24, 24, 24), [6]),          # ragged CTA tiles
+]
+
+
+@pytest.mark.parametrize("store", [0, 1])
+@pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES)
+def test_stepper_matches_oracle(store, nx, ny, nz, T, P, rates, calls):
+    u, up, m = _fields(nx, ny, nz, 3)
+    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, store, calls)
+    ou, oup = _run_oracle(u, up, m, T, rates, calls)
+    assert np.array_equal(bits(gu), bits(ou))
+    assert np.array_equal(bits(gup), bits(oup))
+
+
+def test_c1_config_bit_exact_and_byte_accounting():
+    """BASELINE configs[0]: 64^3, 2 z-blocks, rate 16, 10 steps (PULSE + LAYERED)."""
+    u, up, m = _fields(64, 64, 64, 0, kind="pulse")
+    rates = (16, 16, 16)
+    gu, gup, st, evs = _run_gpu(u, up, m, 2, 32, rates, 0, [10], profile=1)
+    ou, oup = _run_oracle(u, up, m, 2, rates, [10])
+    assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+    stored = oracle.zfp_bytes(64, 64, 64, 16)
+    assert st["sweeps"] == 5
+    assert st["h2d_bytes"] == 5 * 3 * stored         # region sharing: every plane once per sweep
+    assert st["d2h_bytes"] == 5 * 2 * stored         # m is never written back
+    assert st["kernel_launches"] > 0
+    _audit(evs)
+
+
+def _audit(evs):
+    """SPEC.md:285-286 StageEvent invariants: per block h2d <= decode <= stencil
+    <= encode <= d2h in start order; no two events on one lane overlap."""
+    assert evs
+    by_lane = {}
+    for e in evs:
+        assert e["end_ms"] >= e["start_ms"]
+        by_lane.setdefault(e["lane"], []).append(e)
+    for lane, es in by_lane.items():
+        es.sort(key=lambda e: e["start_ms"])
+        for a, b in zip(es, es[1:]):
+            assert b["start_ms"] >= a["end_ms"] - 1e-3, (lane, a, b)
+    order = [0, 1, 2, 3, 4]
+    blocks = {}
+    for e in evs:
+        blocks.setdefault((e["sweep"], e["block"]), {}).setdefault(e["stage"], e)
+    for key, stg in blocks.items():
+        starts = [stg[s]["start_ms"] for s in order if s in stg]
+        assert starts == sorted(starts), key
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("rates", [(16, 16, 16), (0, 0, 0), (8, 24, 12)])
+def test_partitioned_group_bit_identical_to_single(world, rates):
+    """z-partitioned run (halos exchanged in compressed form) == world 1 == oracle."""
+    z = Z()
+    nx, ny, nz, T, P = 32, 24, 128, 2, 16
+    u, up, m = _fields(nx, ny, nz, 5)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0)
+    ctxs = z.oocz_create_local_group(cfg, world)
+    S = nz // world
+    try:
+        for r, c in enumerate(ctxs):
+            for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                z.oocz_set_field(c, f, a[r * S:(r + 1) * S])
+        z.oocz_step_local_group(ctxs, 7)
+        gu = np.concatenate([z.oocz_get_field(c, z.OOCZ_U, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+        gup = np.concatenate([z.oocz_get_field(c, z.OOCZ_UPREV, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+        halo = sum(z.oocz_get_stats(c)["halo_bytes"] for c in ctxs)
+    finally:
+        for c in ctxs:
+            z.oocz_destroy(c)
+    ou, oup = _run_oracle(u, up, m, T, rates, [7])
+    assert np.array_equal(bits(gu), bits(ou))
+    assert np.array_equal(bits(gup), bits(oup))
+    h = 4 * T
+    per = [oracle.zfp_bytes(nx, ny, h, r) if r else 4 * nx * ny * h for r in rates]
+    sweeps = 4
+    assert halo == (world - 1) * 2 * (sweeps * (per[0] + per[1]) + per[2])
+
+
+def test_set_get_round_trip_and_errors():
+    z = Z()
+    nx, ny, nz = 16, 16, 32
+    u, up, m = _fields(nx, ny, nz, 6)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=2, block_planes=16, rate=[12, 12, 12])
+    with z.Stepper(cfg) as s:
+        with pytest.raises(z.OoczError) as ei:
+            s.step(1)                                   # fields not set
+        assert ei.value.status == z.OOCZ_ESTATE
+        bad = u.copy()
+        bad[3, 4, 5] = np.nan
+        with pytest.raises(z.OoczError) as ei:
+            z.oocz_set_field(s.ctx, z.OOCZ_U, bad)
+        assert ei.value.status == z.OOCZ_ENONFINITE
+        with pytest.raises(z.OoczError) as ei:
+            z.oocz_set_field(s.ctx, z.OOCZ_M, np.full_like(m, 0.21))   # > 105/512
+        assert ei.value.status == z.OOCZ_ECFL
+        with pytest.raises(z.OoczError) as ei:
+            z.oocz_set_field(s.ctx, z.OOCZ_M, -m)
+        assert ei.value.status == z.OOCZ_ECFL
+        s.set(u, up, m)
+        assert np.array_equal(bits(s.get(z.OOCZ_U)), bits(oracle.roundtrip(u, 12)))
+        assert np.array_equal(bits(s.get(z.OOCZ_M)), bits(oracle.roundtrip(m, 12)))
+        s.step(0)
+        assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(oracle.roundtrip(up, 12)))
+
+
+def test_slots_and_many_sweeps_pipelined():
+    """Deep pipelines across many sweeps (cross-sweep hazards) stay exact."""
+    u, up, m = _fields(32, 32, 128, 7)
+    for slots in (2, 3, 5):
+        gu, gup, _, _ = _run_gpu(u, up, m, 2, 16, (16, 16, 16), 0, [40], slots=slots)
+        ou, oup = _run_oracle(u, up, m, 2, (16, 16, 16), [40])
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), slots
