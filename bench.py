@@ -1,0 +1,328 @@
+#!/usr/bin/env python3
+"""Benchmark of the out-of-core compressed stencil stepper (arXiv 2109.05410).
+
+One bench "step" = one sweep = T = 4 leapfrog steps over the whole grid through
+the whole hot path (per z-block H2D/decode ->
+4 cone-limited 25-point steps -> encode/D2H, region sharing, 3 streams).
+
+Workload (BASELINE.json configs[1]): 512^3 fp32, DENSE(seed 1) wavefield,
+u- = u, LAYERED m; P = 128 (4 z-blocks), T = 4, ZFP fixed rate 16 on all three
+fields, and the same with compression off ("raw") for the paper's speedup
+question.  Metric: cell-updates/s = nx*ny*nz*T*K / time of K sweeps.
+
+  value : compressed store resident in HBM (inputs already on the device):
+          decode -> stencil -> encode per block, device-timed (CUDA events on
+          the library's own streams), max over ranks.
+  e2e   : the paper's out-of-core path through the public C ABI with the
+          store in pinned HOST memory: every sweep moves the whole compressed
+          state H2D and the read-write fields D2H inside the timed region.
+
+Multi-GPU (torchrun, N > 1): the grid is z-partitioned, one 512^3 slab per
+rank (weak scaling), radius-4 halos exchanged in compressed form with NCCL.
+
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed on
+the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "cell-updates/s out-of-core, ZFP vs raw, at 1/2/4/8 B200; max rel. error"
+NX = NY = NZ = 512
+T = 4
+P = 128
+RATE = 16
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            j = json.load(fh)
+        return float(j["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------- GPU arm
+def make_fields(rank: int, S: int):
+    from paper_2109_05410_b200 import synth
+    z0 = rank * S
+    u = synth.dense(NX, NY, NZ, seed=1, z0=z0 % NZ, z1=z0 % NZ + S) if S <= NZ else None
+    m = synth.layered(NX, NY, NZ, z0=z0 % NZ, z1=z0 % NZ + S)
+    return u, u, m
+
+
+def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile):
+    """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
+    import torch
+    cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=T, block_planes=P, rate=list(rates), store=store,
+                                slots=2, profile=profile)
+    ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
+    try:
+        for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
+            Z.oocz_set_field(ctx, f, a)
+        Z.oocz_step(ctx, warmup * T)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        l0 = Z.oocz_kernel_launch_count()
+        Z.oocz_step(ctx, steps * T)
+        launches = Z.oocz_kernel_launch_count() - l0
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        st = Z.oocz_get_stats(ctx)
+        dev_s = st["last_step_device_ms"] / 1e3
+        if dist:
+            t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dev_s = float(t.item())
+        evs = Z.oocz_get_events(ctx) if profile else []
+        # per-sweep bytes of the timed call only
+        st_all = st
+        return dev_s, st_all, evs, launches, ctx
+    except Exception:
+        Z.oocz_destroy(ctx)
+        raise
+
+
+def roofline(evs, peak_gbs, peak_src):
+    """Dominant kernel of the timed region from the per-launch CUDA events."""
+    from paper_2109_05410_b200.oocz import STAGES
+    per = {}
+    for e in evs:
+        name = STAGES[e["stage"]]
+        if name not in ("stencil", "decode", "encode"):
+            continue
+        d = per.setdefault(name, [0.0, 0, 0])
+        d[0] += e["end_ms"] - e["start_ms"]
+        d[1] += e["bytes"]
+        d[2] += 1
+    if not per:
+        return None, {}
+    dom = max(per, key=lambda k: per[k][0])
+    ms, nbytes, n = per[dom]
+    achieved = nbytes / (ms / 1e3) / 1e9
+    table = {k: {"ms": round(v[0], 4), "launches": v[2], "GB/s": round(v[1] / (v[0] / 1e3) / 1e9, 1)}
+             for k, v in per.items()}
+    kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
+    return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": peak_gbs,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
+            "traffic": None, "avg_launch_ms": round(ms / n, 4),
+            "algorithmic_bytes_per_launch": int(nbytes / n)}, table
+
+
+def gpu_arm(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as td
+        td.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist = td
+    from paper_2109_05410_b200 import oocz as Z
+    nccl_id = None
+    if world > 1:
+        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idt.copy_(torch.frombuffer(bytearray(Z.oocz_get_nccl_id()), dtype=torch.uint8))
+        dist.broadcast(idt, 0)
+        nccl_id = bytes(idt.cpu().numpy().tolist())
+    fields = make_fields(rank, NZ)
+    cells = NX * NY * NZ * world * T * args.steps
+    peak_gbs, peak_src = peaks()
+    out = {}
+    with ClockSampler(local) as clk:
+        for label, store, rates in (("zfp_dev", 1, (RATE,) * 3), ("zfp_host", 0, (RATE,) * 3),
+                                    ("raw_dev", 1, (0, 0, 0)), ("raw_host", 0, (0, 0, 0))):
+            dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
+                                                     args.steps, args.warmup, dist, profile=int(label == "zfp_dev"))
+            sweeps_total = st["sweeps"]
+            out[label] = {"s": dev_s, "cups": cells / dev_s, "launches": launches, "evs": evs,
+                          "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
+                          "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
+                          "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
+            Z.oocz_destroy(ctx)
+    clocks = clk.summary()
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+    roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
+    v, e = out["zfp_dev"], out["zfp_host"]
+    line = {
+        "metric": METRIC,
+        "value": round(v["cups"], 1),
+        "unit": "cell-updates/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": round(v["s"] * 1e3 / args.steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic (DENSE seed 1 wavefield, u- = u, LAYERED m; SURVEY 8(d))",
+        "config": {"workload": f"C2: {NX}^3 fp32 per GPU, 25-point leapfrog, P={P} ({NZ // P} z-blocks), "
+                               f"T={T}, ZFP rate {RATE} on u, u-, m; compressed store resident in HBM",
+                   "grid": [NX, NY, NZ * world], "tb": T, "block_planes": P, "rate": RATE,
+                   "step": "one sweep = T leapfrog steps over the whole grid",
+                   "l2": "inputs larger than L2 (compressed store 768 MiB + 480 MiB slab per GPU)",
+                   "parallelism": f"z-slabs x{world}, NCCL compressed halos" if world > 1 else "single GPU"},
+        "e2e": {"value": round(e["cups"], 1), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": int(e["h2d_per_sweep"]), "d2h_bytes_per_step": int(e["d2h_per_sweep"]),
+                "path": "oocz_step with the store in pinned host memory (the paper's out-of-core path)",
+                "host_link_GBps": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9, 2)},
+        "raw": {"value": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1),
+                "e2e_h2d_bytes_per_step": int(out["raw_host"]["h2d_per_sweep"])},
+        "speedup_zfp_vs_raw": {"value": round(v["cups"] / out["raw_dev"]["cups"], 3),
+                               "e2e": round(e["cups"] / out["raw_host"]["cups"], 3),
+                               "paper_context": "1.20x (fp64, V100-PCIe, PAPER.md:227)"},
+        "gpu_launches": int(v["launches"]),
+        "roofline": roof,
+        "kernels": table,
+        "clocks": clocks,
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+    print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------- CPU oracle arm
+def _oracle_sweep_sample(planes: int):
+    """One sweep (T steps + round trips) of the oracle on a 512 x 512 x `planes`
+    sample of the workload; returns (cells*T, seconds)."""
+    import oracle
+    from paper_2109_05410_b200 import synth
+    u = synth.dense(NX, NY, NZ, seed=1, z0=0, z1=planes)
+    m = synth.layered(NX, NY, NZ, z0=0, z1=planes)
+    t0 = time.perf_counter()
+    oracle.advance(u, u, m, T, (RATE,) * 3, T)
+    dt = time.perf_counter() - t0
+    return NX * NY * planes * T, dt
+
+
+def cpu_baseline(seconds: float = 15.0):
+    import oracle
+    oracle.build()
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    # size the sample to ~`seconds` of work: calibrate on 16 planes
+    n, dt = _oracle_sweep_sample(16)
+    rate = n / dt
+    planes = int(max(16, min(NZ, (seconds * rate) / (NX * NY * T))) // 4 * 4)
+    n, dt = _oracle_sweep_sample(planes)
+    return {"value": round(n / dt, 1), "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+            "sample": f"one sweep (T={T} steps + rate-{RATE} round trips) of a {NX}x{NY}x{planes} slab "
+                      f"of the C2 workload, {dt:.1f} s"}
+
+
+def reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    planes = 32
+    for _ in range(args.warmup):
+        _oracle_sweep_sample(planes)
+    tot_n, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        n, dt = _oracle_sweep_sample(planes)
+        tot_n += n
+        tot_s += dt
+    v = tot_n / tot_s
+    sample = (f"each step: one sweep (T={T} steps + rate-{RATE} round trips) of a {NX}x{NY}x{planes} "
+              f"slab of the C2 workload")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "cell-updates/s",
+        "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(tot_s * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C2 sample: {NX}x{NY}x{planes} of the {NX}^3 grid, T={T}, rate {RATE}"},
+        "cpu_baseline": {"value": round(v, 1), "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(v, 1), "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        reference_arm(args)
+    else:
+        gpu_arm(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -77,12 +77,19 @@ typedef struct {
     double   step_ms;                 /* host wall time spent inside oocz_step               */
     /* per-stage device time summed over blocks (profile = 1 only), ms */
     double   h2d_ms, decode_ms, stencil_ms, encode_ms, d2h_ms, copy_ms, halo_ms;
+    /* device time of oocz_step calls (CUDA events on the library's own streams:
+       from the first enqueued operation to the join of all streams), ms */
+    double   last_step_device_ms, step_device_ms;
 } oocz_stats;
 
 /* one pipeline stage of one block (profile = 1), times relative to the
  * first event of the last oocz_step call (SPEC.md:282-287 StageEvent) */
 enum { OOCZ_ST_H2D = 0, OOCZ_ST_DECODE = 1, OOCZ_ST_STENCIL = 2, OOCZ_ST_ENCODE = 3,
-       OOCZ_ST_D2H = 4, OOCZ_ST_HALO = 5 };
+       OOCZ_ST_D2H = 4, OOCZ_ST_HALO = 5, OOCZ_ST_COPY = 6 };
+/* events are per operation: one per stencil launch, one per field for decode /
+ * encode; `bytes` is that operation's ALGORITHMIC byte count (DESIGN.md
+ * "Roofline"): stencil 16 B per updated cell; decode/encode the compressed bytes
+ * plus 4 B per value; copies and transfers the bytes moved. */
 typedef struct {
     int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute, 2 = d2h, 3 = comm */
     double   start_ms, end_ms;

@@ -118,6 +118,9 @@ struct oocz_ctx {
     // profiling
     struct Prof { int sweep, block, stage, lane; cudaEvent_t a, b; uint64_t bytes; };
     std::vector<Prof> prof;
+    std::vector<cudaEvent_t> ev_pool;       // timing events, reused across calls
+    size_t ev_used = 0;
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_join_h2d = nullptr, ev_join_comp = nullptr;
     std::vector<oocz_event> events;
     oocz_stats stats{};
 };
@@ -187,12 +190,20 @@ cudaError_t decode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, 
     return launch_zfp_decode(reinterpret_cast<const uint64_t*>(src), c->nx, c->ny, nplanes, rate, dst, s);
 }
 
+cudaEvent_t pool_event(oocz_ctx* c)
+{
+    if (c->ev_used == c->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        c->ev_pool.push_back(e);
+    }
+    return c->ev_pool[c->ev_used++];
+}
+
 void prof_begin(oocz_ctx* c, int sweep, int block, int stage, int lane, cudaStream_t s, uint64_t bytes)
 {
     if (!c->cfg.profile) return;
-    oocz_ctx::Prof p{sweep, block, stage, lane, nullptr, nullptr, bytes};
-    cudaEventCreate(&p.a);
-    cudaEventCreate(&p.b);
+    oocz_ctx::Prof p{sweep, block, stage, lane, pool_event(c), pool_event(c), bytes};
     cudaEventRecord(p.a, s);
     c->prof.push_back(p);
 }
@@ -402,6 +413,10 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     CKC(mk(ctx->ev_out_ready, nslots));
     CKC(mk(ctx->ev_out_free, nslots));
     CKC(mk(ctx->ev_written, D));
+    CKC(cudaEventCreate(&ctx->ev_t0));
+    CKC(cudaEventCreate(&ctx->ev_t1));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join_h2d, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join_comp, cudaEventDisableTiming));
     if (preset_halo) {
         ctx->halo = preset_halo;
     } else if (world > 1) {
@@ -479,7 +494,9 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     cudaFree(ctx->d_flags);
     for (auto* v : {&ctx->ev_in_ready, &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free, &ctx->ev_written})
         for (auto e : *v) cudaEventDestroy(e);
-    for (auto& p : ctx->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : {ctx->ev_t0, ctx->ev_t1, ctx->ev_join_h2d, ctx->ev_join_comp})
+        if (e) cudaEventDestroy(e);
     if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
     if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
@@ -653,7 +670,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
 
     // ---- (a4) slab assembly: time-t C_{i-1} from the previous block, halo from a neighbour rank
     if (i > 0) {
-        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 1, sc, 0);
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 3 * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < 3; f++)
             CK(cudaMemcpyAsync(ctx->slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sc));
         prof_end(ctx, sc);
@@ -664,33 +681,36 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
             return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
     }
     // ---- (a3) decode the read unit into the slab
-    {
-        uint64_t bytes = 0;
-        for (int f = 0; f < 3; f++) bytes += (uint64_t)rd_planes * pb;
+    for (int f = 0; f < 3; f++) {
+        // algorithmic bytes: compressed (or raw) read unit in + fp32 planes out
+        const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 1, sc, bytes);
-        for (int f = 0; f < 3; f++)
-            CK(decode_or_copy(ctx, f, src[f], rd_planes, ctx->slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sc));
+        CK(decode_or_copy(ctx, f, src[f], rd_planes, ctx->slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sc));
         prof_end(ctx, sc);
     }
     if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sc));
     // keep the time-t C_i for block i+1 (reading R14)
-    if (i < D - 1)
+    if (i < D - 1) {
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 3 * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < 3; f++)
             CK(cudaMemcpyAsync(ctx->ccopy[f], ctx->slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
                                cudaMemcpyDeviceToDevice, sc));
+        prof_end(ctx, sc);
+    }
 
     // ---- (a5) T cone-limited steps, in place, roles swapping
     float* cu = ctx->slab[OOCZ_U];
     float* cp = ctx->slab[OOCZ_UPREV];
-    prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 0);
     for (int s = 1; s <= ts; s++) {
         const int z0 = std::max(4 * s, g.vlo);
         const int z1 = std::min(ctx->L - 4 * s, g.vhi);
+        // algorithmic bytes: read u, u-, m and write u+ once per updated cell
+        prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 16ull * (uint64_t)std::max(z1 - z0, 0) * ctx->plane_elems);
         CK(launch_stencil_step(cu, cp, ctx->slab[OOCZ_M], ctx->nx, ctx->ny, ctx->L, ctx->cfg.c, z0, z1, g.vlo,
                                g.vhi, sc));
+        prof_end(ctx, sc);
         std::swap(cu, cp);
     }
-    prof_end(ctx, sc);
 
     // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-
     const float* own[2] = {cu + (size_t)h * ctx->plane_elems, cp + (size_t)h * ctx->plane_elems};
@@ -701,9 +721,11 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     }
     if (host) {
         CK(cudaStreamWaitEvent(sc, ctx->ev_out_free[slot], 0));
-        prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, 0);
-        for (int f = 0; f < 2; f++) CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], sc));
-        prof_end(ctx, sc);
+        for (int f = 0; f < 2; f++) {
+            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
+            CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], sc));
+            prof_end(ctx, sc);
+        }
         CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
         // ---- (a7) D2H into the store, in place
         cudaStream_t sd = ctx->s_d2h;
@@ -719,10 +741,11 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
         CK(cudaEventRecord(ctx->ev_out_free[slot], sd));
         CK(cudaEventRecord(ctx->ev_written[i], sd));
     } else {
-        prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, 0);
-        for (int f = 0; f < 2; f++)
+        for (int f = 0; f < 2; f++) {
+            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
             CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), sc));
-        prof_end(ctx, sc);
+            prof_end(ctx, sc);
+        }
     }
     ctx->seq++;
     return OOCZ_OK;
@@ -736,25 +759,35 @@ static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
     for (int f = 0; f < 3; f++)
         if (!ctx->field_set[f]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", f);
     CK(cudaSetDevice(ctx->device));
-    for (auto& p : ctx->prof) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
     ctx->prof.clear();
     ctx->events.clear();
-    *base = nullptr;
-    if (ctx->cfg.profile) {
-        CK(cudaEventCreate(base));
-        CK(cudaEventRecord(*base, ctx->s_h2d));
-        CK(cudaStreamWaitEvent(ctx->s_comp, *base, 0));
-        CK(cudaStreamWaitEvent(ctx->s_d2h, *base, 0));
-    }
+    ctx->ev_used = 0;
+    // device-side timing of the whole call: all three streams start after t0
+    *base = ctx->ev_t0;
+    CK(cudaEventRecord(ctx->ev_t0, ctx->s_h2d));
+    CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_t0, 0));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_t0, 0));
     return OOCZ_OK;
 }
 
 static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
 {
     CK(cudaSetDevice(ctx->device));
+    // join the three streams into s_d2h and stamp t1 there
+    CK(cudaEventRecord(ctx->ev_join_h2d, ctx->s_h2d));
+    CK(cudaEventRecord(ctx->ev_join_comp, ctx->s_comp));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_h2d, 0));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_comp, 0));
+    CK(cudaEventRecord(ctx->ev_t1, ctx->s_d2h));
     CK(cudaStreamSynchronize(ctx->s_h2d));
     CK(cudaStreamSynchronize(ctx->s_comp));
     CK(cudaStreamSynchronize(ctx->s_d2h));
+    {
+        float ms = 0;
+        CK(cudaEventElapsedTime(&ms, ctx->ev_t0, ctx->ev_t1));
+        ctx->stats.last_step_device_ms = ms;
+        ctx->stats.step_device_ms += ms;
+    }
     ctx->stats.steps += (uint64_t)nsteps;
     ctx->stats.halo_bytes = halo_bytes_sent(ctx->halo);
     if (ctx->cfg.profile && base) {
@@ -771,9 +804,9 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
                 case OOCZ_ST_ENCODE: ctx->stats.encode_ms += d; break;
                 case OOCZ_ST_D2H: ctx->stats.d2h_ms += d; break;
                 case OOCZ_ST_HALO: ctx->stats.halo_ms += d; break;
+                case OOCZ_ST_COPY: ctx->stats.copy_ms += d; break;
             }
         }
-        cudaEventDestroy(base);
     }
     return OOCZ_OK;
 }

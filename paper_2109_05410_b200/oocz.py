@@ -27,7 +27,7 @@ OOCZ_OK, OOCZ_EINVAL, OOCZ_EALIGN, OOCZ_ECFL, OOCZ_ECAPACITY = 0, -1, -2, -3, -4
 OOCZ_ENONFINITE, OOCZ_ESTATE, OOCZ_ECUDA, OOCZ_ENCCL = -5, -6, -7, -8
 OOCZ_U, OOCZ_UPREV, OOCZ_M = 0, 1, 2
 OOCZ_STORE_HOST, OOCZ_STORE_DEVICE = 0, 1
-STAGES = {0: "h2d", 1: "decode", 2: "stencil", 3: "encode", 4: "d2h", 5: "halo"}
+STAGES = {0: "h2d", 1: "decode", 2: "stencil", 3: "encode", 4: "d2h", 5: "halo", 6: "copy"}
 
 
 class oocz_config(C.Structure):
@@ -43,7 +43,8 @@ class oocz_stats(C.Structure):
                 ("device_bytes_used", C.c_uint64), ("host_bytes_pinned", C.c_uint64),
                 ("step_ms", C.c_double), ("h2d_ms", C.c_double), ("decode_ms", C.c_double),
                 ("stencil_ms", C.c_double), ("encode_ms", C.c_double), ("d2h_ms", C.c_double),
-                ("copy_ms", C.c_double), ("halo_ms", C.c_double)]
+                ("copy_ms", C.c_double), ("halo_ms", C.c_double),
+                ("last_step_device_ms", C.c_double), ("step_device_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
