@@ -144,7 +144,9 @@ oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t world, int32
 oocz_status oocz_step_local_group(oocz_ctx* const* ctxs, int32_t world, int64_t nsteps);
 /* copy up to cap events of the last oocz_step (profile = 1) into evs; *n = total */
 oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, size_t cap, size_t* n);
-const char* oocz_last_error(const oocz_ctx* ctx);  /* owned by ctx; valid until the next call */
+/* owned by ctx; valid until the next call.  With ctx == NULL: the last failure of a
+ * stateless codec / kernel call on this host thread. */
+const char* oocz_last_error(const oocz_ctx* ctx);
 void        oocz_destroy(oocz_ctx* ctx);
 
 /* ---------------------------------------------------------------- codec / kernels

@@ -16,6 +16,8 @@ namespace oocz {
 
 // count of this library's kernel launches (oocz_kernel_launch_count)
 void note_launches(uint64_t n);
+// record a failure of a stateless call (oocz_last_error(NULL)); returns s
+oocz_status stateless_status(cudaError_t e, const char* what);
 
 // launch-configuration helpers
 constexpr int kNumSMs = 148;  // B200

@@ -42,6 +42,14 @@ namespace oocz {
 static std::atomic<uint64_t> g_launches{0};
 void note_launches(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+static thread_local std::string g_stateless_err;
+oocz_status stateless_status(cudaError_t e, const char* what)
+{
+    if (e == cudaSuccess) return OOCZ_OK;
+    g_stateless_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return OOCZ_ECUDA;
+}
+
 namespace {
 
 __global__ void scan_field_kernel(const float* __restrict__ in, size_t n, unsigned int* flags)
@@ -503,7 +511,10 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     delete ctx;
 }
 
-extern "C" const char* oocz_last_error(const oocz_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+extern "C" const char* oocz_last_error(const oocz_ctx* ctx)
+{
+    return ctx ? ctx->err.c_str() : g_stateless_err.c_str();
+}
 
 extern "C" oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out)
 {

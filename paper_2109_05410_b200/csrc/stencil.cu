@@ -7,23 +7,26 @@
 // it updates planes [z0, z1) of a z-slab in place (u+ overwrites u-).
 //
 // Design (HBM-bound: >= 16 B per cell-update: read u, u-, m, write u+):
-//  * CTA tile 128 (x) x 8 (y) cells, 256 threads, each thread 4 consecutive x.
-//  * The u plane tile with its radius-4 x/y halo (136 x 16 floats) arrives by
-//    TMA (cp.async.bulk.tensor.3d) into an 8-stage shared-memory ring guarded
-//    by mbarriers; planes are prefetched 3 ahead.  TMA out-of-bounds fill gives
-//    the zero Dirichlet ghost in x, y and z for free: the tensor map covers only
-//    the planes [zv0, zv1) that hold data.
-//  * z-neighbours come from a 9-deep register queue of float4 (values, not
+//  * CTA tile 128 (x) x 16 (y) cells marched along a z chunk; warp-specialised:
+//    warp 0 is a TMA producer (one elected lane), warps 1..16 compute one row
+//    each, 4 consecutive x per thread.
+//  * Producer: cp.async.bulk.tensor.3d loads of
+//      - the u plane tile with its radius-4 x/y halo (136 x 24 floats) into an
+//        8-stage ring; TMA out-of-bounds fill gives the zero Dirichlet ghost in
+//        x, y and z (the tensor map covers only the planes [zv0, zv1) that hold
+//        data);
+//      - the u- and m tiles (128 x 16 each) into a 4-stage ring.
+//    full/empty mbarrier pairs per stage: consumers release a stage as soon as
+//    every consumer warp is done with it (no CTA-wide barrier per plane), so
+//    the producer stays 3 u planes / 3 u-,m planes ahead.
+//  * Consumers: z-neighbours from a 9-deep float4 register queue (values, not
 //    partial sums, so the prescribed summation order is kept); x/y neighbours
-//    are 128-bit shared-memory loads.
-//  * u- and m are streamed with 128-bit loads one plane ahead; u+ is stored
-//    with 128-bit stores.
-//  * Each CTA marches a 32-plane z chunk (8 halo planes of extra TMA traffic,
-//    mostly L2 hits) so that a 512^2 x 160 slab gives ~1300 CTAs.
+//    and u-, m from shared memory with 128-bit loads; u+ with 128-bit stores.
 //  * Arithmetic: DESIGN.md R5 order with __fadd_rn / __fmul_rn / __fmaf_rn, so
 //    results are bit-identical to the fp32 oracle.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -31,14 +34,18 @@
 namespace oocz {
 namespace {
 
-constexpr int TX = 128, TY = 8;
-constexpr int SW = TX + 8, SH = TY + 8;         // smem tile incl. halo
-constexpr int kStageFloats = SW * SH;          // 2176 floats = 8704 B (128 B multiple)
-constexpr int NS = 8;                          // ring stages
-constexpr int ZCHUNK = 32;
-constexpr int kThreads = 32 * TY;
-constexpr unsigned kStageBytes = kStageFloats * sizeof(float);
-constexpr size_t kSmemBytes = (size_t)NS * kStageBytes + 128;
+constexpr int TX = 128, TY = 16;
+constexpr int SW = TX + 8, SH = TY + 8;          // u tile incl. halo
+constexpr int kUStageFloats = SW * SH;          // 3264 floats = 13056 B (128 B multiple)
+constexpr int kRStageFloats = 2 * TX * TY;      // u- tile then m tile, 16 KiB
+constexpr int NU = 8;                           // u ring stages
+constexpr int NR = 4;                           // u-/m ring stages
+constexpr int kConsumerWarps = TY;
+constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr unsigned kUBytes = kUStageFloats * sizeof(float);
+constexpr unsigned kRTileBytes = TX * TY * sizeof(float);
+constexpr size_t kSmemBytes = (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 128;
+constexpr int kMaxChunk = 64;
 
 struct Coeffs { float c0x3, c1, c2, c3, c4; };
 
@@ -52,6 +59,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n"
@@ -60,7 +70,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity)
         : "memory");
 }
-__device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, int c0, int c1, int c2,
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -69,86 +79,111 @@ __device__ __forceinline__ void tma_load_3d(float* dst, const CUtensorMap* map, 
         : "memory");
 }
 
-__global__ void __launch_bounds__(kThreads, 2)
-stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, float* __restrict__ uprev,
-                 const float* __restrict__ m, int nx, int ny, int z0, int z1, int zv0, Coeffs cf)
+__global__ void __launch_bounds__(kThreads, 1)
+stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
+                 const __grid_constant__ CUtensorMap tm_m, float* __restrict__ uprev, int nx, int ny,
+                 int z0, int z1, int zchunk, int zv0, Coeffs cf)
 {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* ring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    __shared__ __align__(8) uint64_t full[NS];
+    float* uring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
+    float* rring = uring + NU * kUStageFloats;
+    __shared__ __align__(8) uint64_t ufull[NU], uempty[NU], rfull[NR], rempty[NR];
 
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zb = z0 + blockIdx.z * ZCHUNK;
-    const int ze = min(zb + ZCHUNK, z1);
+    const int zb = z0 + blockIdx.z * zchunk;
+    const int ze = min(zb + zchunk, z1);
     const int pfirst = zb - 4, plast = ze + 4;  // u planes needed: [pfirst, plast)
-    const bool leader = threadIdx.x == 0;
 
-    if (leader) {
-        for (int s = 0; s < NS; s++) mbar_init(&full[s], 1);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NU; s++) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], kConsumerWarps); }
+        for (int s = 0; s < NR; s++) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], kConsumerWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
 
-    auto issue = [&](int p) {  // leader only
-        const int s = (p - pfirst) % NS;
-        mbar_expect_tx(&full[s], kStageBytes);
-        tma_load_3d(ring + s * kStageFloats, &tm_u, x0 - 4, y0 - 4, p - zv0, &full[s]);
-    };
-    auto wait_plane = [&](int p) -> const float* {
-        const int s = (p - pfirst) % NS;
-        mbar_wait(&full[s], (uint32_t)(((p - pfirst) / NS) & 1));
-        return ring + s * kStageFloats;
-    };
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (lane == 0) {
+            int jr = 0;
+            for (int i = 0; pfirst + i < plast; i++) {
+                const int p = pfirst + i;
+                const int s = i % NU;
+                if (i >= NU) mbar_wait(&uempty[s], ((i / NU) & 1) ^ 1);
+                mbar_expect_tx(&ufull[s], kUBytes);
+                tma_load_3d(uring + s * kUStageFloats, &tm_u, x0 - 4, y0 - 4, p - zv0, &ufull[s]);
+                const int z = p - 4;                       // u-, m of plane z go with u plane z+4
+                if (z >= zb && z < ze) {
+                    const int r = jr % NR;
+                    if (jr >= NR) mbar_wait(&rempty[r], ((jr / NR) & 1) ^ 1);
+                    mbar_expect_tx(&rfull[r], 2 * kRTileBytes);
+                    float* dst = rring + r * kRStageFloats;
+                    tma_load_3d(dst, &tm_up, x0, y0, z, &rfull[r]);
+                    tma_load_3d(dst + TX * TY, &tm_m, x0, y0, z, &rfull[r]);
+                    jr++;
+                }
+            }
+        }
+        return;
+    }
 
-    if (leader)
-        for (int p = pfirst; p < min(pfirst + NS, plast); p++) issue(p);
-
-    const int gx = x0 + 4 * tx, gy = y0 + ty;
+    // ---------------------------------------------------------------- consumers
+    const int ty = warp - 1;
+    const int gx = x0 + 4 * lane, gy = y0 + ty;
     const bool active = gx < nx && gy < ny;
     const size_t plane = (size_t)nx * ny;
     const size_t col = (size_t)gy * nx + gx;
-    const int cidx = (ty + 4) * SW + 4 + 4 * tx;  // this thread's centre in a stage
+    const int cidx = (ty + 4) * SW + 4 + 4 * lane;  // this thread's centre in a u stage
+    const int ridx = ty * TX + 4 * lane;             // ... in a u- / m tile
 
-    // register queue: planes z-4 .. z+4
+    auto ustage = [&](int p) { return (p - pfirst) % NU; };
+    auto wait_u = [&](int p) -> const float* {
+        const int i = p - pfirst;
+        mbar_wait(&ufull[i % NU], (uint32_t)((i / NU) & 1));
+        return uring + (i % NU) * kUStageFloats;
+    };
+    auto release_u = [&](int p) {
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&uempty[ustage(p)]);
+    };
+
     float4 q[9];
 #pragma unroll
+    for (int i = 0; i < 8; i++) q[i] = *reinterpret_cast<const float4*>(wait_u(pfirst + i) + cidx);
+#pragma unroll
     for (int i = 0; i < 8; i++) {
-        const float* st = wait_plane(pfirst + i);
-        q[i] = *reinterpret_cast<const float4*>(st + cidx);
-    }
-    __syncthreads();  // halo stages (planes zb-4 .. zb-1) are free again
-    if (leader) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        for (int p = pfirst + NS; p < min(pfirst + NS + 4, plast); p++) issue(p);
-    }
-
-    float4 up_n = make_float4(0.f, 0.f, 0.f, 0.f), m_n = up_n;
-    if (active && zb < ze) {
-        up_n = *reinterpret_cast<const float4*>(uprev + (size_t)zb * plane + col);
-        m_n = __ldg(reinterpret_cast<const float4*>(m + (size_t)zb * plane + col));
+        const int p = pfirst + i;
+        if (p < zb || p >= ze) release_u(p);          // halo planes: centre was their only use
     }
 
     for (int z = zb; z < ze; z++) {
-        const float4 upv = up_n, mv = m_n;
-        if (active && z + 1 < ze) {  // stream u-, m one plane ahead
-            up_n = *reinterpret_cast<const float4*>(uprev + (size_t)(z + 1) * plane + col);
-            m_n = __ldg(reinterpret_cast<const float4*>(m + (size_t)(z + 1) * plane + col));
-        }
-        {
-            const float* st4 = wait_plane(z + 4);
-            q[8] = *reinterpret_cast<const float4*>(st4 + cidx);
-        }
-        const float* st = wait_plane(z);
-        const float* crow = st + cidx;
+        q[8] = *reinterpret_cast<const float4*>(wait_u(z + 4) + cidx);
+        const int j = z - zb;
+        mbar_wait(&rfull[j % NR], (uint32_t)((j / NR) & 1));
+        const float* rt = rring + (j % NR) * kRStageFloats;
+        const float4 upv = *reinterpret_cast<const float4*>(rt + ridx);
+        const float4 mv = *reinterpret_cast<const float4*>(rt + TX * TY + ridx);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[j % NR]);
+
+        const float* crow = uring + ustage(z) * kUStageFloats + cidx;  // plane z already landed
         const float4 xl = *reinterpret_cast<const float4*>(crow - 4);
         const float4 xr = *reinterpret_cast<const float4*>(crow + 4);
-        float4 ym[4], yp[4];
+        // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
+        // which is the first addition of the prescribed order anyway
+        float ay[4][4];
 #pragma unroll
         for (int d = 1; d <= 4; d++) {
-            ym[d - 1] = *reinterpret_cast<const float4*>(crow - d * SW);
-            yp[d - 1] = *reinterpret_cast<const float4*>(crow + d * SW);
+            const float4 a = *reinterpret_cast<const float4*>(crow - d * SW);
+            const float4 b = *reinterpret_cast<const float4*>(crow + d * SW);
+            ay[d - 1][0] = __fadd_rn(a.x, b.x);
+            ay[d - 1][1] = __fadd_rn(a.y, b.y);
+            ay[d - 1][2] = __fadd_rn(a.z, b.z);
+            ay[d - 1][3] = __fadd_rn(a.w, b.w);
         }
+        release_u(z);
+        if (z + 4 >= ze) release_u(z + 4);
+
         const float4 uc = q[4];
         const float w[12] = {xl.x, xl.y, xl.z, xl.w, uc.x, uc.y, uc.z, uc.w, xr.x, xr.y, xr.z, xr.w};
         const float ucv[4] = {uc.x, uc.y, uc.z, uc.w};
@@ -161,14 +196,11 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, float* __restrict__ u
             float s[4];
 #pragma unroll
             for (int d = 1; d <= 4; d++) {
-                const float* ymd = reinterpret_cast<const float*>(&ym[d - 1]);
-                const float* ypd = reinterpret_cast<const float*>(&yp[d - 1]);
                 const float* zmd = reinterpret_cast<const float*>(&q[4 - d]);
                 const float* zpd = reinterpret_cast<const float*>(&q[4 + d]);
                 const float ax = __fadd_rn(w[4 + o - d], w[4 + o + d]);
-                const float ay = __fadd_rn(ymd[o], ypd[o]);
                 const float az = __fadd_rn(zmd[o], zpd[o]);
-                s[d - 1] = __fadd_rn(__fadd_rn(ax, ay), az);
+                s[d - 1] = __fadd_rn(__fadd_rn(ax, ay[d - 1][o]), az);
             }
             float L = __fmul_rn(cf.c0x3, u0);
             L = __fmaf_rn(cf.c1, s[0], L);
@@ -181,11 +213,6 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, float* __restrict__ u
             *reinterpret_cast<float4*>(uprev + (size_t)z * plane + col) = make_float4(res[0], res[1], res[2], res[3]);
 #pragma unroll
         for (int i = 0; i < 8; i++) q[i] = q[i + 1];
-        __syncthreads();  // stage of plane z is free
-        if (leader && z + NS < plast) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(z + NS);
-        }
     }
 }
 
@@ -202,6 +229,18 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
+bool make_map(CUtensorMap* map, const float* base, int nx, int ny, int nplanes, int bx, int by) {
+    auto encode = get_encode_fn();
+    if (!encode) return false;
+    const cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nplanes};
+    const cuuint64_t gstride[2] = {(cuuint64_t)nx * sizeof(float), (cuuint64_t)nx * ny * sizeof(float)};
+    const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    const cuuint32_t estride[3] = {1, 1, 1};
+    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim, gstride, box,
+                  estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 }  // namespace
 
 cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, int nx, int ny, int nz,
@@ -210,18 +249,10 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
     if (nx <= 0 || ny <= 0 || nx % 4 || z0 < 0 || z1 > nz || zv0 < 0 || zv1 > nz || zv0 >= zv1)
         return cudaErrorInvalidValue;
     if (z1 <= z0) return cudaSuccess;
-    auto encode = get_encode_fn();
-    if (!encode) return cudaErrorNotSupported;
-    CUtensorMap map;
-    const cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)(zv1 - zv0)};
-    const cuuint64_t gstride[2] = {(cuuint64_t)nx * sizeof(float), (cuuint64_t)nx * ny * sizeof(float)};
-    const cuuint32_t box[3] = {SW, SH, 1};
-    const cuuint32_t estride[3] = {1, 1, 1};
-    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                        const_cast<float*>(u) + (size_t)zv0 * nx * ny, gdim, gstride, box, estride,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    CUtensorMap mu, mup, mm;
+    if (!make_map(&mu, u + (size_t)zv0 * nx * ny, nx, ny, zv1 - zv0, SW, SH) ||
+        !make_map(&mup, uprev, nx, ny, nz, TX, TY) || !make_map(&mm, m, nx, ny, nz, TX, TY))
+        return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(stencil25_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -230,8 +261,14 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
         attr_set = true;
     }
     Coeffs cf{3.0f * c[0], c[1], c[2], c[3], c[4]};  // fl32(3 c0), as the oracle
-    dim3 grid((nx + TX - 1) / TX, (ny + TY - 1) / TY, (z1 - z0 + ZCHUNK - 1) / ZCHUNK);
-    stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(map, uprev, m, nx, ny, z0, z1, zv0, cf);
+    // z chunk: aim for ~4 waves of one CTA per SM, between 16 and kMaxChunk planes
+    const long tiles = (long)((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
+    const int nzu = z1 - z0;
+    long want = (tiles * nzu + 4L * kNumSMs - 1) / (4L * kNumSMs);
+    int chunk = (int)std::min<long>(kMaxChunk, std::max<long>(16, want));
+    chunk = std::min(chunk, nzu);
+    dim3 grid((nx + TX - 1) / TX, (ny + TY - 1) / TY, (nzu + chunk - 1) / chunk);
+    stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, zv0, cf);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -250,7 +287,7 @@ extern "C" oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev
         return OOCZ_EINVAL;
     cudaError_t e = oocz::launch_stencil_step(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1,
                                               (cudaStream_t)stream);
-    return e == cudaSuccess ? OOCZ_OK : OOCZ_ECUDA;
+    return oocz::stateless_status(e, __func__);
 }
 
 extern "C" oocz_status oocz_stencil_steps(float* d_u, float* d_uprev, const float* d_m, int32_t nx,

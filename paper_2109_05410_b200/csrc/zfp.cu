@@ -225,7 +225,7 @@ extern "C" oocz_status oocz_zfp_encode(const float* d_in, int32_t nx, int32_t ny
     if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
         return OOCZ_EINVAL;
     cudaError_t e = oocz::launch_zfp_encode(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
-    return e == cudaSuccess ? OOCZ_OK : OOCZ_ECUDA;
+    return oocz::stateless_status(e, __func__);
 }
 
 extern "C" oocz_status oocz_zfp_decode(const uint64_t* d_in, int32_t nx, int32_t ny, int32_t nz,
@@ -235,5 +235,5 @@ extern "C" oocz_status oocz_zfp_decode(const uint64_t* d_in, int32_t nx, int32_t
     if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
         return OOCZ_EINVAL;
     cudaError_t e = oocz::launch_zfp_decode(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
-    return e == cudaSuccess ? OOCZ_OK : OOCZ_ECUDA;
+    return oocz::stateless_status(e, __func__);
 }

@@ -146,12 +146,12 @@ ZB_HD float dequantize(int32_t q, int emax) {
 
 // ---------------------------------------------------------------- bit I/O
 struct BitWriter {
-    uint64_t* p;      // next output word
+    uint64_t* p;      // output words of this block
     uint64_t acc;     // pending bits (LSB first)
     int nb;           // number of pending bits, < 64
     int words;        // words stored so far
-    ZB_HD void put(uint64_t v, int n) {        // 0 <= n <= 64, v < 2^n
-        if (n == 0) return;
+    // append the low n bits of v (1 <= n <= 64, v < 2^n)
+    ZB_HD void put(uint64_t v, int n) {
         acc |= v << nb;
         nb += n;
         if (nb >= 64) {
@@ -169,9 +169,11 @@ struct BitWriter {
 struct BitReader {
     const uint64_t* p;  // stream words of this block
     int pos;            // bit position
-    ZB_HD uint64_t peek(int m) const {           // 0 <= m <= 64
+    // next m bits (0 <= m <= 64) without consuming them; never reads past the
+    // word holding the last requested bit
+    ZB_HD uint64_t peek(int m) const {
         if (m == 0) return 0ull;
-        int w = pos >> 6, o = pos & 63;
+        const int w = pos >> 6, o = pos & 63;
         uint64_t v = p[w] >> o;
         if (o + m > 64) v |= p[w + 1] << (64 - o);
         return v & lowmask(m);
@@ -180,57 +182,103 @@ struct BitReader {
 };
 
 // ---------------------------------------------------------------- plane coder
-// Encodes planes[31..0] (plane k: bit i = bit k of coefficient i) under a budget
-// of `bits` bits.  PlaneAt(k) returns plane k.
+// Both coders run ONE flat loop of per-lane "events" whose body is
+// straight-line code (both alternatives computed, then selected), so the 32
+// lanes of a warp -- 32 different blocks -- never wait for each other's group
+// tests and the compiler has no branch to re-nest into an inner loop:
+//   plane start : the first n bits of plane k verbatim, plus the group flag 0
+//                 when nothing new is significant in the plane (plane done);
+//   found one   : flag 1, the zero run and the one (1 | 2 << tz: tz + 2 bits;
+//                 tz + 1 bits when the one sits at position 63, which is never
+//                 sent), plus the closing flag 0 when no one is left.
+// The encoded stream is exactly the bit-serial coder's, cut at the budget.
+
+// Emit the low `len` bits of v (len <= 65: a 0 flag after a full word), cut at
+// the remaining budget.
+ZB_HD void emit(BitWriter& bw, uint64_t v, int len, int& bits) {
+    if (len > bits) { len = bits; v &= lowmask(len); }
+    if (len > 64) { bw.put(v, 64); bw.put(0, len - 64); }
+    else if (len > 0) bw.put(v, len);
+    bits -= len;
+}
+
 template <class PlaneAt>
 ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
-    int n = 0;                                 // significant coefficients so far
-    for (int k = 31; k >= 0 && bits > 0; --k) {
-        uint64_t x = plane_at(k);
-        int m = n < bits ? n : bits;           // first n bits verbatim
-        bw.put(x & lowmask(m), m);
-        bits -= m;
-        x = shr64(x, m);
-        while (n < 64 && bits > 0) {           // group tests over the rest
-            if (x == 0) { bw.put(0, 1); bits -= 1; break; }
-            bw.put(1, 1); bits -= 1;
-            int tz = ctz64(x);                 // zero run up to the next one
-            int cnt; uint64_t pat;
-            if (n + tz < 63) { cnt = tz + 1; pat = 1ull << tz; }
-            else { cnt = tz; pat = 0; }        // position 63 is implied, never sent
-            int e = cnt < bits ? cnt : bits;
-            bw.put(pat & lowmask(e), e);
-            bits -= e;
-            n += tz + 1;
-            x = shr64(x, tz + 1);
-        }
+    int k = 31, n = 0;
+    bool inplane = false;                      // group tests of plane k pending
+    uint64_t y = 0;                            // plane k above position n
+    while (k >= 0 && bits > 0) {
+        // plane start
+        const uint64_t x = plane_at(k);
+        const uint64_t yA = shr64(x, n);
+        const bool emptyA = n < 64 && yA == 0;
+        const bool doneA = n >= 64 || yA == 0;
+        const uint64_t vA = x & lowmask(n);
+        const int lenA = n + (emptyA ? 1 : 0);
+        // found one (y != 0 whenever inplane)
+        const int tz = ctz64(y | (1ull << 63));
+        const bool implied = n + tz >= 63;
+        const uint64_t yB = (y >> tz) >> 1;
+        const bool closeB = !implied && yB == 0;
+        const uint64_t vB = implied ? 1ull : (1ull | (2ull << (tz & 63)));
+        const int lenB = (implied ? tz + 1 : tz + 2) + (closeB ? 1 : 0);
+        const int nB = implied ? 64 : n + tz + 1;
+        // select
+        const uint64_t v = inplane ? vB : vA;
+        const int len = inplane ? lenB : lenA;
+        const bool done = inplane ? (implied || yB == 0) : doneA;
+        y = inplane ? yB : yA;
+        n = inplane ? nB : n;
+        emit(bw, v, len, bits);
+        k -= done ? 1 : 0;
+        inplane = !done;
     }
 }
 
-// Decodes under a budget of `bits` bits; PlaneSet(k, x) stores plane k.
+// 64 stream bits from the current position (bits past the block's budget are
+// garbage and never used)
+ZB_HD uint64_t peek64(const BitReader& br) {
+    const int w = br.pos >> 6, o = br.pos & 63;
+    const uint64_t lo = br.p[w] >> o;
+    return o ? (lo | (br.p[w + 1] << (64 - o))) : lo;
+}
+
 template <class PlaneSet>
 ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br) {
-    int n = 0;
-    for (int k = 31; k >= 0; --k) {
-        uint64_t x = 0;
-        if (bits > 0) {
-            int m = n < bits ? n : bits;
-            x = br.read(m);
-            bits -= m;
-            while (n < 64 && bits > 0) {
-                bits -= 1;
-                if (!br.read(1)) break;        // group empty
-                int L = 63 - n < bits ? 63 - n : bits;
-                uint64_t w = br.peek(L);
-                if (w) { int tz = ctz64(w); br.pos += tz + 1; bits -= tz + 1; n += tz; }
-                else   { br.pos += L; bits -= L; n += L; }
-                // a one at n: found, implied (n = 63), or budget ran out (zfp's rule)
-                x += 1ull << n;
-                n += 1;
-            }
-        }
-        plane_set(k, x);
+    int k = 31, n = 0;
+    bool inplane = false;                      // a 1 flag was read: scan pending
+    uint64_t x = 0;
+    while (k >= 0 && (bits > 0 || inplane)) {
+        const uint64_t w = peek64(br);
+        // plane start: n verbatim bits, then the first group flag
+        const int mA = n < bits ? n : bits;
+        const uint64_t xA = w & lowmask(mA);
+        const bool fA = n < 64 && bits - mA > 0;               // a flag follows
+        const bool contA = fA && ((w >> (mA & 63)) & 1ull);
+        const int cA = mA + (fA ? 1 : 0);
+        // found one: zero run (at most 63 - n bits, within the budget), deposit
+        // at n -- found, implied (n = 63) or budget end (zfp's rule) -- then the
+        // next group flag
+        const int L = 63 - n < bits ? 63 - n : bits;
+        const uint64_t sB = w & lowmask(L < 0 ? 0 : L);
+        const int r = sB ? ctz64(sB) : L;
+        const int c0 = sB ? r + 1 : L;
+        const int nB = n + r;
+        const uint64_t xB = x | (1ull << (nB & 63));
+        const bool fB = nB + 1 < 64 && bits - c0 > 0;
+        const bool contB = fB && ((w >> (c0 & 63)) & 1ull);
+        const int cB = c0 + (fB ? 1 : 0);
+        // select
+        x = inplane ? xB : xA;
+        n = inplane ? nB + 1 : n;
+        const int c = inplane ? cB : cA;
+        const bool cont = inplane ? contB : contA;
+        br.pos += c;
+        bits -= c;
+        if (!cont) { plane_set(k, x); --k; }
+        inplane = cont;
     }
+    for (; k >= 0; --k) plane_set(k, 0ull);
 }
 
 }  // namespace zb

@@ -129,7 +129,7 @@ def _stream(s) -> int | None:
 
 def _check(rc: int, ctx=None):
     if rc != OOCZ_OK:
-        msg = _lib.oocz_last_error(ctx).decode() if ctx else ""
+        msg = (_lib.oocz_last_error(ctx) or b"").decode()
         raise OoczError(rc, msg)
 
 

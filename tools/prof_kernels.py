@@ -1,0 +1,26 @@
+"""Launch each hot kernel on the C2 workload a few times (for ncu captures)."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2109_05410_b200 import oocz as Z  # noqa: E402
+from paper_2109_05410_b200 import synth  # noqa: E402
+
+n = 512
+planes = int(os.environ.get("PLANES", "160"))      # one slab: P + 2h
+rate = int(os.environ.get("RATE", "16"))
+u = torch.from_numpy(synth.dense(n, n, n, seed=1, z0=0, z1=planes)).cuda()
+m = torch.from_numpy(synth.layered(n, n, n, z0=0, z1=planes)).cuda()
+up = u.clone()
+words = torch.empty(Z.oocz_zfp_bytes(n, n, planes, rate) // 8, dtype=torch.int64, device="cuda")
+out = torch.empty_like(u)
+s = torch.cuda.current_stream()
+for _ in range(int(os.environ.get("REPS", "3"))):
+    Z.oocz_zfp_encode(u, n, n, planes, rate, words, s)
+    Z.oocz_zfp_decode(words, n, n, planes, rate, out, s)
+    Z.oocz_stencil_step_planes(u, up, m, n, n, planes, Z.default_coeffs(), 4, planes - 4, 0, planes, s)
+torch.cuda.synchronize()
+print("done")
