@@ -142,6 +142,26 @@ def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmu
         raise
 
 
+def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7) -> dict:
+    """Compressed run `a` vs the uncompressed run `b` after the same steps
+    (R18/R19): normwise max|a-b|/max|b| over the whole
+    field, and the paper's mean point-wise |a-b|/|b| over `per_plane` seeded
+    points per plane (|b| < 1e-30 skipped)."""
+    from paper_2109_05410_b200 import synth
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    normwise = float(np.abs(a64 - b64).max() / max(np.abs(b64).max(), 1e-300))
+    nz, ny, nx = b.shape
+    r = synth.uniforms(seed, 2 * per_plane * nz).reshape(nz, per_plane, 2)
+    ys = (r[..., 0] * ny).astype(np.int64)
+    xs = (r[..., 1] * nx).astype(np.int64)
+    zs = np.repeat(np.arange(nz), per_plane).reshape(nz, per_plane)
+    av, bv = a64[zs, ys, xs], b64[zs, ys, xs]
+    keep = np.abs(bv) >= 1e-30
+    mean_pw = float(np.mean(np.abs(av - bv)[keep] / np.abs(bv)[keep])) if keep.any() else 0.0
+    return {"normwise_max": normwise, "mean_pointwise": mean_pw, "points": int(keep.sum()),
+            "skipped": int((~keep).sum()), "vs": "same build, compression off (raw)"}
+
+
 def roofline(evs, peak_gbs, peak_src):
     """Dominant kernel of the timed region from the per-launch CUDA events."""
     from paper_2109_05410_b200.oocz import STAGES
@@ -201,6 +221,8 @@ def gpu_arm(args):
                           "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
                           "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
                           "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
+            if store == 1:   # final u^t, for the compressed-vs-raw error (same step count)
+                out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX), np.float32))
             Z.oocz_destroy(ctx)
     clocks = clk.summary()
     if rank != 0:
@@ -208,6 +230,8 @@ def gpu_arm(args):
             dist.destroy_process_group()
         return
     roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
+    err = rel_errors(out["zfp_dev"]["u"], out["raw_dev"]["u"])
+    err["steps"] = (args.warmup + args.steps) * T
     v, e = out["zfp_dev"], out["zfp_host"]
     line = {
         "metric": METRIC,
@@ -237,6 +261,7 @@ def gpu_arm(args):
         "speedup_zfp_vs_raw": {"value": round(v["cups"] / out["raw_dev"]["cups"], 3),
                                "e2e": round(e["cups"] / out["raw_host"]["cups"], 3),
                                "paper_context": "1.20x (fp64, V100-PCIe, PAPER.md:227)"},
+        "max_rel_error": err,
         "gpu_launches": int(v["launches"]),
         "roofline": roof,
         "kernels": table,

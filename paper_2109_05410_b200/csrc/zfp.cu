@@ -18,6 +18,8 @@ namespace oocz {
 namespace {
 
 constexpr int kThreads = 128;
+constexpr int kEncodeBlocksPerSM = 6;
+constexpr int kDecodeBlocksPerSM = 4;
 
 struct BlockPos { long long bx, by, bz; };
 
@@ -30,71 +32,59 @@ __device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
     return p;
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kEncodeBlocksPerSM)
 zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, uint64_t* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t smem[];
-    uint64_t* planes = smem;                       // [32][kThreads]
-    uint64_t* words = smem + 32 * kThreads;        // [kThreads][rate + 1]
+    __shared__ uint64_t planes[32 * kThreads];     // [plane][thread]: conflict-free
     const int t = threadIdx.x;
-    const int stride = rate + 1;
-    const long long b0 = (long long)blockIdx.x * kThreads;
-    const long long b = b0 + t;
+    const long long b = (long long)blockIdx.x * kThreads + t;
+    if (b >= nblocks) return;
 
-    if (b < nblocks) {
-        const BlockPos p = block_pos(b, nbx, nby);
-        const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
-        uint32_t v[64];
+    const BlockPos p = block_pos(b, nbx, nby);
+    const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+    uint32_t v[64];
 #pragma unroll
-        for (int k = 0; k < 4; k++)
+    for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
-                v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
-                v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
-                v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
-                v[16 * k + 4 * j + 3] = __float_as_uint(f.w);
-            }
-        zb::BitWriter bw{words + (size_t)t * stride, 0ull, 0, 0};
-        const int Emax = zb::block_exponent(v);
-        if (Emax < 0) {
-            bw.put(0, 1);                          // all-zero block: one 0 bit
-        } else {
-            const uint32_t e = (uint32_t)Emax + 1u; // emax + 127, emax = Emax - 126
-            bw.put(2u * e + 1u, zb::kHeaderBits);
-            int32_t q[64];
-#pragma unroll
-            for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
-            zb::fwd_xform(q);
-            constexpr int perm[64] = OOCZ_PERM3;
-            uint32_t lo[32], hi[32];
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
-                hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
-            }
-            zb::transpose32(lo);
-            zb::transpose32(hi);
-#pragma unroll
-            for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
-            zb::encode_planes([&](int k) { return planes[k * kThreads + t]; },
-                              64 * rate - zb::kHeaderBits, bw);
+        for (int j = 0; j < 4; j++) {
+            const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+            v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
+            v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
+            v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
+            v[16 * k + 4 * j + 3] = __float_as_uint(f.w);
         }
-        bw.finish(rate);
+    // the block's `rate` words are written straight to global memory: the warp's
+    // 32 streams are adjacent, so L2 merges the partial-sector writes
+    zb::BitWriter bw{out + (size_t)b * rate, 0ull, 0, 0};
+    const int Emax = zb::block_exponent(v);
+    if (Emax < 0) {
+        bw.put(0, 1);                              // all-zero block: one 0 bit
+    } else {
+        const uint32_t e = (uint32_t)Emax + 1u;    // emax + 127, emax = Emax - 126
+        bw.put(2u * e + 1u, zb::kHeaderBits);
+        int32_t q[64];
+#pragma unroll
+        for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+        zb::fwd_xform(q);
+        constexpr int perm[64] = OOCZ_PERM3;
+        uint32_t lo[32], hi[32];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
+            hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
+        }
+        zb::transpose32(lo);
+        zb::transpose32(hi);
+#pragma unroll
+        for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
+        zb::encode_planes([&](int k) { return planes[k * kThreads + t]; },
+                          64 * rate - zb::kHeaderBits, bw);
     }
-    __syncthreads();
-    // coalesced copy-out of this CTA's contiguous word range
-    const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
-    const int total = (int)nb * rate;
-    uint64_t* dst = out + (size_t)b0 * rate;
-    for (int w = t; w < total; w += kThreads) {
-        const int tt = w / rate, ww = w - tt * rate;
-        dst[w] = words[tt * stride + ww];
-    }
+    bw.finish(rate);
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, kDecodeBlocksPerSM)
 zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, float* __restrict__ out)
 {
@@ -175,16 +165,8 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    const size_t smem = codec_smem_bytes(rate);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(zfp_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)codec_smem_bytes(64));
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
     const long long grid = (nblocks + kThreads - 1) / kThreads;
-    zfp_encode_kernel<<<(unsigned)grid, kThreads, smem, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
+    zfp_encode_kernel<<<(unsigned)grid, kThreads, 0, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -202,37 +202,49 @@ ZB_HD void emit(BitWriter& bw, uint64_t v, int len, int& bits) {
     bits -= len;
 }
 
+// One encoder event.  State: plane index k, significant count n, whether the
+// group tests of plane k are under way, remaining budget.  The remaining plane
+// bits y = x >> n drive both alternatives:
+//   plane start : x & mask(n), then a 0 flag if y == 0 (plane done);
+//   found one   : tz = ctz(y): 1 | 2 << tz (tz + 2 bits; tz + 1 if the one is at
+//                 63, which is implied), then a closing 0 flag if y had a single
+//                 one left (y & (y - 1) == 0).
+struct EncState {
+    int k, n, bits;
+    bool inplane;
+    ZB_HD bool active() const { return k >= 0 && bits > 0; }
+};
+
+template <class PlaneAt>
+ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
+    const int n = st.n;
+    const uint64_t x = plane_at(st.k);
+    const uint64_t y = shr64(x, n);
+    const int tz = ctz64(y | 0x8000000000000000ull);
+    const bool implied = n + tz >= 63;
+    const bool lastone = (y & (y - 1ull)) == 0ull;
+    // found one
+    const uint64_t vB = implied ? 1ull : (1ull | (2ull << (tz & 63)));
+    const int lenB = implied ? tz + 1 : tz + 2 + (lastone ? 1 : 0);
+    const bool doneB = implied || lastone;
+    const int nB = implied ? 64 : n + tz + 1;
+    // plane start
+    const bool yz = y == 0ull;
+    const uint64_t vA = n >= 64 ? x : (x & ((1ull << (n & 63)) - 1ull));
+    const int lenA = n + ((n < 64 && yz) ? 1 : 0);
+    const bool doneA = n >= 64 || yz;
+    const bool ip = st.inplane;
+    emit(bw, ip ? vB : vA, ip ? lenB : lenA, st.bits);
+    const bool done = ip ? doneB : doneA;
+    st.n = ip ? nB : n;
+    st.k -= done ? 1 : 0;
+    st.inplane = !done;
+}
+
 template <class PlaneAt>
 ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
-    int k = 31, n = 0;
-    bool inplane = false;                      // group tests of plane k pending
-    uint64_t y = 0;                            // plane k above position n
-    while (k >= 0 && bits > 0) {
-        // plane start
-        const uint64_t x = plane_at(k);
-        const uint64_t yA = shr64(x, n);
-        const bool emptyA = n < 64 && yA == 0;
-        const bool doneA = n >= 64 || yA == 0;
-        const uint64_t vA = x & lowmask(n);
-        const int lenA = n + (emptyA ? 1 : 0);
-        // found one (y != 0 whenever inplane)
-        const int tz = ctz64(y | (1ull << 63));
-        const bool implied = n + tz >= 63;
-        const uint64_t yB = (y >> tz) >> 1;
-        const bool closeB = !implied && yB == 0;
-        const uint64_t vB = implied ? 1ull : (1ull | (2ull << (tz & 63)));
-        const int lenB = (implied ? tz + 1 : tz + 2) + (closeB ? 1 : 0);
-        const int nB = implied ? 64 : n + tz + 1;
-        // select
-        const uint64_t v = inplane ? vB : vA;
-        const int len = inplane ? lenB : lenA;
-        const bool done = inplane ? (implied || yB == 0) : doneA;
-        y = inplane ? yB : yA;
-        n = inplane ? nB : n;
-        emit(bw, v, len, bits);
-        k -= done ? 1 : 0;
-        inplane = !done;
-    }
+    EncState st{31, 0, bits, false};
+    while (st.active()) encode_event(st, plane_at, bw);
 }
 
 // 64 stream bits from the current position (bits past the block's budget are
@@ -243,42 +255,56 @@ ZB_HD uint64_t peek64(const BitReader& br) {
     return o ? (lo | (br.p[w + 1] << (64 - o))) : lo;
 }
 
+// One decoder event (state as EncState plus the plane being assembled):
+//   plane start : n verbatim bits, then the first group flag;
+//   found one   : the zero run -- r = ctz(w | ~0 << L) is the distance to the
+//                 next one, or L when there is none within the L = min(63 - n,
+//                 budget) scan bits -- the deposit at n + r (found, implied at 63,
+//                 or budget end: zfp's rule), then the next group flag.
+struct DecState {
+    int k, n, bits;
+    bool inplane;
+    uint64_t x;
+    ZB_HD bool active() const { return k >= 0 && (bits > 0 || inplane); }
+};
+
+template <class PlaneSet>
+ZB_HD void decode_event(DecState& st, BitReader& br, PlaneSet plane_set) {
+    const int n = st.n, bits = st.bits;
+    const uint64_t w = peek64(br);
+    // plane start
+    const int mA = n < bits ? n : bits;
+    const uint64_t xA = mA >= 64 ? w : (w & ((1ull << (mA & 63)) - 1ull));
+    const bool fA = n < 64 && bits > mA;
+    const bool contA = fA && ((w >> (mA & 63)) & 1ull);
+    const int cA = mA + (fA ? 1 : 0);
+    // found one
+    const int L = 63 - n < bits ? 63 - n : bits;
+    const int r = ctz64(w | (~0ull << (L & 63)));
+    const int c0 = r + (r < L ? 1 : 0);
+    const int nB = n + r;
+    const uint64_t xB = st.x | (1ull << (nB & 63));
+    const bool fB = nB < 63 && bits > c0;
+    const bool contB = fB && ((w >> (c0 & 63)) & 1ull);
+    const int cB = c0 + (fB ? 1 : 0);
+    // select
+    const bool ip = st.inplane;
+    const uint64_t x = ip ? xB : xA;
+    const int c = ip ? cB : cA;
+    const bool cont = ip ? contB : contA;
+    st.n = ip ? nB + 1 : n;
+    st.x = x;
+    br.pos += c;
+    st.bits = bits - c;
+    if (!cont) { plane_set(st.k, x); st.k -= 1; }
+    st.inplane = cont;
+}
+
 template <class PlaneSet>
 ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br) {
-    int k = 31, n = 0;
-    bool inplane = false;                      // a 1 flag was read: scan pending
-    uint64_t x = 0;
-    while (k >= 0 && (bits > 0 || inplane)) {
-        const uint64_t w = peek64(br);
-        // plane start: n verbatim bits, then the first group flag
-        const int mA = n < bits ? n : bits;
-        const uint64_t xA = w & lowmask(mA);
-        const bool fA = n < 64 && bits - mA > 0;               // a flag follows
-        const bool contA = fA && ((w >> (mA & 63)) & 1ull);
-        const int cA = mA + (fA ? 1 : 0);
-        // found one: zero run (at most 63 - n bits, within the budget), deposit
-        // at n -- found, implied (n = 63) or budget end (zfp's rule) -- then the
-        // next group flag
-        const int L = 63 - n < bits ? 63 - n : bits;
-        const uint64_t sB = w & lowmask(L < 0 ? 0 : L);
-        const int r = sB ? ctz64(sB) : L;
-        const int c0 = sB ? r + 1 : L;
-        const int nB = n + r;
-        const uint64_t xB = x | (1ull << (nB & 63));
-        const bool fB = nB + 1 < 64 && bits - c0 > 0;
-        const bool contB = fB && ((w >> (c0 & 63)) & 1ull);
-        const int cB = c0 + (fB ? 1 : 0);
-        // select
-        x = inplane ? xB : xA;
-        n = inplane ? nB + 1 : n;
-        const int c = inplane ? cB : cA;
-        const bool cont = inplane ? contB : contA;
-        br.pos += c;
-        bits -= c;
-        if (!cont) { plane_set(k, x); --k; }
-        inplane = cont;
-    }
-    for (; k >= 0; --k) plane_set(k, 0ull);
+    DecState st{31, 0, bits, false, 0ull};
+    while (st.active()) decode_event(st, br, plane_set);
+    for (int k = st.k; k >= 0; --k) plane_set(k, 0ull);
 }
 
 }  // namespace zb
