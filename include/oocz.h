@@ -91,7 +91,7 @@ enum { OOCZ_ST_H2D = 0, OOCZ_ST_DECODE = 1, OOCZ_ST_STENCIL = 2, OOCZ_ST_ENCODE 
  * "Roofline"): stencil 16 B per updated cell; decode/encode the compressed bytes
  * plus 4 B per value; copies and transfers the bytes moved. */
 typedef struct {
-    int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute, 2 = d2h, 3 = comm */
+    int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute, 2 = d2h, 3 = comm, 4 = decode */
     double   start_ms, end_ms;
     uint64_t bytes;
 } oocz_event;

@@ -15,10 +15,14 @@
 //    are exactly "the i-th remainder and the (i-1)-th common region" halves it
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
-//  * copies, codec and stencil overlap on three CUDA streams (Fig. 5).
+//  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
+//    compute (stencil + encode), d2h.  Blocks alternate between two slab sets,
+//    so the decode of block i+1 (integer-ALU bound) runs while block i's
+//    stencil (HBM bound) does.
 //
 // Device-side data layout (per rank):
-//   slab[f]   : (P + 2h) planes of nx*ny fp32, slab plane 0 = rank plane iP - h
+//   slab[s][f]: two sets (blocks alternate) of (P + 2h) planes of nx*ny fp32,
+//               slab plane 0 = rank plane iP - h
 //   ccopy[f]  : 2h planes, time-t copy of C_i (u, u-, m)
 //   in[slot]  : H2D staging of one read unit (3 fields), `slots` deep
 //   out[slot] : D2H staging of one write unit (2 read-write fields)
@@ -108,7 +112,7 @@ struct oocz_ctx {
 
     std::vector<Geom> geom;
     // device buffers
-    float* slab[3] = {nullptr, nullptr, nullptr};
+    float* slab[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
     float* ccopy[3] = {nullptr, nullptr, nullptr};
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
@@ -118,7 +122,9 @@ struct oocz_ctx {
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
     size_t store_bytes[3] = {0, 0, 0};
     // streams / events
-    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_decoded[2] = {nullptr, nullptr}, ev_slab_free[2] = {nullptr, nullptr};
+    cudaEvent_t ev_halo = nullptr, ev_join_dec = nullptr;
     std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written;
     long long seq = 0;                      // global block sequence number
     // halo exchange (world > 1)
@@ -354,7 +360,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     }
     // memory plan and budget check
     const size_t pb = ctx->plane_elems * sizeof(float);
-    size_t need = 3 * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
+    size_t need = 2 * 3 * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
     if (host) {
@@ -381,8 +387,10 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         }
     }
     for (int f = 0; f < 3; f++) {
-        CKC(cudaMalloc(&ctx->slab[f], (size_t)ctx->L * pb));
-        CKC(cudaMemset(ctx->slab[f], 0, (size_t)ctx->L * pb));
+        for (int k = 0; k < 2; k++) {
+            CKC(cudaMalloc(&ctx->slab[k][f], (size_t)ctx->L * pb));
+            CKC(cudaMemset(ctx->slab[k][f], 0, (size_t)ctx->L * pb));
+        }
         CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
     }
     CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
@@ -405,6 +413,13 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     ctx->stats.device_bytes_used = need;
     CKC(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&ctx->s_dec, cudaStreamNonBlocking));
+    for (int k = 0; k < 2; k++) {
+        CKC(cudaEventCreateWithFlags(&ctx->ev_decoded[k], cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&ctx->ev_slab_free[k], cudaEventDisableTiming));
+    }
+    CKC(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join_dec, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
     const int nslots = host ? cfg->slots : 1;
     auto mk = [&](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
@@ -489,10 +504,12 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     cudaSetDevice(ctx->device);
     if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamSynchronize(ctx->s_comp);
+    if (ctx->s_dec) cudaStreamSynchronize(ctx->s_dec);
     if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h);
     if (ctx->halo) halo_destroy(ctx->halo);
     for (int f = 0; f < 3; f++) {
-        cudaFree(ctx->slab[f]);
+        cudaFree(ctx->slab[0][f]);
+        cudaFree(ctx->slab[1][f]);
         cudaFree(ctx->ccopy[f]);
         if (ctx->cfg.store == OOCZ_STORE_HOST) cudaFreeHost(ctx->store[f]);
         else cudaFree(ctx->store[f]);
@@ -507,6 +524,13 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         if (e) cudaEventDestroy(e);
     if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
+    if (ctx->s_dec) cudaStreamDestroy(ctx->s_dec);
+    for (int k = 0; k < 2; k++) {
+        if (ctx->ev_decoded[k]) cudaEventDestroy(ctx->ev_decoded[k]);
+        if (ctx->ev_slab_free[k]) cudaEventDestroy(ctx->ev_slab_free[k]);
+    }
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+    if (ctx->ev_join_dec) cudaEventDestroy(ctx->ev_join_dec);
     if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
     delete ctx;
 }
@@ -550,7 +574,7 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src
     for (int z = 0; z < ctx->S; z += chunk) {
         const int np = std::min(chunk, ctx->S - z);
         const size_t n = (size_t)np * ctx->plane_elems;
-        float* buf = ctx->slab[field];
+        float* buf = ctx->slab[0][field];
         CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->plane_elems, n * sizeof(float),
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         CK(launch_scan_field(buf, n, ctx->d_flags, s));
@@ -618,7 +642,7 @@ static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, float* dst, size
         const size_t n = (size_t)np * ctx->plane_elems;
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
-        float* buf = ctx->slab[field];
+        float* buf = ctx->slab[0][field];
         if (host) {
             uint8_t* dev = ctx->in_slot[0];
             CK(cudaMemcpyAsync(dev, ctx->store[field] + off, bytes, cudaMemcpyHostToDevice, s));
@@ -652,16 +676,19 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
+    const int set = (int)(ctx->seq % 2);         // slab set of this block
+    float* const* slab = ctx->slab[set];
     const int rd_planes = g.rd1 - g.rd0;
     const uint8_t* src[3];
-    cudaStream_t sc = ctx->s_comp;
+    cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
+    // rows written back by blocks i and i+1 of the previous sweep must have landed
+    cudaEvent_t rows_final = ctx->ev_written[std::min(i + 1, D - 1)];
 
     // ---- (a2) H2D of the read unit (u, u-, m) into a staging slot
     if (host) {
         cudaStream_t sh = ctx->s_h2d;
         CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
-        // rows written back by blocks i and i+1 of the previous sweep must have landed
-        CK(cudaStreamWaitEvent(sh, ctx->ev_written[std::min(i + 1, D - 1)], 0));
+        CK(cudaStreamWaitEvent(sh, rows_final, 0));
         uint64_t bytes = 0;
         for (int f = 0; f < 3; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
         prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
@@ -674,50 +701,55 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
         prof_end(ctx, sh);
         ctx->stats.h2d_bytes += bytes;
         CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
-        CK(cudaStreamWaitEvent(sc, ctx->ev_in_ready[slot], 0));
+        CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
     } else {
+        CK(cudaStreamWaitEvent(sd, rows_final, 0));
         for (int f = 0; f < 3; f++) src[f] = ctx->store[f] + rows_off(ctx, f, g.rd0);
     }
 
-    // ---- (a4) slab assembly: time-t C_{i-1} from the previous block, halo from a neighbour rank
-    if (i > 0) {
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 3 * 2 * (uint64_t)(2 * h) * pb);
+    // ---- (a4) slab assembly on the decode stream, once this slab set is free
+    CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
+    if (i > 0) {  // time-t C_{i-1}, kept by the previous block
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, 3 * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < 3; f++)
-            CK(cudaMemcpyAsync(ctx->slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sc));
-        prof_end(ctx, sc);
+            CK(cudaMemcpyAsync(slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
+        prof_end(ctx, sd);
     }
-    if (ctx->halo) {
+    if (ctx->halo) {  // neighbour-rank halos received at the sweep start
         std::string herr;
-        if (!halo_insert(ctx->halo, i == 0, i == D - 1, ctx->slab, g.slab0, ctx->S, ctx->nx, ctx->ny, sc, &herr))
+        CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
+        if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, ctx->S, ctx->nx, ctx->ny, sd, &herr))
             return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
     }
     // ---- (a3) decode the read unit into the slab
     for (int f = 0; f < 3; f++) {
         // algorithmic bytes: compressed (or raw) read unit in + fp32 planes out
         const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
-        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 1, sc, bytes);
-        CK(decode_or_copy(ctx, f, src[f], rd_planes, ctx->slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sc));
-        prof_end(ctx, sc);
+        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
+        CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sd));
+        prof_end(ctx, sd);
     }
-    if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sc));
+    if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
     // keep the time-t C_i for block i+1 (reading R14)
     if (i < D - 1) {
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 3 * 2 * (uint64_t)(2 * h) * pb);
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, 3 * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < 3; f++)
-            CK(cudaMemcpyAsync(ctx->ccopy[f], ctx->slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
-                               cudaMemcpyDeviceToDevice, sc));
-        prof_end(ctx, sc);
+            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
+                               cudaMemcpyDeviceToDevice, sd));
+        prof_end(ctx, sd);
     }
+    CK(cudaEventRecord(ctx->ev_decoded[set], sd));
 
-    // ---- (a5) T cone-limited steps, in place, roles swapping
-    float* cu = ctx->slab[OOCZ_U];
-    float* cp = ctx->slab[OOCZ_UPREV];
+    // ---- (a5) T cone-limited steps, in place, roles swapping (compute stream)
+    CK(cudaStreamWaitEvent(sc, ctx->ev_decoded[set], 0));
+    float* cu = slab[OOCZ_U];
+    float* cp = slab[OOCZ_UPREV];
     for (int s = 1; s <= ts; s++) {
         const int z0 = std::max(4 * s, g.vlo);
         const int z1 = std::min(ctx->L - 4 * s, g.vhi);
         // algorithmic bytes: read u, u-, m and write u+ once per updated cell
         prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 16ull * (uint64_t)std::max(z1 - z0, 0) * ctx->plane_elems);
-        CK(launch_stencil_step(cu, cp, ctx->slab[OOCZ_M], ctx->nx, ctx->ny, ctx->L, ctx->cfg.c, z0, z1, g.vlo,
+        CK(launch_stencil_step(cu, cp, slab[OOCZ_M], ctx->nx, ctx->ny, ctx->L, ctx->cfg.c, z0, z1, g.vlo,
                                g.vhi, sc));
         prof_end(ctx, sc);
         std::swap(cu, cp);
@@ -737,26 +769,29 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
             CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], sc));
             prof_end(ctx, sc);
         }
+        CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
         CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
         // ---- (a7) D2H into the store, in place
-        cudaStream_t sd = ctx->s_d2h;
-        CK(cudaStreamWaitEvent(sd, ctx->ev_out_ready[slot], 0));
+        cudaStream_t so = ctx->s_d2h;
+        CK(cudaStreamWaitEvent(so, ctx->ev_out_ready[slot], 0));
         uint64_t bytes = 0;
         for (int f = 0; f < 2; f++) bytes += (uint64_t)(P / 4) * ctx->row_bytes[f];
-        prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, sd, bytes);
+        prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, so, bytes);
         for (int f = 0; f < 2; f++)
             CK(cudaMemcpyAsync(ctx->store[f] + rows_off(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
-                               (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, sd));
-        prof_end(ctx, sd);
+                               (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, so));
+        prof_end(ctx, so);
         ctx->stats.d2h_bytes += bytes;
-        CK(cudaEventRecord(ctx->ev_out_free[slot], sd));
-        CK(cudaEventRecord(ctx->ev_written[i], sd));
+        CK(cudaEventRecord(ctx->ev_out_free[slot], so));
+        CK(cudaEventRecord(ctx->ev_written[i], so));
     } else {
         for (int f = 0; f < 2; f++) {
             prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
             CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), sc));
             prof_end(ctx, sc);
         }
+        CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
+        CK(cudaEventRecord(ctx->ev_written[i], sc));
     }
     ctx->seq++;
     return OOCZ_OK;
@@ -777,6 +812,7 @@ static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
     *base = ctx->ev_t0;
     CK(cudaEventRecord(ctx->ev_t0, ctx->s_h2d));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_t0, 0));
+    CK(cudaStreamWaitEvent(ctx->s_dec, ctx->ev_t0, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_t0, 0));
     return OOCZ_OK;
 }
@@ -787,11 +823,14 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
     // join the three streams into s_d2h and stamp t1 there
     CK(cudaEventRecord(ctx->ev_join_h2d, ctx->s_h2d));
     CK(cudaEventRecord(ctx->ev_join_comp, ctx->s_comp));
+    CK(cudaEventRecord(ctx->ev_join_dec, ctx->s_dec));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_dec, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_h2d, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_comp, 0));
     CK(cudaEventRecord(ctx->ev_t1, ctx->s_d2h));
     CK(cudaStreamSynchronize(ctx->s_h2d));
     CK(cudaStreamSynchronize(ctx->s_comp));
+    CK(cudaStreamSynchronize(ctx->s_dec));
     CK(cudaStreamSynchronize(ctx->s_d2h));
     {
         float ms = 0;
@@ -846,6 +885,7 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
                 CK(cudaSetDevice(ctx->device));
                 if (!halo_sweep_begin(ctx->halo, ctx->s_comp, &herr))
                     return fail(ctx, OOCZ_ENCCL, "halo exchange: %s", herr.c_str());
+                CK(cudaEventRecord(ctx->ev_halo, ctx->s_comp));   // the decode stream inserts them
             }
         }
         for (int r = 0; r < n; r++) {

@@ -6,11 +6,15 @@
 // Format: zfp 0.5.5 fixed-rate layout; per-block logic in
 // zfp_block.cuh.
 //
-// Kernel shape: one thread per 4^3 block, 128 threads per CTA; consecutive
-// threads own consecutive bx, so the 16 float4 row loads / stores of a warp are
-// coalesced.  The 32 bit-plane words of each thread live in shared memory in a
-// [plane][thread] layout (conflict-free).  Compressed words are staged through
-// shared memory so that global traffic is coalesced in both kernels.
+// Kernel shape: one thread per 4^3 block (NB = 1 block per thread; NB = 2,
+// two interleaved event streams per thread, measured slower on B200: the
+// doubled shared memory halves occupancy).  Block b of the CTA's range is
+// owned by thread b % 128: consecutive threads own consecutive bx, so the
+// float4 row loads / stores of a warp are coalesced.  The 32
+// bit-plane words of each block live in shared memory in a [plane][thread]
+// layout (conflict-free).  The decoder stages its compressed words through
+// shared memory (coalesced loads); the encoder writes its words directly (the
+// warp's 32 streams are adjacent, so L2 merges the partial-sector writes).
 #include "common.cuh"
 #include "zfp_block.cuh"
 
@@ -18,8 +22,8 @@ namespace oocz {
 namespace {
 
 constexpr int kThreads = 128;
-constexpr int kEncodeBlocksPerSM = 6;
-constexpr int kDecodeBlocksPerSM = 4;
+constexpr int NB = 1;                       // blocks (event streams) per thread
+constexpr int kBlocksPerCTA = kThreads * NB;
 
 struct BlockPos { long long bx, by, bz; };
 
@@ -32,37 +36,43 @@ __device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
     return p;
 }
 
-__global__ void __launch_bounds__(kThreads, kEncodeBlocksPerSM)
+__global__ void __launch_bounds__(kThreads)
 zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, uint64_t* __restrict__ out)
 {
-    __shared__ uint64_t planes[32 * kThreads];     // [plane][thread]: conflict-free
+    extern __shared__ __align__(16) uint64_t smem[];   // [NB][32][kThreads]
     const int t = threadIdx.x;
-    const long long b = (long long)blockIdx.x * kThreads + t;
-    if (b >= nblocks) return;
+    const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
+    zb::BitWriter bw[NB];
+    zb::EncState st[NB];
 
-    const BlockPos p = block_pos(b, nbx, nby);
-    const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
-    uint32_t v[64];
 #pragma unroll
-    for (int k = 0; k < 4; k++)
+    for (int s = 0; s < NB; s++) {
+        const long long b = b0 + s * kThreads + t;
+        uint64_t* planes = smem + s * 32 * kThreads;
+        st[s] = zb::EncState{-1, 0, 0, false};
+        bw[s] = zb::BitWriter{out + (size_t)b * rate, 0ull, 0, 0};
+        if (b >= nblocks) continue;
+        const BlockPos p = block_pos(b, nbx, nby);
+        const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+        uint32_t v[64];
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
-            v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
-            v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
-            v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
-            v[16 * k + 4 * j + 3] = __float_as_uint(f.w);
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+                v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
+                v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
+                v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
+                v[16 * k + 4 * j + 3] = __float_as_uint(f.w);
+            }
+        const int Emax = zb::block_exponent(v);
+        if (Emax < 0) {
+            bw[s].put(0, 1);                           // all-zero block: one 0 bit
+            continue;
         }
-    // the block's `rate` words are written straight to global memory: the warp's
-    // 32 streams are adjacent, so L2 merges the partial-sector writes
-    zb::BitWriter bw{out + (size_t)b * rate, 0ull, 0, 0};
-    const int Emax = zb::block_exponent(v);
-    if (Emax < 0) {
-        bw.put(0, 1);                              // all-zero block: one 0 bit
-    } else {
-        const uint32_t e = (uint32_t)Emax + 1u;    // emax + 127, emax = Emax - 126
-        bw.put(2u * e + 1u, zb::kHeaderBits);
+        const uint32_t e = (uint32_t)Emax + 1u;        // emax + 127, emax = Emax - 126
+        bw[s].put(2u * e + 1u, zb::kHeaderBits);
         int32_t q[64];
 #pragma unroll
         for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
@@ -78,78 +88,124 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         zb::transpose32(hi);
 #pragma unroll
         for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
-        zb::encode_planes([&](int k) { return planes[k * kThreads + t]; },
-                          64 * rate - zb::kHeaderBits, bw);
+        st[s] = zb::EncState{31, 0, 64 * rate - zb::kHeaderBits, false};
     }
-    bw.finish(rate);
+    // interleaved event streams
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int s = 0; s < NB; s++) any |= st[s].active();
+        if (!any) break;
+#pragma unroll
+        for (int s = 0; s < NB; s++)
+            if (st[s].active()) {
+                const uint64_t* planes = smem + s * 32 * kThreads;
+                zb::encode_event(st[s], [&](int k) { return planes[k * kThreads + t]; }, bw[s]);
+            }
+    }
+#pragma unroll
+    for (int s = 0; s < NB; s++)
+        if (b0 + s * kThreads + t < nblocks) bw[s].finish(rate);
 }
 
-__global__ void __launch_bounds__(kThreads, kDecodeBlocksPerSM)
+__global__ void __launch_bounds__(kThreads)
 zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, float* __restrict__ out)
 {
     extern __shared__ __align__(16) uint64_t smem[];
-    uint64_t* planes = smem;                       // [32][kThreads]
-    uint64_t* words = smem + 32 * kThreads;        // [kThreads][rate + 1]
+    uint64_t* planes_all = smem;                       // [NB][32][kThreads]
+    uint64_t* words = smem + NB * 32 * kThreads;       // [NB*kThreads][rate + 1]
     const int t = threadIdx.x;
     const int stride = rate + 1;
-    const long long b0 = (long long)blockIdx.x * kThreads;
-    const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
-    {   // coalesced stage-in
+    const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
+    const long long nb = nblocks - b0 < kBlocksPerCTA ? nblocks - b0 : kBlocksPerCTA;
+    {   // coalesced stage-in of the CTA's contiguous word range
         const int total = (int)nb * rate;
         const uint64_t* src = in + (size_t)b0 * rate;
         for (int w = t; w < total; w += kThreads) {
-            const int tt = w / rate, ww = w - tt * rate;
-            words[tt * stride + ww] = __ldg(src + w);
+            const int bb = w / rate, ww = w - bb * rate;
+            words[bb * stride + ww] = __ldg(src + w);
         }
     }
     __syncthreads();
-    if (t >= nb) return;
 
-    const BlockPos p = block_pos(b0 + t, nbx, nby);
-    float* base = out + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
-    zb::BitReader br{words + (size_t)t * stride, 0};
-    if (!br.read(1)) {                             // zero block -> +0.0
+    zb::BitReader br[NB];
+    zb::DecState st[NB];
+    int emax[NB];
+    bool zero[NB];
+#pragma unroll
+    for (int s = 0; s < NB; s++) {
+        const int bb = s * kThreads + t;
+        br[s] = zb::BitReader{words + (size_t)bb * stride, 0};
+        st[s] = zb::DecState{-1, 0, 0, false, 0ull};
+        emax[s] = 0;
+        zero[s] = true;
+        if (bb >= nb) continue;
+        if (!br[s].read(1)) continue;                  // zero block
+        zero[s] = false;
+        emax[s] = (int)br[s].read(zb::kEBits) - 127;
+        st[s] = zb::DecState{31, 0, 64 * rate - zb::kHeaderBits, false, 0ull};
+    }
+    for (;;) {
+        bool any = false;
+#pragma unroll
+        for (int s = 0; s < NB; s++) any |= st[s].active();
+        if (!any) break;
+#pragma unroll
+        for (int s = 0; s < NB; s++)
+            if (st[s].active()) {
+                uint64_t* planes = planes_all + s * 32 * kThreads;
+                zb::decode_event(st[s], br[s], [&](int k, uint64_t x) { planes[k * kThreads + t] = x; });
+            }
+    }
+#pragma unroll
+    for (int s = 0; s < NB; s++) {
+        const int bb = s * kThreads + t;
+        if (bb >= nb) continue;
+        const BlockPos p = block_pos(b0 + bb, nbx, nby);
+        float* base = out + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+        if (zero[s]) {                                 // zero block -> +0.0
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+#pragma unroll
+                for (int j = 0; j < 4; j++)
+                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) = make_float4(0.f, 0.f, 0.f, 0.f);
+            continue;
+        }
+        uint64_t* planes = planes_all + s * 32 * kThreads;
+        for (int k = st[s].k; k >= 0; --k) planes[k * kThreads + t] = 0ull;   // planes past the budget
+        uint32_t lo[32], hi[32];
+#pragma unroll
+        for (int k = 0; k < 32; k++) {
+            const uint64_t x = planes[k * kThreads + t];
+            lo[k] = (uint32_t)x;
+            hi[k] = (uint32_t)(x >> 32);
+        }
+        zb::transpose32(lo);
+        zb::transpose32(hi);
+        constexpr int perm[64] = OOCZ_PERM3;
+        int32_t q[64];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            q[perm[i]] = (int32_t)((lo[i] ^ zb::kNBMask) - zb::kNBMask);
+            q[perm[i + 32]] = (int32_t)((hi[i] ^ zb::kNBMask) - zb::kNBMask);
+        }
+        zb::inv_xform(q);
 #pragma unroll
         for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int j = 0; j < 4; j++)
-                *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) = make_float4(0.f, 0.f, 0.f, 0.f);
-        return;
+            for (int j = 0; j < 4; j++) {
+                const int l = 16 * k + 4 * j;
+                *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
+                    make_float4(zb::dequantize(q[l], emax[s]), zb::dequantize(q[l + 1], emax[s]),
+                                zb::dequantize(q[l + 2], emax[s]), zb::dequantize(q[l + 3], emax[s]));
+            }
     }
-    const int emax = (int)br.read(zb::kEBits) - 127;
-    zb::decode_planes([&](int k, uint64_t x) { planes[k * kThreads + t] = x; },
-                      64 * rate - zb::kHeaderBits, br);
-    uint32_t lo[32], hi[32];
-#pragma unroll
-    for (int k = 0; k < 32; k++) {
-        const uint64_t x = planes[k * kThreads + t];
-        lo[k] = (uint32_t)x;
-        hi[k] = (uint32_t)(x >> 32);
-    }
-    zb::transpose32(lo);
-    zb::transpose32(hi);
-    constexpr int perm[64] = OOCZ_PERM3;
-    int32_t q[64];
-#pragma unroll
-    for (int i = 0; i < 32; i++) {
-        q[perm[i]] = (int32_t)((lo[i] ^ zb::kNBMask) - zb::kNBMask);
-        q[perm[i + 32]] = (int32_t)((hi[i] ^ zb::kNBMask) - zb::kNBMask);
-    }
-    zb::inv_xform(q);
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int l = 16 * k + 4 * j;
-            *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
-                make_float4(zb::dequantize(q[l], emax), zb::dequantize(q[l + 1], emax),
-                            zb::dequantize(q[l + 2], emax), zb::dequantize(q[l + 3], emax));
-        }
 }
 
-size_t codec_smem_bytes(int rate) {
-    return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * (rate + 1));
+size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
+size_t decode_smem_bytes(int rate) {
+    return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads + kBlocksPerCTA * (rate + 1));
 }
 
 bool codec_args_ok(int nx, int ny, int nz, int rate) {
@@ -165,8 +221,16 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    const long long grid = (nblocks + kThreads - 1) / kThreads;
-    zfp_encode_kernel<<<(unsigned)grid, kThreads, 0, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(zfp_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)encode_smem_bytes());
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
+    zfp_encode_kernel<<<(unsigned)grid, kThreads, encode_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
+                                                                           nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
 }
@@ -177,16 +241,16 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    const size_t smem = codec_smem_bytes(rate);
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(zfp_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)codec_smem_bytes(64));
+                                             (int)decode_smem_bytes(64));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const long long grid = (nblocks + kThreads - 1) / kThreads;
-    zfp_decode_kernel<<<(unsigned)grid, kThreads, smem, s>>>(in, nx, ny, nx / 4, ny / 4, nblocks, rate, out);
+    const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
+    zfp_decode_kernel<<<(unsigned)grid, kThreads, decode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
+                                                                               nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
 }

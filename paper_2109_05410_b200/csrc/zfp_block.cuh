@@ -22,9 +22,12 @@
 
 #if defined(__CUDACC__)
 #define ZB_HD __host__ __device__ __forceinline__
-#define ZB_UNROLL _Pragma("unroll")
 #else
 #define ZB_HD inline
+#endif
+#if defined(__CUDA_ARCH__)
+#define ZB_UNROLL _Pragma("unroll")
+#else
 #define ZB_UNROLL
 #endif
 
