@@ -108,10 +108,11 @@ def make_fields(rank: int, S: int):
     return u, u, m
 
 
-def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile):
+def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=T, block_planes=P, rate=list(rates), store=store,
+                                m_resident=m_resident,
                                 slots=2, profile=profile)
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
@@ -130,9 +131,8 @@ def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmu
         st = Z.oocz_get_stats(ctx)
         dev_s = st["last_step_device_ms"] / 1e3
         if dist:
-            t = torch.tensor([dev_s], dtype=torch.float64, device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            dev_s = float(t.item())
+            from paper_2109_05410_b200 import dist as D
+            dev_s = D.max_over_ranks(dist, dev_s, device="cuda")
         evs = Z.oocz_get_events(ctx) if profile else []
         # per-sweep bytes of the timed call only
         st_all = st
@@ -140,6 +140,47 @@ def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmu
     except Exception:
         Z.oocz_destroy(ctx)
         raise
+
+
+def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
+    """Each hot kernel alone on one block's slab (P + 2h planes of the C2 data),
+    CUDA events on the launching stream, L2 flushed between launches; achieved =
+    algorithmic bytes / median duration."""
+    import torch
+    planes = P + 8 * T
+    u = torch.from_numpy(np.ascontiguousarray(fields[0][:planes])).cuda()
+    m = torch.from_numpy(np.ascontiguousarray(fields[2][:planes])).cuda()
+    up = u.clone()
+    out = torch.empty_like(u)
+    words = torch.empty(Z.oocz_zfp_bytes(NX, NY, planes, RATE) // 8, dtype=torch.int64, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    s = torch.cuda.current_stream()
+
+    def med(fn):
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(s)
+            fn()
+            b.record(s)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b) / 1e3)
+        return sorted(ts)[len(ts) // 2]
+
+    cells = NX * NY * planes
+    cbytes = cells // 64 * 8 * RATE
+    upd = NX * NY * (planes - 8)
+    res = {}
+    for name, fn, nbytes in (
+            ("zfp_encode_kernel", lambda: Z.oocz_zfp_encode(u, NX, NY, planes, RATE, words, s), 4 * cells + cbytes),
+            ("zfp_decode_kernel", lambda: Z.oocz_zfp_decode(words, NX, NY, planes, RATE, out, s), 4 * cells + cbytes),
+            ("stencil25_kernel", lambda: Z.oocz_stencil_step_planes(u, up, m, NX, NY, planes, Z.default_coeffs(),
+                                                                    4, planes - 4, 0, planes, s), 16 * upd)):
+        t = med(fn)
+        res[name] = {"ms": round(t * 1e3, 4), "achieved_GBps": round(nbytes / t / 1e9, 1),
+                     "frac": round(nbytes / t / 1e9 / peak_gbs, 4), "algorithmic_bytes": int(nbytes)}
+    return res
 
 
 def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7) -> dict:
@@ -158,8 +199,11 @@ def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7
     av, bv = a64[zs, ys, xs], b64[zs, ys, xs]
     keep = np.abs(bv) >= 1e-30
     mean_pw = float(np.mean(np.abs(av - bv)[keep] / np.abs(bv)[keep])) if keep.any() else 0.0
+    sig = np.abs(bv) >= 1e-6 * np.abs(b64).max()     # points the wave has reached
+    mean_sig = float(np.mean(np.abs(av - bv)[sig] / np.abs(bv)[sig])) if sig.any() else 0.0
     return {"normwise_max": normwise, "mean_pointwise": mean_pw, "points": int(keep.sum()),
-            "skipped": int((~keep).sum()), "vs": "same build, compression off (raw)"}
+            "skipped": int((~keep).sum()), "mean_pointwise_significant": mean_sig,
+            "significant_points": int(sig.sum()), "vs": "same build, compression off (raw)"}
 
 
 def roofline(evs, peak_gbs, peak_src):
@@ -200,22 +244,22 @@ def gpu_arm(args):
         td.init_process_group("nccl", device_id=torch.device("cuda", local))
         dist = td
     from paper_2109_05410_b200 import oocz as Z
-    nccl_id = None
-    if world > 1:
-        idt = torch.zeros(128, dtype=torch.uint8, device="cuda")
-        if rank == 0:
-            idt.copy_(torch.frombuffer(bytearray(Z.oocz_get_nccl_id()), dtype=torch.uint8))
-        dist.broadcast(idt, 0)
-        nccl_id = bytes(idt.cpu().numpy().tolist())
+    from paper_2109_05410_b200 import dist as D
+    nccl_id = D.share_nccl_id(dist, rank, Z.oocz_get_nccl_id, device="cuda") if world > 1 else None
     fields = make_fields(rank, NZ)
     cells = NX * NY * NZ * world * T * args.steps
     peak_gbs, peak_src = peaks()
     out = {}
     with ClockSampler(local) as clk:
-        for label, store, rates in (("zfp_dev", 1, (RATE,) * 3), ("zfp_host", 0, (RATE,) * 3),
-                                    ("raw_dev", 1, (0, 0, 0)), ("raw_host", 0, (0, 0, 0))):
+        modes = [("zfp_dev", 1, (RATE,) * 3), ("zfp_host", 0, (RATE,) * 3),
+                 ("raw_dev", 1, (0, 0, 0)), ("raw_host", 0, (0, 0, 0))]
+        if not args.quick:   # configs[1]: rates 8/16/24
+            modes += [(f"r{r}_{k}", st, (r,) * 3) for r in (8, 24) for k, st in (("dev", 1), ("host", 0))]
+            modes += [("mres_dev", 1, (RATE,) * 3), ("mres_host", 0, (RATE,) * 3)]
+        for label, store, rates in modes:
             dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
-                                                     args.steps, args.warmup, dist, profile=int(label == "zfp_dev"))
+                                                     args.steps, args.warmup, dist, profile=int(label == "zfp_dev"),
+                                                     m_resident=int(label.startswith("mres")))
             sweeps_total = st["sweeps"]
             out[label] = {"s": dev_s, "cups": cells / dev_s, "launches": launches, "evs": evs,
                           "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
@@ -232,6 +276,23 @@ def gpu_arm(args):
     roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
     err = rel_errors(out["zfp_dev"]["u"], out["raw_dev"]["u"])
     err["steps"] = (args.warmup + args.steps) * T
+    orch = None
+    if "mres_dev" in out:
+        orch = {"what": "m decoded once and kept in HBM (m_resident=1): SURVEY 8(f) row 2, beyond the paper",
+                "value": round(out["mres_dev"]["cups"], 1), "e2e": round(out["mres_host"]["cups"], 1),
+                "e2e_h2d_bytes_per_step": int(out["mres_host"]["h2d_per_sweep"]),
+                "e2e_host_link_GBps": round(out["mres_host"]["h2d_per_sweep"] /
+                                            (out["mres_host"]["s"] / args.steps) / 1e9, 2)}
+    per_rate = {}
+    for r in (8, 24):
+        if f"r{r}_dev" in out:
+            er = rel_errors(out[f"r{r}_dev"]["u"], out["raw_dev"]["u"])
+            per_rate[str(r)] = {"value": round(out[f"r{r}_dev"]["cups"], 1),
+                                "e2e": round(out[f"r{r}_host"]["cups"], 1),
+                                "e2e_h2d_bytes_per_step": int(out[f"r{r}_host"]["h2d_per_sweep"]),
+                                "normwise_max_rel_error": er["normwise_max"],
+                                "mean_pointwise_rel_error": er["mean_pointwise"]}
+    iso = isolated_kernels(Z, fields, peak_gbs)
     v, e = out["zfp_dev"], out["zfp_host"]
     line = {
         "metric": METRIC,
@@ -264,7 +325,10 @@ def gpu_arm(args):
         "max_rel_error": err,
         "gpu_launches": int(v["launches"]),
         "roofline": roof,
-        "kernels": table,
+        "kernels_in_step": table,
+        "roofline_isolated": iso,
+        "other_rates": per_rate,
+        "orchestrated": orch,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
@@ -345,6 +409,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="rate 16 and raw only")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)

@@ -65,6 +65,10 @@ typedef struct {
     int32_t  slots;        /* staging slots per direction (>= 2); host store only             */
     int32_t  profile;      /* 1: record per-stage CUDA events (oocz_get_events)               */
     uint64_t device_bytes; /* device memory budget; 0 = whatever cudaMemGetInfo reports free  */
+    int32_t  m_resident;   /* 1: decode the read-only m ONCE into HBM (nx*ny*(nz/world + 8T)
+                              fp32) and keep it, instead of streaming and decoding it every
+                              sweep: orchestration beyond the paper (the
+                              paper's future work PAPER.md:254).  Results are identical.     */
 } oocz_config;
 
 typedef struct {

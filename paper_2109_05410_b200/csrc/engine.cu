@@ -114,6 +114,7 @@ struct oocz_ctx {
     // device buffers
     float* slab[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
     float* ccopy[3] = {nullptr, nullptr, nullptr};
+    float* m_full = nullptr;                // m_resident: decoded m, planes [-h, S + h)
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
     size_t in_slot_bytes = 0, out_slot_bytes = 0;
@@ -377,6 +378,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     for (int f = 0; f < 3; f++) ctx->store_bytes[f] = (size_t)(S / 4) * ctx->row_bytes[f];
     if (!host) need += ctx->store_bytes[0] + ctx->store_bytes[1] + ctx->store_bytes[2];
     if (world > 1) need += halo_device_bytes(ctx->plane_elems, h, cfg->rate, ctx->row_bytes);
+    if (cfg->m_resident) need += (size_t)(S + 2 * h) * pb;
     {
         size_t fr = 0, tot = 0;
         CKC(cudaMemGetInfo(&fr, &tot));
@@ -394,6 +396,10 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
     }
     CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
+    if (cfg->m_resident) {
+        CKC(cudaMalloc(&ctx->m_full, (size_t)(S + 2 * h) * pb));
+        CKC(cudaMemset(ctx->m_full, 0, (size_t)(S + 2 * h) * pb));
+    }
     if (host) {
         for (int s = 0; s < cfg->slots; s++) {
             uint8_t* a = nullptr;
@@ -517,6 +523,7 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     for (auto p : ctx->in_slot) cudaFree(p);
     for (auto p : ctx->out_slot) cudaFree(p);
     cudaFree(ctx->d_flags);
+    cudaFree(ctx->m_full);
     for (auto* v : {&ctx->ev_in_ready, &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free, &ctx->ev_written})
         for (auto e : *v) cudaEventDestroy(e);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
@@ -580,13 +587,18 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src
         CK(launch_scan_field(buf, n, ctx->d_flags, s));
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
+        const uint8_t* coded;
         if (host) {
             uint8_t* dev = ctx->in_slot[0];         // device staging of the encoded rows
             CK(encode_or_copy(ctx, field, buf, np, dev, s));
             CK(cudaMemcpyAsync(ctx->store[field] + off, dev, bytes, cudaMemcpyDeviceToHost, s));
+            coded = dev;
         } else {
             CK(encode_or_copy(ctx, field, buf, np, ctx->store[field] + off, s));
+            coded = ctx->store[field] + off;
         }
+        if (field == OOCZ_M && ctx->m_full)         // m_resident: keep the decoded RT(m)
+            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->plane_elems, s));
     }
     unsigned int flags[2] = {0, 0};
     CK(cudaMemcpyAsync(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost, s));
@@ -677,7 +689,10 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
     const int set = (int)(ctx->seq % 2);         // slab set of this block
-    float* const* slab = ctx->slab[set];
+    // m_resident: m is read in place from the decoded copy, never streamed
+    const int nf = ctx->m_full ? 2 : 3;
+    float* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
+                      ctx->m_full ? ctx->m_full + (size_t)(g.slab0 + h) * ctx->plane_elems : ctx->slab[set][2]};
     const int rd_planes = g.rd1 - g.rd0;
     const uint8_t* src[3];
     cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
@@ -690,9 +705,9 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
         CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
         CK(cudaStreamWaitEvent(sh, rows_final, 0));
         uint64_t bytes = 0;
-        for (int f = 0; f < 3; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
+        for (int f = 0; f < nf; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
         prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
-        for (int f = 0; f < 3; f++) {
+        for (int f = 0; f < nf; f++) {
             const size_t nbytes = (size_t)(rd_planes / 4) * ctx->row_bytes[f];
             CK(cudaMemcpyAsync(ctx->in_slot[slot] + ctx->in_off[f], ctx->store[f] + rows_off(ctx, f, g.rd0),
                                nbytes, cudaMemcpyHostToDevice, sh));
@@ -710,8 +725,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     // ---- (a4) slab assembly on the decode stream, once this slab set is free
     CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
     if (i > 0) {  // time-t C_{i-1}, kept by the previous block
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, 3 * 2 * (uint64_t)(2 * h) * pb);
-        for (int f = 0; f < 3; f++)
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
+        for (int f = 0; f < nf; f++)
             CK(cudaMemcpyAsync(slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
         prof_end(ctx, sd);
     }
@@ -722,7 +737,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
             return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
     }
     // ---- (a3) decode the read unit into the slab
-    for (int f = 0; f < 3; f++) {
+    for (int f = 0; f < nf; f++) {
         // algorithmic bytes: compressed (or raw) read unit in + fp32 planes out
         const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
@@ -732,8 +747,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
     // keep the time-t C_i for block i+1 (reading R14)
     if (i < D - 1) {
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, 3 * 2 * (uint64_t)(2 * h) * pb);
-        for (int f = 0; f < 3; f++)
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
+        for (int f = 0; f < nf; f++)
             CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
                                cudaMemcpyDeviceToDevice, sd));
         prof_end(ctx, sd);

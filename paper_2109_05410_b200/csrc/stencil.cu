@@ -38,8 +38,8 @@ constexpr int TX = 128, TY = 16;
 constexpr int SW = TX + 8, SH = TY + 8;          // u tile incl. halo
 constexpr int kUStageFloats = SW * SH;          // 3264 floats = 13056 B (128 B multiple)
 constexpr int kRStageFloats = 2 * TX * TY;      // u- tile then m tile, 16 KiB
-constexpr int NU = 8;                           // u ring stages
-constexpr int NR = 4;                           // u-/m ring stages
+constexpr int NU = 10;                          // u ring stages (5 ahead of the plane in use)
+constexpr int NR = 5;                           // u-/m ring stages
 constexpr int kConsumerWarps = TY;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr unsigned kUBytes = kUStageFloats * sizeof(float);
@@ -261,12 +261,19 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
         attr_set = true;
     }
     Coeffs cf{3.0f * c[0], c[1], c[2], c[3], c[4]};  // fl32(3 c0), as the oracle
-    // z chunk: aim for ~4 waves of one CTA per SM, between 16 and kMaxChunk planes
+    // z chunk: one CTA per SM, so pick the chunk count that minimises
+    // waves x (planes per chunk + halo cost); the 8 halo planes of a chunk are
+    // re-read mostly from L2 (weight 1/4)
     const long tiles = (long)((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
     const int nzu = z1 - z0;
-    long want = (tiles * nzu + 4L * kNumSMs - 1) / (4L * kNumSMs);
-    int chunk = (int)std::min<long>(kMaxChunk, std::max<long>(16, want));
-    chunk = std::min(chunk, nzu);
+    int chunk = std::min(nzu, kMaxChunk);
+    double best = 1e300;
+    for (int nch = (nzu + kMaxChunk - 1) / kMaxChunk; nch <= std::max(1, nzu / 12); nch++) {
+        const int c = (nzu + nch - 1) / nch;
+        const long waves = (tiles * ((nzu + c - 1) / c) + kNumSMs - 1) / kNumSMs;
+        const double cost = (double)waves * (c + 2.0);
+        if (cost < best - 1e-9) { best = cost; chunk = c; }
+    }
     dim3 grid((nx + TX - 1) / TX, (ny + TY - 1) / TY, (nzu + chunk - 1) / chunk);
     stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, zv0, cf);
     note_launches(1);

@@ -112,9 +112,8 @@ __global__ void __launch_bounds__(kThreads)
 zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, float* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t smem[];
-    uint64_t* planes_all = smem;                       // [NB][32][kThreads]
-    uint64_t* words = smem + NB * 32 * kThreads;       // [NB*kThreads][rate + 1]
+    __shared__ uint64_t planes_all[NB * 32 * kThreads];   // [NB][32][kThreads]
+    extern __shared__ __align__(16) uint64_t words[];      // [NB*kThreads][rate + 1] + 1 spare
     const int t = threadIdx.x;
     const int stride = rate + 1;
     const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
@@ -137,14 +136,14 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     for (int s = 0; s < NB; s++) {
         const int bb = s * kThreads + t;
         br[s] = zb::BitReader{words + (size_t)bb * stride, 0};
-        st[s] = zb::DecState{-1, 0, 0, false, 0ull};
+        st[s] = zb::DecState{-1, 0, 0, false, 0u, 0u};
         emax[s] = 0;
         zero[s] = true;
         if (bb >= nb) continue;
         if (!br[s].read(1)) continue;                  // zero block
         zero[s] = false;
         emax[s] = (int)br[s].read(zb::kEBits) - 127;
-        st[s] = zb::DecState{31, 0, 64 * rate - zb::kHeaderBits, false, 0ull};
+        st[s] = zb::DecState{31, 0, 64 * rate - zb::kHeaderBits, false, 0u, 0u};
     }
     for (;;) {
         bool any = false;
@@ -204,9 +203,9 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
 }
 
 size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
-size_t decode_smem_bytes(int rate) {
-    return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads + kBlocksPerCTA * (rate + 1));
-}
+// the 64-bit stream window reads up to one word past a block's last word: the
+// row padding, and one spare word after the last row
+size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(kBlocksPerCTA * (rate + 1) + 1); }
 
 bool codec_args_ok(int nx, int ny, int nz, int rate) {
     return nx >= 0 && ny >= 0 && nz >= 0 && nx % 4 == 0 && ny % 4 == 0 && nz % 4 == 0 &&

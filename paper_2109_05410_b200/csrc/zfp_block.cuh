@@ -250,15 +250,36 @@ ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
     while (st.active()) encode_event(st, plane_at, bw);
 }
 
-// 64 stream bits from the current position (bits past the block's budget are
-// garbage and never used)
-ZB_HD uint64_t peek64(const BitReader& br) {
-    const int w = br.pos >> 6, o = br.pos & 63;
-    const uint64_t lo = br.p[w] >> o;
-    return o ? (lo | (br.p[w + 1] << (64 - o))) : lo;
+// ---- 32-bit helpers: each is one or two SASS instructions on the device
+ZB_HD uint32_t fshr32(uint32_t lo, uint32_t hi, int s) {   // ((hi:lo) >> s) & 0xffffffff, 0 <= s < 32
+#if defined(__CUDA_ARCH__)
+    return __funnelshift_r(lo, hi, s);
+#else
+    return s ? (lo >> s) | (hi << (32 - s)) : lo;
+#endif
+}
+ZB_HD uint32_t bmask32(int m) {                            // low clamp(m, 0, 32) bits set
+#if defined(__CUDA_ARCH__)
+    uint32_t r;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(r) : "r"(m < 0 ? 0 : m));
+    return r;
+#else
+    return m <= 0 ? 0u : (m >= 32 ? ~0u : ((1u << m) - 1u));
+#endif
+}
+ZB_HD int ctz32nz(uint32_t x) {                            // x != 0
+#if defined(__CUDA_ARCH__)
+    return __ffs((int)x) - 1;
+#else
+    return __builtin_ctz(x);
+#endif
+}
+ZB_HD uint32_t bit64(uint32_t lo, uint32_t hi, int p) {    // bit p (0..63) of hi:lo
+    return (p < 32 ? fshr32(lo, hi, p) : (hi >> (p & 31))) & 1u;
 }
 
-// One decoder event (state as EncState plus the plane being assembled):
+// One decoder event on a 64-bit window wl:wh of the stream (three 32-bit
+// words funnel-shifted: no 64-bit shifts, no predication):
 //   plane start : n verbatim bits, then the first group flag;
 //   found one   : the zero run -- r = ctz(w | ~0 << L) is the distance to the
 //                 next one, or L when there is none within the L = min(63 - n,
@@ -267,45 +288,50 @@ ZB_HD uint64_t peek64(const BitReader& br) {
 struct DecState {
     int k, n, bits;
     bool inplane;
-    uint64_t x;
+    uint32_t xlo, xhi;               // plane k being assembled
     ZB_HD bool active() const { return k >= 0 && (bits > 0 || inplane); }
 };
 
 template <class PlaneSet>
 ZB_HD void decode_event(DecState& st, BitReader& br, PlaneSet plane_set) {
     const int n = st.n, bits = st.bits;
-    const uint64_t w = peek64(br);
+    const uint32_t* p32 = reinterpret_cast<const uint32_t*>(br.p) + (br.pos >> 5);
+    const int o = br.pos & 31;
+    const uint32_t w0 = p32[0], w1 = p32[1], w2 = p32[2];
+    const uint32_t wl = fshr32(w0, w1, o), wh = fshr32(w1, w2, o);
     // plane start
     const int mA = n < bits ? n : bits;
-    const uint64_t xA = mA >= 64 ? w : (w & ((1ull << (mA & 63)) - 1ull));
-    const bool fA = n < 64 && bits > mA;
-    const bool contA = fA && ((w >> (mA & 63)) & 1ull);
-    const int cA = mA + (fA ? 1 : 0);
+    const uint32_t aLo = wl & bmask32(mA), aHi = wh & bmask32(mA - 32);
+    const uint32_t fA = (uint32_t)(n < 64) & (uint32_t)(bits > mA);   // a flag follows
+    const uint32_t contA = fA & bit64(wl, wh, mA & 63);               // (no short-circuit branch)
+    const int cA = mA + (int)fA;
     // found one
     const int L = 63 - n < bits ? 63 - n : bits;
-    const int r = ctz64(w | (~0ull << (L & 63)));
+    const uint32_t tLo = wl | ~bmask32(L), tHi = wh | ~bmask32(L - 32);
+    const int r = tLo ? ctz32nz(tLo) : 32 + ctz32nz(tHi | 0x80000000u);
     const int c0 = r + (r < L ? 1 : 0);
     const int nB = n + r;
-    const uint64_t xB = st.x | (1ull << (nB & 63));
-    const bool fB = nB < 63 && bits > c0;
-    const bool contB = fB && ((w >> (c0 & 63)) & 1ull);
-    const int cB = c0 + (fB ? 1 : 0);
+    const uint32_t bLo = st.xlo | (nB < 32 ? 1u << (nB & 31) : 0u);
+    const uint32_t bHi = st.xhi | (nB >= 32 ? 1u << (nB & 31) : 0u);
+    const uint32_t fB = (uint32_t)(nB < 63) & (uint32_t)(bits > c0);
+    const uint32_t contB = fB & bit64(wl, wh, c0 & 63);
+    const int cB = c0 + (int)fB;
     // select
     const bool ip = st.inplane;
-    const uint64_t x = ip ? xB : xA;
+    st.xlo = ip ? bLo : aLo;
+    st.xhi = ip ? bHi : aHi;
     const int c = ip ? cB : cA;
-    const bool cont = ip ? contB : contA;
+    const bool cont = (ip ? contB : contA) != 0u;
     st.n = ip ? nB + 1 : n;
-    st.x = x;
     br.pos += c;
     st.bits = bits - c;
-    if (!cont) { plane_set(st.k, x); st.k -= 1; }
+    if (!cont) { plane_set(st.k, ((uint64_t)st.xhi << 32) | st.xlo); st.k -= 1; }
     st.inplane = cont;
 }
 
 template <class PlaneSet>
 ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br) {
-    DecState st{31, 0, bits, false, 0ull};
+    DecState st{31, 0, bits, false, 0u, 0u};
     while (st.active()) decode_event(st, br, plane_set);
     for (int k = st.k; k >= 0; --k) plane_set(k, 0ull);
 }

@@ -33,7 +33,7 @@ extern "C" int zb_encode_block(const float* x, int rate, uint64_t* out) {
 }
 
 extern "C" int zb_decode_block(const uint64_t* in_words, int rate, float* x) {
-    uint64_t in[65] = {0};                 // one spare word, as the kernel's smem staging has
+    uint64_t in[66] = {0};                 // spare words, as the kernel's smem staging has
     std::memcpy(in, in_words, sizeof(uint64_t) * (size_t)rate);
     BitReader br{in, 0};
     if (!br.read(1)) { for (int i = 0; i < 64; i++) x[i] = 0.0f; return 0; }

@@ -163,3 +163,44 @@ def test_slots_and_many_sweeps_pipelined():
         gu, gup, _, _ = _run_gpu(u, up, m, 2, 16, (16, 16, 16), 0, [40], slots=slots)
         ou, oup = _run_oracle(u, up, m, 2, (16, 16, 16), [40])
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), slots
+
+
+@pytest.mark.parametrize("store", [0, 1])
+@pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", [CASES[0], CASES[2], CASES[3], CASES[4]])
+def test_m_resident_matches_oracle(store, nx, ny, nz, T, P, rates, calls):
+    """Orchestration beyond the paper: m decoded once and
+    kept in HBM -- same bits, and no m bytes on the host link."""
+    z = Z()
+    u, up, m = _fields(nx, ny, nz, 3)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store, m_resident=1)
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        for n in calls:
+            s.step(n)
+        gu, gup, st = s.get(z.OOCZ_U), s.get(z.OOCZ_UPREV), s.stats()
+    ou, oup = _run_oracle(u, up, m, T, rates, calls)
+    assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+    if store == 0:
+        stored = [oracle.zfp_bytes(nx, ny, nz, r) if r else 4 * nx * ny * nz for r in rates]
+        assert st["h2d_bytes"] == st["sweeps"] * (stored[0] + stored[1])
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_m_resident_partitioned_group(world):
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 24, 128, 2, 16, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz, 5)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0, m_resident=1)
+    ctxs = z.oocz_create_local_group(cfg, world)
+    S = nz // world
+    try:
+        for r, c in enumerate(ctxs):
+            for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                z.oocz_set_field(c, f, a[r * S:(r + 1) * S])
+        z.oocz_step_local_group(ctxs, 7)
+        gu = np.concatenate([z.oocz_get_field(c, z.OOCZ_U, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+    finally:
+        for c in ctxs:
+            z.oocz_destroy(c)
+    ou, _ = _run_oracle(u, up, m, T, rates, [7])
+    assert np.array_equal(bits(gu), bits(ou))
