@@ -256,6 +256,10 @@ def gpu_arm(args):
         if not args.quick:   # configs[1]: rates 8/16/24
             modes += [(f"r{r}_{k}", st, (r,) * 3) for r in (8, 24) for k, st in (("dev", 1), ("host", 0))]
             modes += [("mres_dev", 1, (RATE,) * 3), ("mres_host", 0, (RATE,) * 3)]
+            # the paper's codes 2-4 as fp32 rate vectors, out of core:
+            # one read-write field (u-, reading R7) at 16/32, the read-only m at 16/32,
+            # one read-write field + m at 12/32 (the paper's 24/64)
+            modes += [("pm2_host", 0, (0, 16, 0)), ("pm3_host", 0, (0, 0, 16)), ("pm4_host", 0, (0, 12, 12))]
         for label, store, rates in modes:
             dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
                                                      args.steps, args.warmup, dist, profile=int(label == "zfp_dev"),
@@ -265,7 +269,8 @@ def gpu_arm(args):
                           "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
                           "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
                           "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
-            if store == 1:   # final u^t, for the compressed-vs-raw error (same step count)
+            if store == 1 or label.startswith("pm") or (label == "raw_host" and not args.quick):
+                # final u^t, for the compressed-vs-raw error (same step count)
                 out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX), np.float32))
             Z.oocz_destroy(ctx)
     clocks = clk.summary()
@@ -276,6 +281,19 @@ def gpu_arm(args):
     roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
     err = rel_errors(out["zfp_dev"]["u"], out["raw_dev"]["u"])
     err["steps"] = (args.warmup + args.steps) * T
+    paper_modes = None
+    if "pm2_host" in out:
+        ref = out["raw_host"]
+        paper_modes = {"what": "PAPER.md:212-215 codes as rate vectors (u, u-, m); out of core; "
+                               "speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, fp64, V100-PCIe)",
+                       "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1)}}
+        for key, lab, rates in (("2_rw_16", "pm2_host", [0, 16, 0]), ("3_ro_16", "pm3_host", [0, 0, 16]),
+                                ("4_rw_ro_12", "pm4_host", [0, 12, 12])):
+            er = rel_errors(out[lab]["u"], ref["u"])
+            paper_modes[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
+                                "speedup": round(out[lab]["cups"] / ref["cups"], 3),
+                                "normwise_max_rel_error": er["normwise_max"],
+                                "mean_pointwise_rel_error": er["mean_pointwise"]}
     orch = None
     if "mres_dev" in out:
         orch = {"what": "m decoded once and kept in HBM (m_resident=1): SURVEY 8(f) row 2, beyond the paper",
@@ -329,6 +347,7 @@ def gpu_arm(args):
         "roofline_isolated": iso,
         "other_rates": per_rate,
         "orchestrated": orch,
+        "paper_modes": paper_modes,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

@@ -7,7 +7,7 @@
 // it updates planes [z0, z1) of a z-slab in place (u+ overwrites u-).
 //
 // Design (HBM-bound: >= 16 B per cell-update: read u, u-, m, write u+):
-//  * CTA tile 128 (x) x 16 (y) cells marched along a z chunk; warp-specialised:
+//  * CTA tile 128 (x) x 16 (y) cells marched along z; warp-specialised:
 //    warp 0 is a TMA producer (one elected lane), warps 1..16 compute one row
 //    each, 4 consecutive x per thread.
 //  * Producer: cp.async.bulk.tensor.3d loads of
@@ -19,6 +19,10 @@
 //    full/empty mbarrier pairs per stage: consumers release a stage as soon as
 //    every consumer warp is done with it (no CTA-wide barrier per plane), so
 //    the producer stays 3 u planes / 3 u-,m planes ahead.
+//  * Persistent: one CTA per SM; work items (z chunk, tile) in chunk-major
+//    order, CTA b takes items b, b + G, ...: all CTAs stay in the same z chunk
+//    (halo rows hit in L2) and one continuous producer pipeline per CTA runs
+//    across items (no relaunch, no per-item pipeline drain).
 //  * Consumers: z-neighbours from a 9-deep float4 register queue (values, not
 //    partial sums, so the prescribed summation order is kept); x/y neighbours
 //    and u-, m from shared memory with 128-bit loads; u+ with 128-bit stores.
@@ -44,8 +48,7 @@ constexpr int kConsumerWarps = TY;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr unsigned kUBytes = kUStageFloats * sizeof(float);
 constexpr unsigned kRTileBytes = TX * TY * sizeof(float);
-constexpr size_t kSmemBytes = (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 128;
-constexpr int kMaxChunk = 64;
+constexpr size_t kSmemBytes = (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 2 * (NU + NR) * sizeof(uint64_t);
 
 struct Coeffs { float c0x3, c1, c2, c3, c4; };
 
@@ -79,21 +82,42 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// Work item `it` of the chunk-major enumeration (z chunk, tile): CTA b takes
+// items b, b + G, b + 2G, ... so at any time all CTAs work in the same z chunk
+// and a tile's radius-4 y/x halo rows are L2 hits from its neighbours' loads.
+struct Seg { int x0, y0, zb, ze; };
+
+__device__ __forceinline__ bool next_seg(long& it, long items, long tiles, int ntx, int z0, int z1, int chunk,
+                                         Seg& sg) {
+    if (it >= items) return false;
+    const long c = it / tiles, t = it - c * tiles;
+    sg.x0 = (int)(t % ntx) * TX;
+    sg.y0 = (int)(t / ntx) * TY;
+    sg.zb = z0 + (int)c * chunk;
+    sg.ze = min(sg.zb + chunk, z1);
+    it += gridDim.x;
+    return true;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
 stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
                  const __grid_constant__ CUtensorMap tm_m, float* __restrict__ uprev, int nx, int ny,
-                 int z0, int z1, int zchunk, int zv0, Coeffs cf)
+                 int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs cf)
 {
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* uring = reinterpret_cast<float*>((reinterpret_cast<uintptr_t>(smem_raw) + 127) & ~uintptr_t(127));
-    float* rring = uring + NU * kUStageFloats;
-    __shared__ __align__(8) uint64_t ufull[NU], uempty[NU], rfull[NR], rempty[NR];
+    // dynamic smem only (no static shared variables before it), 1024-aligned, and
+    // pointers derived from it directly so the compiler emits LDS, not generic LD
+    extern __shared__ __align__(1024) float smem_f[];
+    float* uring = smem_f;
+    float* rring = smem_f + NU * kUStageFloats;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_f + NU * kUStageFloats + NR * kRStageFloats);
+    uint64_t* ufull = bars;
+    uint64_t* uempty = bars + NU;
+    uint64_t* rfull = bars + 2 * NU;
+    uint64_t* rempty = bars + 2 * NU + NR;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int zb = z0 + blockIdx.z * zchunk;
-    const int ze = min(zb + zchunk, z1);
-    const int pfirst = zb - 4, plast = ze + 4;  // u planes needed: [pfirst, plast)
+    // persistent: items blockIdx.x, + gridDim.x, ... of (z chunk, tile)
+    const long items = tiles * ((z1 - z0 + chunk - 1) / chunk);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NU; s++) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], kConsumerWarps); }
@@ -104,23 +128,29 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer
+        // issues every segment's u planes [zb-4, ze+4) and u-/m planes [zb, ze)
+        // in consumption order; ring slots and phases follow global counters
+        // that run on across segments, so the pipeline never drains in between
         if (lane == 0) {
-            int jr = 0;
-            for (int i = 0; pfirst + i < plast; i++) {
-                const int p = pfirst + i;
-                const int s = i % NU;
-                if (i >= NU) mbar_wait(&uempty[s], ((i / NU) & 1) ^ 1);
-                mbar_expect_tx(&ufull[s], kUBytes);
-                tma_load_3d(uring + s * kUStageFloats, &tm_u, x0 - 4, y0 - 4, p - zv0, &ufull[s]);
-                const int z = p - 4;                       // u-, m of plane z go with u plane z+4
-                if (z >= zb && z < ze) {
-                    const int r = jr % NR;
-                    if (jr >= NR) mbar_wait(&rempty[r], ((jr / NR) & 1) ^ 1);
-                    mbar_expect_tx(&rfull[r], 2 * kRTileBytes);
-                    float* dst = rring + r * kRStageFloats;
-                    tma_load_3d(dst, &tm_up, x0, y0, z, &rfull[r]);
-                    tma_load_3d(dst + TX * TY, &tm_m, x0, y0, z, &rfull[r]);
-                    jr++;
+            long it = blockIdx.x;
+            unsigned gu = 0, gr = 0;
+            Seg sg;
+            while (next_seg(it, items, tiles, ntx, z0, z1, chunk, sg)) {
+                for (int p = sg.zb - 4; p < sg.ze + 4; p++, gu++) {
+                    const int s = gu % NU;
+                    if (gu >= NU) mbar_wait(&uempty[s], ((gu / NU) & 1) ^ 1);
+                    mbar_expect_tx(&ufull[s], kUBytes);
+                    tma_load_3d(uring + s * kUStageFloats, &tm_u, sg.x0 - 4, sg.y0 - 4, p - zv0, &ufull[s]);
+                    const int z = p - 4;                   // u-, m of plane z go with u plane z+4
+                    if (z >= sg.zb) {
+                        const int r = gr % NR;
+                        if (gr >= NR) mbar_wait(&rempty[r], ((gr / NR) & 1) ^ 1);
+                        mbar_expect_tx(&rfull[r], 2 * kRTileBytes);
+                        float* dst = rring + r * kRStageFloats;
+                        tma_load_3d(dst, &tm_up, sg.x0, sg.y0, z, &rfull[r]);
+                        tma_load_3d(dst + TX * TY, &tm_m, sg.x0, sg.y0, z, &rfull[r]);
+                        gr++;
+                    }
                 }
             }
         }
@@ -129,90 +159,102 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
 
     // ---------------------------------------------------------------- consumers
     const int ty = warp - 1;
-    const int gx = x0 + 4 * lane, gy = y0 + ty;
-    const bool active = gx < nx && gy < ny;
     const size_t plane = (size_t)nx * ny;
-    const size_t col = (size_t)gy * nx + gx;
     const int cidx = (ty + 4) * SW + 4 + 4 * lane;  // this thread's centre in a u stage
     const int ridx = ty * TX + 4 * lane;             // ... in a u- / m tile
+    long it = blockIdx.x;
+    unsigned gu0 = 0, gr0 = 0;                       // global index of the segment's first u / u- plane
+    Seg sg;
+    while (next_seg(it, items, tiles, ntx, z0, z1, chunk, sg)) {
+        const int zb = sg.zb, ze = sg.ze, pfirst = zb - 4;
+        const int gx = sg.x0 + 4 * lane, gy = sg.y0 + ty;
+        const bool active = gx < nx && gy < ny;
+        const size_t col = (size_t)gy * nx + gx;
+        auto uslot = [&](int p) { return (gu0 + (unsigned)(p - pfirst)) % NU; };
+        auto wait_u = [&](int p) -> const float* {
+            const unsigned g = gu0 + (unsigned)(p - pfirst);
+            mbar_wait(&ufull[g % NU], (g / NU) & 1);
+            return uring + (g % NU) * kUStageFloats;
+        };
+        auto release_u = [&](int p) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&uempty[uslot(p)]);
+        };
 
-    auto ustage = [&](int p) { return (p - pfirst) % NU; };
-    auto wait_u = [&](int p) -> const float* {
-        const int i = p - pfirst;
-        mbar_wait(&ufull[i % NU], (uint32_t)((i / NU) & 1));
-        return uring + (i % NU) * kUStageFloats;
-    };
-    auto release_u = [&](int p) {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&uempty[ustage(p)]);
-    };
-
-    float4 q[9];
+        float4 q[9];
 #pragma unroll
-    for (int i = 0; i < 8; i++) q[i] = *reinterpret_cast<const float4*>(wait_u(pfirst + i) + cidx);
+        for (int i = 0; i < 8; i++) q[i] = *reinterpret_cast<const float4*>(wait_u(pfirst + i) + cidx);
 #pragma unroll
-    for (int i = 0; i < 8; i++) {
-        const int p = pfirst + i;
-        if (p < zb || p >= ze) release_u(p);          // halo planes: centre was their only use
-    }
-
-    for (int z = zb; z < ze; z++) {
-        q[8] = *reinterpret_cast<const float4*>(wait_u(z + 4) + cidx);
-        const int j = z - zb;
-        mbar_wait(&rfull[j % NR], (uint32_t)((j / NR) & 1));
-        const float* rt = rring + (j % NR) * kRStageFloats;
-        const float4 upv = *reinterpret_cast<const float4*>(rt + ridx);
-        const float4 mv = *reinterpret_cast<const float4*>(rt + TX * TY + ridx);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&rempty[j % NR]);
-
-        const float* crow = uring + ustage(z) * kUStageFloats + cidx;  // plane z already landed
-        const float4 xl = *reinterpret_cast<const float4*>(crow - 4);
-        const float4 xr = *reinterpret_cast<const float4*>(crow + 4);
-        // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
-        // which is the first addition of the prescribed order anyway
-        float ay[4][4];
-#pragma unroll
-        for (int d = 1; d <= 4; d++) {
-            const float4 a = *reinterpret_cast<const float4*>(crow - d * SW);
-            const float4 b = *reinterpret_cast<const float4*>(crow + d * SW);
-            ay[d - 1][0] = __fadd_rn(a.x, b.x);
-            ay[d - 1][1] = __fadd_rn(a.y, b.y);
-            ay[d - 1][2] = __fadd_rn(a.z, b.z);
-            ay[d - 1][3] = __fadd_rn(a.w, b.w);
+        for (int i = 0; i < 8; i++) {
+            const int p = pfirst + i;
+            if (p < zb || p >= ze) release_u(p);      // halo planes: centre was their only use
         }
-        release_u(z);
-        if (z + 4 >= ze) release_u(z + 4);
 
-        const float4 uc = q[4];
-        const float w[12] = {xl.x, xl.y, xl.z, xl.w, uc.x, uc.y, uc.z, uc.w, xr.x, xr.y, xr.z, xr.w};
-        const float ucv[4] = {uc.x, uc.y, uc.z, uc.w};
-        const float upa[4] = {upv.x, upv.y, upv.z, upv.w};
-        const float ma[4] = {mv.x, mv.y, mv.z, mv.w};
-        float res[4];
-#pragma unroll
-        for (int o = 0; o < 4; o++) {
-            const float u0 = ucv[o];
-            float s[4];
+        for (int z = zb; z < ze; z++) {
+            q[8] = *reinterpret_cast<const float4*>(wait_u(z + 4) + cidx);
+            const unsigned g = gr0 + (unsigned)(z - zb);
+            const float* rt = rring + (g % NR) * kRStageFloats;
+            const float* crow = uring + uslot(z) * kUStageFloats + cidx;  // plane z already landed
+            const float4 xl = *reinterpret_cast<const float4*>(crow - 4);
+            const float4 xr = *reinterpret_cast<const float4*>(crow + 4);
+            // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
+            // which is the first addition of the prescribed order anyway
+            float ay[4][4];
 #pragma unroll
             for (int d = 1; d <= 4; d++) {
-                const float* zmd = reinterpret_cast<const float*>(&q[4 - d]);
-                const float* zpd = reinterpret_cast<const float*>(&q[4 + d]);
-                const float ax = __fadd_rn(w[4 + o - d], w[4 + o + d]);
-                const float az = __fadd_rn(zmd[o], zpd[o]);
-                s[d - 1] = __fadd_rn(__fadd_rn(ax, ay[d - 1][o]), az);
+                const float4 a = *reinterpret_cast<const float4*>(crow - d * SW);
+                const float4 b = *reinterpret_cast<const float4*>(crow + d * SW);
+                ay[d - 1][0] = __fadd_rn(a.x, b.x);
+                ay[d - 1][1] = __fadd_rn(a.y, b.y);
+                ay[d - 1][2] = __fadd_rn(a.z, b.z);
+                ay[d - 1][3] = __fadd_rn(a.w, b.w);
             }
-            float L = __fmul_rn(cf.c0x3, u0);
-            L = __fmaf_rn(cf.c1, s[0], L);
-            L = __fmaf_rn(cf.c2, s[1], L);
-            L = __fmaf_rn(cf.c3, s[2], L);
-            L = __fmaf_rn(cf.c4, s[3], L);
-            res[o] = __fmaf_rn(ma[o], L, __fmaf_rn(2.0f, u0, -upa[o]));
-        }
-        if (active)
-            *reinterpret_cast<float4*>(uprev + (size_t)z * plane + col) = make_float4(res[0], res[1], res[2], res[3]);
+            release_u(z);
+            if (z + 4 >= ze) release_u(z + 4);
+
+            const float4 uc = q[4];
+            const float w[12] = {xl.x, xl.y, xl.z, xl.w, uc.x, uc.y, uc.z, uc.w, xr.x, xr.y, xr.z, xr.w};
+            const float ucv[4] = {uc.x, uc.y, uc.z, uc.w};
+            float Lv[4];
 #pragma unroll
-        for (int i = 0; i < 8; i++) q[i] = q[i + 1];
+            for (int o = 0; o < 4; o++) {
+                const float u0 = ucv[o];
+                float sd[4];
+#pragma unroll
+                for (int d = 1; d <= 4; d++) {
+                    const float* zmd = reinterpret_cast<const float*>(&q[4 - d]);
+                    const float* zpd = reinterpret_cast<const float*>(&q[4 + d]);
+                    const float ax = __fadd_rn(w[4 + o - d], w[4 + o + d]);
+                    const float az = __fadd_rn(zmd[o], zpd[o]);
+                    sd[d - 1] = __fadd_rn(__fadd_rn(ax, ay[d - 1][o]), az);
+                }
+                float L = __fmul_rn(cf.c0x3, u0);
+                L = __fmaf_rn(cf.c1, sd[0], L);
+                L = __fmaf_rn(cf.c2, sd[1], L);
+                L = __fmaf_rn(cf.c3, sd[2], L);
+                L = __fmaf_rn(cf.c4, sd[3], L);
+                Lv[o] = L;
+            }
+            // u- and m are read only now, when they are needed
+            mbar_wait(&rfull[g % NR], (g / NR) & 1);
+            const float4 upv = *reinterpret_cast<const float4*>(rt + ridx);
+            const float4 mv = *reinterpret_cast<const float4*>(rt + TX * TY + ridx);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[g % NR]);
+            const float upa[4] = {upv.x, upv.y, upv.z, upv.w};
+            const float ma[4] = {mv.x, mv.y, mv.z, mv.w};
+            float res[4];
+#pragma unroll
+            for (int o = 0; o < 4; o++) res[o] = __fmaf_rn(ma[o], Lv[o], __fmaf_rn(2.0f, ucv[o], -upa[o]));
+            if (active)
+                *reinterpret_cast<float4*>(uprev + (size_t)z * plane + col) = make_float4(res[0], res[1], res[2], res[3]);
+            // shift the queue (an unroll by 9 to rotate by renaming measured slower:
+            // 9x the code, instruction-cache and register pressure)
+#pragma unroll
+            for (int i = 0; i < 8; i++) q[i] = q[i + 1];
+        }
+        gu0 += (unsigned)(ze - zb + 8);
+        gr0 += (unsigned)(ze - zb);
     }
 }
 
@@ -261,21 +303,25 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
         attr_set = true;
     }
     Coeffs cf{3.0f * c[0], c[1], c[2], c[3], c[4]};  // fl32(3 c0), as the oracle
-    // z chunk: one CTA per SM, so pick the chunk count that minimises
-    // waves x (planes per chunk + halo cost); the 8 halo planes of a chunk are
-    // re-read mostly from L2 (weight 1/4)
-    const long tiles = (long)((nx + TX - 1) / TX) * ((ny + TY - 1) / TY);
+    // persistent: one CTA per SM; the chunk count minimises the busiest CTA's
+    // load, ceil(items / G) x (planes per chunk + 2): the 8 halo planes of a
+    // chunk are mostly L2 hits (weight 1/4)
+    const int ntx = (nx + TX - 1) / TX;
+    const long tiles = (long)ntx * ((ny + TY - 1) / TY);
     const int nzu = z1 - z0;
-    int chunk = std::min(nzu, kMaxChunk);
+    int chunk = nzu;
     double best = 1e300;
-    for (int nch = (nzu + kMaxChunk - 1) / kMaxChunk; nch <= std::max(1, nzu / 12); nch++) {
+    for (int nch = 1; nch <= std::max(1, nzu / 8); nch++) {
         const int c = (nzu + nch - 1) / nch;
-        const long waves = (tiles * ((nzu + c - 1) / c) + kNumSMs - 1) / kNumSMs;
-        const double cost = (double)waves * (c + 2.0);
+        const long items = tiles * ((nzu + c - 1) / c);
+        const long per = (items + kNumSMs - 1) / kNumSMs;
+        const double cost = (double)per * (c + 2.0);
         if (cost < best - 1e-9) { best = cost; chunk = c; }
     }
-    dim3 grid((nx + TX - 1) / TX, (ny + TY - 1) / TY, (nzu + chunk - 1) / chunk);
-    stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, zv0, cf);
+    const long items = tiles * ((nzu + chunk - 1) / chunk);
+    const int grid = (int)std::min<long>(kNumSMs, items);
+    stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, ntx, tiles,
+                                                        zv0, cf);
     note_launches(1);
     return cudaGetLastError();
 }

@@ -196,60 +196,6 @@ struct BitReader {
 //                 sent), plus the closing flag 0 when no one is left.
 // The encoded stream is exactly the bit-serial coder's, cut at the budget.
 
-// Emit the low `len` bits of v (len <= 65: a 0 flag after a full word), cut at
-// the remaining budget.
-ZB_HD void emit(BitWriter& bw, uint64_t v, int len, int& bits) {
-    if (len > bits) { len = bits; v &= lowmask(len); }
-    if (len > 64) { bw.put(v, 64); bw.put(0, len - 64); }
-    else if (len > 0) bw.put(v, len);
-    bits -= len;
-}
-
-// One encoder event.  State: plane index k, significant count n, whether the
-// group tests of plane k are under way, remaining budget.  The remaining plane
-// bits y = x >> n drive both alternatives:
-//   plane start : x & mask(n), then a 0 flag if y == 0 (plane done);
-//   found one   : tz = ctz(y): 1 | 2 << tz (tz + 2 bits; tz + 1 if the one is at
-//                 63, which is implied), then a closing 0 flag if y had a single
-//                 one left (y & (y - 1) == 0).
-struct EncState {
-    int k, n, bits;
-    bool inplane;
-    ZB_HD bool active() const { return k >= 0 && bits > 0; }
-};
-
-template <class PlaneAt>
-ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
-    const int n = st.n;
-    const uint64_t x = plane_at(st.k);
-    const uint64_t y = shr64(x, n);
-    const int tz = ctz64(y | 0x8000000000000000ull);
-    const bool implied = n + tz >= 63;
-    const bool lastone = (y & (y - 1ull)) == 0ull;
-    // found one
-    const uint64_t vB = implied ? 1ull : (1ull | (2ull << (tz & 63)));
-    const int lenB = implied ? tz + 1 : tz + 2 + (lastone ? 1 : 0);
-    const bool doneB = implied || lastone;
-    const int nB = implied ? 64 : n + tz + 1;
-    // plane start
-    const bool yz = y == 0ull;
-    const uint64_t vA = n >= 64 ? x : (x & ((1ull << (n & 63)) - 1ull));
-    const int lenA = n + ((n < 64 && yz) ? 1 : 0);
-    const bool doneA = n >= 64 || yz;
-    const bool ip = st.inplane;
-    emit(bw, ip ? vB : vA, ip ? lenB : lenA, st.bits);
-    const bool done = ip ? doneB : doneA;
-    st.n = ip ? nB : n;
-    st.k -= done ? 1 : 0;
-    st.inplane = !done;
-}
-
-template <class PlaneAt>
-ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
-    EncState st{31, 0, bits, false};
-    while (st.active()) encode_event(st, plane_at, bw);
-}
-
 // ---- 32-bit helpers: each is one or two SASS instructions on the device
 ZB_HD uint32_t fshr32(uint32_t lo, uint32_t hi, int s) {   // ((hi:lo) >> s) & 0xffffffff, 0 <= s < 32
 #if defined(__CUDA_ARCH__)
@@ -276,6 +222,66 @@ ZB_HD int ctz32nz(uint32_t x) {                            // x != 0
 }
 ZB_HD uint32_t bit64(uint32_t lo, uint32_t hi, int p) {    // bit p (0..63) of hi:lo
     return (p < 32 ? fshr32(lo, hi, p) : (hi >> (p & 31))) & 1u;
+}
+
+// Emit the low `len` bits of v (len <= 65: a 0 flag after a full word), cut at
+// the remaining budget.
+ZB_HD void emit(BitWriter& bw, uint64_t v, int len, int& bits) {
+    if (len > bits) { len = bits; v &= lowmask(len); }
+    if (len > 64) { bw.put(v, 64); bw.put(0, len - 64); }
+    else if (len > 0) bw.put(v, len);
+    bits -= len;
+}
+
+// One encoder event.  State: plane index k, significant count n, whether the
+// group tests of plane k are under way, remaining budget.  The remaining plane
+// bits y = x >> n drive both alternatives:
+//   plane start : x & mask(n), then a 0 flag if y == 0 (plane done);
+//   found one   : tz = ctz(y): 1 | 2 << tz (tz + 2 bits; tz + 1 if the one is at
+//                 63, which is implied), then a closing 0 flag if y had a single
+//                 one left (y & (y - 1) == 0).
+struct EncState {
+    int k, n, bits;
+    bool inplane;
+    ZB_HD bool active() const { return k >= 0 && bits > 0; }
+};
+
+template <class PlaneAt>
+ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
+    const int n = st.n;
+    const uint64_t x = plane_at(st.k);
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    // y = x >> n on 32-bit halves (n in 0..64)
+    const uint32_t yl = n < 32 ? fshr32(xl, xh, n) : (n < 64 ? xh >> (n & 31) : 0u);
+    const uint32_t yh = n < 32 ? xh >> n : 0u;
+    const int tz = yl ? ctz32nz(yl) : 32 + ctz32nz(yh | 0x80000000u);
+    const bool implied = n + tz >= 63;
+    const bool lastone = yl ? ((yl & (yl - 1u)) == 0u && yh == 0u) : ((yh & (yh - 1u)) == 0u);
+    // found one: 1 | 2 << tz
+    const int t1 = tz + 1;
+    const uint32_t vBl = implied ? 1u : (1u | (t1 < 32 ? 1u << (t1 & 31) : 0u));
+    const uint32_t vBh = implied ? 0u : (t1 >= 32 ? 1u << (t1 & 31) : 0u);
+    const int lenB = implied ? tz + 1 : tz + 2 + (lastone ? 1 : 0);
+    const bool doneB = implied || lastone;
+    const int nB = implied ? 64 : n + t1;
+    // plane start: x & mask(n)
+    const bool yz = (yl | yh) == 0u;
+    const uint32_t vAl = xl & bmask32(n), vAh = xh & bmask32(n - 32);
+    const int lenA = n + ((n < 64 && yz) ? 1 : 0);
+    const bool doneA = n >= 64 || yz;
+    const bool ip = st.inplane;
+    const uint32_t vl = ip ? vBl : vAl, vh = ip ? vBh : vAh;
+    emit(bw, ((uint64_t)vh << 32) | vl, ip ? lenB : lenA, st.bits);
+    const bool done = ip ? doneB : doneA;
+    st.n = ip ? nB : n;
+    st.k -= done ? 1 : 0;
+    st.inplane = !done;
+}
+
+template <class PlaneAt>
+ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
+    EncState st{31, 0, bits, false};
+    while (st.active()) encode_event(st, plane_at, bw);
 }
 
 // One decoder event on a 64-bit window wl:wh of the stream (three 32-bit
