@@ -142,6 +142,57 @@ def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmu
         raise
 
 
+def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
+    """Measured host-link peak (the out-of-core roofline's denominator):
+    pinned cudaMemcpyAsync H2D alone, D2H alone, and both at once on two
+    streams (the pipeline's situation), CUDA events, best of `reps`."""
+    import torch
+    h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def run(h2d: bool, d2h: bool) -> float:
+        best = 0.0
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(s1)
+            s2.wait_event(e0)
+            if h2d:
+                with torch.cuda.stream(s1):
+                    d_a.copy_(h_in, non_blocking=True)
+            if d2h:
+                with torch.cuda.stream(s2):
+                    h_out.copy_(d_b, non_blocking=True)
+            e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e1.record(s1)
+            e2.record(s2)
+            torch.cuda.synchronize()
+            ms = max(e0.elapsed_time(e1), e0.elapsed_time(e2))
+            best = max(best, nbytes / (ms / 1e3) / 1e9)
+        return best
+
+    return {"h2d_GBps": round(run(True, False), 2), "d2h_GBps": round(run(False, True), 2),
+            "concurrent_per_direction_GBps": round(run(True, True), 2), "bytes": nbytes}
+
+
+def lanes_summary(evs) -> dict:
+    """Per-lane busy time over the profiled step (SPEC.md:352 'per-lane idle')."""
+    names = {0: "h2d", 1: "compute", 2: "d2h", 3: "comm", 4: "decode"}
+    if not evs:
+        return {}
+    t0 = min(e["start_ms"] for e in evs)
+    t1 = max(e["end_ms"] for e in evs)
+    out = {}
+    for lane in sorted({e["lane"] for e in evs}):
+        busy = sum(e["end_ms"] - e["start_ms"] for e in evs if e["lane"] == lane)
+        out[names.get(lane, str(lane))] = {"busy_ms": round(busy, 3), "busy_frac": round(busy / (t1 - t0), 3)}
+    out["span_ms"] = round(t1 - t0, 3)
+    return out
+
+
 def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
     """Each hot kernel alone on one block's slab (P + 2h planes of the C2 data),
     CUDA events on the launching stream, L2 flushed between launches; achieved =
@@ -249,6 +300,7 @@ def gpu_arm(args):
     fields = make_fields(rank, NZ)
     cells = NX * NY * NZ * world * T * args.steps
     peak_gbs, peak_src = peaks()
+    link = host_link_probe()
     out = {}
     with ClockSampler(local) as clk:
         modes = [("zfp_dev", 1, (RATE,) * 3), ("zfp_host", 0, (RATE,) * 3),
@@ -262,7 +314,8 @@ def gpu_arm(args):
             modes += [("pm2_host", 0, (0, 16, 0)), ("pm3_host", 0, (0, 0, 16)), ("pm4_host", 0, (0, 12, 12))]
         for label, store, rates in modes:
             dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
-                                                     args.steps, args.warmup, dist, profile=int(label == "zfp_dev"),
+                                                     args.steps, args.warmup, dist,
+                                                     profile=int(label in ("zfp_dev", "zfp_host")),
                                                      m_resident=int(label.startswith("mres")))
             sweeps_total = st["sweeps"]
             out[label] = {"s": dev_s, "cups": cells / dev_s, "launches": launches, "evs": evs,
@@ -334,7 +387,18 @@ def gpu_arm(args):
         "e2e": {"value": round(e["cups"], 1), "unit": "cell-updates/s",
                 "h2d_bytes_per_step": int(e["h2d_per_sweep"]), "d2h_bytes_per_step": int(e["d2h_per_sweep"]),
                 "path": "oocz_step with the store in pinned host memory (the paper's out-of-core path)",
-                "host_link_GBps": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9, 2)},
+                "host_link_GBps": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9, 2),
+                # the out-of-core roofline: bytes the method must move per sweep
+                # (region sharing: every stored byte once H2D, the read-write ones once
+                # D2H) over the measured concurrent pinned bandwidth, per direction
+                "roofline": {"bound": "host-link",
+                             "achieved": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9, 2),
+                             "peak": link["concurrent_per_direction_GBps"], "unit": "GB/s",
+                             "frac": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9 /
+                                           link["concurrent_per_direction_GBps"], 4),
+                             "peak_source": "measured in this run (bench.host_link_probe)"},
+                "host_link_probe": link,
+                "lanes": lanes_summary(e["evs"])},
         "raw": {"value": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1),
                 "e2e_h2d_bytes_per_step": int(out["raw_host"]["h2d_per_sweep"])},
         "speedup_zfp_vs_raw": {"value": round(v["cups"] / out["raw_dev"]["cups"], 3),
@@ -344,6 +408,7 @@ def gpu_arm(args):
         "gpu_launches": int(v["launches"]),
         "roofline": roof,
         "kernels_in_step": table,
+        "lanes": lanes_summary(v["evs"]),
         "roofline_isolated": iso,
         "other_rates": per_rate,
         "orchestrated": orch,

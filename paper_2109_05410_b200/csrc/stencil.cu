@@ -42,8 +42,19 @@ constexpr int TX = 128, TY = 16;
 constexpr int SW = TX + 8, SH = TY + 8;          // u tile incl. halo
 constexpr int kUStageFloats = SW * SH;          // 3264 floats = 13056 B (128 B multiple)
 constexpr int kRStageFloats = 2 * TX * TY;      // u- tile then m tile, 16 KiB
-constexpr int NU = 10;                          // u ring stages (5 ahead of the plane in use)
-constexpr int NR = 5;                           // u-/m ring stages
+#ifndef OOCZ_STENCIL_NU
+#define OOCZ_STENCIL_NU 10
+#endif
+#ifndef OOCZ_STENCIL_NR
+#define OOCZ_STENCIL_NR 5
+#endif
+constexpr int NU = OOCZ_STENCIL_NU;             // u ring stages (NU - 5 ahead of the plane in use)
+constexpr int NR = OOCZ_STENCIL_NR;             // u-/m ring stages
+static_assert(NU >= 6 && NR >= 2, "the u ring holds planes z..z+4 plus at least one in flight");
+#ifndef OOCZ_STENCIL_CTAS
+#define OOCZ_STENCIL_CTAS 148
+#endif
+constexpr int kStencilCTAs = OOCZ_STENCIL_CTAS;  // persistent CTAs (one per SM at most)
 constexpr int kConsumerWarps = TY;
 constexpr int kThreads = 32 * (1 + kConsumerWarps);
 constexpr unsigned kUBytes = kUStageFloats * sizeof(float);
@@ -182,12 +193,14 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
         };
 
         float4 q[9];
-#pragma unroll
-        for (int i = 0; i < 8; i++) q[i] = *reinterpret_cast<const float4*>(wait_u(pfirst + i) + cidx);
+        // centres of planes zb-4 .. zb+3; a plane outside [zb, ze) is released as soon
+        // as its centre is read (its only use), so the ring never needs more than
+        // 5 stages to get through this prologue
 #pragma unroll
         for (int i = 0; i < 8; i++) {
             const int p = pfirst + i;
-            if (p < zb || p >= ze) release_u(p);      // halo planes: centre was their only use
+            q[i] = *reinterpret_cast<const float4*>(wait_u(p) + cidx);
+            if (p < zb || p >= ze) release_u(p);
         }
 
         for (int z = zb; z < ze; z++) {
@@ -314,12 +327,12 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
     for (int nch = 1; nch <= std::max(1, nzu / 8); nch++) {
         const int c = (nzu + nch - 1) / nch;
         const long items = tiles * ((nzu + c - 1) / c);
-        const long per = (items + kNumSMs - 1) / kNumSMs;
+        const long per = (items + kStencilCTAs - 1) / kStencilCTAs;
         const double cost = (double)per * (c + 2.0);
         if (cost < best - 1e-9) { best = cost; chunk = c; }
     }
     const long items = tiles * ((nzu + chunk - 1) / chunk);
-    const int grid = (int)std::min<long>(kNumSMs, items);
+    const int grid = (int)std::min<long>(kStencilCTAs, items);
     stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, ntx, tiles,
                                                         zv0, cf);
     note_launches(1);

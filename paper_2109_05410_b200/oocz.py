@@ -15,7 +15,7 @@ import re
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "liboocz.so")
+LIB_PATH = os.environ.get("OOCZ_LIB", os.path.join(_HERE, "liboocz.so"))   # override: A/B builds only
 HEADER = os.path.join(os.path.dirname(_HERE), "include", "oocz.h")
 
 if not os.path.exists(LIB_PATH):
