@@ -108,22 +108,23 @@ def make_fields(rank: int, S: int):
     return u, u, m
 
 
-def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0):
+def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
+             tb=T):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
-    cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=T, block_planes=P, rate=list(rates), store=store,
+    cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident,
                                 slots=2, profile=profile)
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
             Z.oocz_set_field(ctx, f, a)
-        Z.oocz_step(ctx, warmup * T)
+        Z.oocz_step(ctx, warmup * tb)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         l0 = Z.oocz_kernel_launch_count()
-        Z.oocz_step(ctx, steps * T)
+        Z.oocz_step(ctx, steps * tb)
         launches = Z.oocz_kernel_launch_count() - l0
         torch.cuda.synchronize()
         if dist:
@@ -312,13 +313,19 @@ def gpu_arm(args):
             # one read-write field (u-, reading R7) at 16/32, the read-only m at 16/32,
             # one read-write field + m at 12/32 (the paper's 24/64)
             modes += [("pm2_host", 0, (0, 16, 0)), ("pm3_host", 0, (0, 0, 16)), ("pm4_host", 0, (0, 12, 12))]
+            # temporal-blocking depth: T = 8 and the paper's T = 12
+            # (PAPER.md:217), same P = 128: host bytes per step fall as 1/T, redundant
+            # stencil work grows as 4(T-1)/P
+            modes += [(f"t{t}_{k}", st, (RATE,) * 3) for t in (8, 12) for k, st in (("dev", 1), ("host", 0))]
         for label, store, rates in modes:
+            tb = int(label[1:label.index("_")]) if label.startswith("t") and label[1].isdigit() else T
             dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
                                                      args.steps, args.warmup, dist,
                                                      profile=int(label in ("zfp_dev", "zfp_host")),
-                                                     m_resident=int(label.startswith("mres")))
+                                                     m_resident=int(label.startswith("mres")), tb=tb)
             sweeps_total = st["sweeps"]
-            out[label] = {"s": dev_s, "cups": cells / dev_s, "launches": launches, "evs": evs,
+            cells_mode = cells // T * tb
+            out[label] = {"s": dev_s, "cups": cells_mode / dev_s, "launches": launches, "evs": evs,
                           "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
                           "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
                           "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
@@ -413,6 +420,11 @@ def gpu_arm(args):
         "other_rates": per_rate,
         "orchestrated": orch,
         "paper_modes": paper_modes,
+        "temporal_blocking": {f"T={t}": {"value": round(out[f"t{t}_dev"]["cups"], 1),
+                                         "e2e": round(out[f"t{t}_host"]["cups"], 1),
+                                         "e2e_h2d_bytes_per_step": int(out[f"t{t}_host"]["h2d_per_sweep"]),
+                                         "step": f"one sweep = {t} leapfrog steps"}
+                              for t in (8, 12) if f"t{t}_dev" in out} or None,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:

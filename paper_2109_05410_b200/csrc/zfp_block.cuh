@@ -138,6 +138,10 @@ ZB_HD int32_t quantize(uint32_t bits, int Emax) {
 ZB_HD float dequantize(int32_t q, int emax) {
     int64_t sb = (int64_t)(emax - 30 + 1023) << 52;
 #if defined(__CUDA_ARCH__)
+    // emax >= -96: every nonzero |fl32(q)| * 2^(emax-30) is >= 2^-126 (normal), so
+    // the fp32 product by a power of two is exact (or overflows exactly as the
+    // rounded fp64 product does): the same bits as the fp64 path, one FMUL
+    if (emax >= -96) return __fmul_rn(__int2float_rn(q), __int_as_float((emax - 30 + 127) << 23));
     double s = __longlong_as_double(sb);
     return __double2float_rn(__dmul_rn((double)__int2float_rn(q), s));
 #else
