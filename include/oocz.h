@@ -138,6 +138,17 @@ oocz_status oocz_step(oocz_ctx* ctx, int64_t nsteps);
 /* Decode this rank's slab of field f into dst (count floats). */
 oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, float* dst, size_t count);
 oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float* d_dst, size_t count);
+/* Checkpoint / restore.  Between oocz_step calls the
+ * compressed store IS the whole state; a decode -> encode round trip is not
+ * idempotent, so a faithful checkpoint keeps the compressed bytes.
+ * oocz_store_bytes: this rank's store size for field f (0 for a bad field).
+ * oocz_save_store copies it to host memory `dst` (exactly that many bytes);
+ * oocz_load_store replaces it from `src` and marks the field set; a context
+ * created with the same config then continues bit for bit (collective for
+ * world > 1: the halos are refreshed from the loaded stores). */
+size_t      oocz_store_bytes(const oocz_ctx* ctx, int32_t field);
+oocz_status oocz_save_store(oocz_ctx* ctx, int32_t field, void* dst, size_t bytes);
+oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void* src, size_t bytes);
 oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out);
 /* In-process z-partitioned group on ONE device: `world` contexts (ranks 0..world-1)
  * that exchange their halos with device copies instead of NCCL, stepped in

@@ -678,6 +678,65 @@ extern "C" oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float
     return get_field_impl(ctx, field, d_dst, count, true);
 }
 
+// ------------------------------------------------------------------ checkpoint
+extern "C" size_t oocz_store_bytes(const oocz_ctx* ctx, int32_t field)
+{
+    return (ctx && field >= 0 && field <= 2) ? ctx->store_bytes[field] : 0;
+}
+
+extern "C" oocz_status oocz_save_store(oocz_ctx* ctx, int32_t field, void* dst, size_t bytes)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+    if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
+    if (!ctx->field_set[field]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", field);
+    if (bytes != ctx->store_bytes[field] || (!dst && bytes))
+        return fail(ctx, OOCZ_EINVAL, "bytes (%zu) != store size (%zu)", bytes, ctx->store_bytes[field]);
+    CK(cudaSetDevice(ctx->device));
+    if (ctx->cfg.store == OOCZ_STORE_HOST) std::memcpy(dst, ctx->store[field], bytes);
+    else CK(cudaMemcpy(dst, ctx->store[field], bytes, cudaMemcpyDeviceToHost));
+    return OOCZ_OK;
+}
+
+extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void* src, size_t bytes)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+    if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
+    if (bytes != ctx->store_bytes[field] || (!src && bytes))
+        return fail(ctx, OOCZ_EINVAL, "bytes (%zu) != store size (%zu)", bytes, ctx->store_bytes[field]);
+    CK(cudaSetDevice(ctx->device));
+    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
+    cudaStream_t s = ctx->s_comp;
+    ctx->field_set[field] = false;
+    if (host) std::memcpy(ctx->store[field], src, bytes);
+    else CK(cudaMemcpy(ctx->store[field], src, bytes, cudaMemcpyHostToDevice));
+    if (field == OOCZ_M && ctx->m_full) {       // m_resident: decode the loaded stream once
+        for (int z = 0; z < ctx->S; z += ctx->P) {
+            const int np = std::min(ctx->P, ctx->S - z);
+            const size_t off = rows_off(ctx, field, z);
+            const uint8_t* coded = ctx->store[field] + off;
+            if (host) {
+                CK(cudaMemcpyAsync(ctx->in_slot[0], coded, (size_t)(np / 4) * ctx->row_bytes[field],
+                                   cudaMemcpyHostToDevice, s));
+                coded = ctx->in_slot[0];
+            }
+            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->plane_elems, s));
+        }
+        CK(cudaStreamSynchronize(s));
+    }
+    ctx->field_set[field] = true;
+    if (ctx->halo) {                            // the neighbours' halos come from the store
+        std::string herr;
+        const bool ok = field == OOCZ_M
+            ? halo_exchange_m(ctx->halo, ctx->store[OOCZ_M], host, ctx->S, ctx->row_bytes[OOCZ_M], s, &herr)
+            : halo_capture_store(ctx->halo, field, ctx->store[field], host, ctx->S, ctx->row_bytes[field], s, &herr);
+        if (!ok || cudaStreamSynchronize(s) != cudaSuccess)
+            return fail(ctx, OOCZ_ENCCL, "halo refresh: %s", herr.c_str());
+    }
+    return OOCZ_OK;
+}
+
 // ------------------------------------------------------------------ step
 // Enqueue one block of one sweep (ts steps).
 static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)

@@ -72,6 +72,9 @@ _SIGS = {
     "oocz_get_field": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_get_field_device": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_get_stats": (C.c_int, [_ctx_p, C.POINTER(oocz_stats)]),
+    "oocz_store_bytes": (C.c_size_t, [_ctx_p, _i32]),
+    "oocz_save_store": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
+    "oocz_load_store": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_create_local_group": (C.c_int, [C.POINTER(oocz_config), _i32, _i32, C.POINTER(_ctx_p)]),
     "oocz_step_local_group": (C.c_int, [C.POINTER(_ctx_p), _i32, C.c_int64]),
     "oocz_get_events": (C.c_int, [_ctx_p, C.POINTER(oocz_event), C.c_size_t, C.POINTER(C.c_size_t)]),
@@ -216,6 +219,21 @@ def oocz_get_field(ctx: int, field: int, dst: np.ndarray) -> np.ndarray:
 
 def oocz_get_field_device(ctx: int, field: int, d_dst, count: int) -> None:
     _check(_lib.oocz_get_field_device(ctx, field, _ptr(d_dst), count), ctx)
+
+
+def oocz_store_bytes(ctx: int, field: int) -> int:
+    return int(_lib.oocz_store_bytes(ctx, field))
+
+
+def oocz_save_store(ctx: int, field: int) -> np.ndarray:
+    buf = np.empty(oocz_store_bytes(ctx, field), np.uint8)
+    _check(_lib.oocz_save_store(ctx, field, buf.ctypes.data, buf.size), ctx)
+    return buf
+
+
+def oocz_load_store(ctx: int, field: int, data: np.ndarray) -> None:
+    a = np.ascontiguousarray(data, np.uint8)
+    _check(_lib.oocz_load_store(ctx, field, a.ctypes.data, a.size), ctx)
 
 
 def oocz_get_stats(ctx: int) -> dict:
