@@ -23,7 +23,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = ["zfp_ref.c", "stencil_ref.c", "ooc_emul.c"]
+_SRCS = ["zfp_ref.c", "zfp_ref64.c", "stencil_ref.c", "ooc_emul.c"]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -57,6 +57,7 @@ def lib():
             i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
             u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
             u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
+            i64p = np.ctypeslib.ndpointer(np.int64, flags="C_CONTIGUOUS")
             ci = C.c_int
             sig = {
                 "orc_exponent_max": (C.c_int32, [f32p]),
@@ -84,6 +85,23 @@ def lib():
                 "orc_advance": (ci, [f32p, f32p, f32p, ci, ci, ci, f32p, ci, i32p, C.c_long]),
                 "orc_ooc_emulate": (ci, [f32p, f32p, f32p, ci, ci, ci, f32p, ci, ci, ci, i32p,
                                          C.c_long, ci, u64p]),
+                "orc64_exponent_max": (C.c_int32, [f64p]),
+                "orc64_fwd_cast": (None, [f64p, ci, i64p]),
+                "orc64_inv_cast": (None, [i64p, ci, f64p]),
+                "orc64_fwd_lift": (None, [i64p]),
+                "orc64_inv_lift": (None, [i64p]),
+                "orc64_fwd_xform": (None, [i64p]),
+                "orc64_inv_xform": (None, [i64p]),
+                "orc64_int2uint": (C.c_uint64, [C.c_int64]),
+                "orc64_uint2int": (C.c_int64, [C.c_uint64]),
+                "orc64_encode_ints": (ci, [u64p, ci, u64p, ci]),
+                "orc64_decode_ints": (ci, [u64p, ci, ci, u64p]),
+                "orc64_encode_block": (ci, [f64p, ci, u64p]),
+                "orc64_decode_block": (ci, [u64p, ci, f64p]),
+                "orc64_zfp_encode": (ci, [f64p, ci, ci, ci, ci, u64p]),
+                "orc64_zfp_decode": (ci, [u64p, ci, ci, ci, ci, f64p]),
+                "orc64_roundtrip": (ci, [f64p, ci, ci, ci, ci]),
+                "orc64_advance": (ci, [f64p, f64p, f64p, ci, ci, ci, f64p, ci, i32p, C.c_long]),
             }
             for name, (res, args) in sig.items():
                 fn = getattr(L, name)
@@ -279,3 +297,125 @@ def ooc_emulate(u0, uprev0, m0, T: int, P: int, G: int, rates, nsteps: int,
     if rc:
         raise ValueError("orc_ooc_emulate: bad arguments")
     return u, up, {"h2d": int(stats[0]), "d2h": int(stats[1]), "halo": int(stats[2])}
+
+
+# ---------------------------------------------------------------- fp64 (zfp_ref64.c)
+C64 = np.array([-205 / 72, 8 / 5, -1 / 5, 8 / 315, -1 / 560], np.float64)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def exponent_max64(block64) -> int:
+    return int(lib().orc64_exponent_max(_f64(block64).reshape(64)))
+
+
+def fwd_cast64(block64, emax):
+    q = np.zeros(64, np.int64)
+    lib().orc64_fwd_cast(_f64(block64).reshape(64), int(emax), q)
+    return q
+
+
+def inv_cast64(q, emax):
+    x = np.zeros(64, np.float64)
+    lib().orc64_inv_cast(np.ascontiguousarray(q, np.int64), int(emax), x)
+    return x
+
+
+def fwd_lift64(v):
+    v = np.array(v, dtype=np.int64).copy()
+    lib().orc64_fwd_lift(v)
+    return v
+
+
+def inv_lift64(v):
+    v = np.array(v, dtype=np.int64).copy()
+    lib().orc64_inv_lift(v)
+    return v
+
+
+def fwd_xform64(q):
+    q = np.array(q, dtype=np.int64).reshape(64).copy()
+    lib().orc64_fwd_xform(q)
+    return q
+
+
+def inv_xform64(q):
+    q = np.array(q, dtype=np.int64).reshape(64).copy()
+    lib().orc64_inv_xform(q)
+    return q
+
+
+def int2uint64(x: int) -> int:
+    return int(lib().orc64_int2uint(int(np.int64(x))))
+
+
+def uint2int64(u: int) -> int:
+    return int(lib().orc64_uint2int(int(u) & 0xFFFFFFFFFFFFFFFF))
+
+
+def encode_block64(block64, rate: int):
+    out = np.zeros(rate, np.uint64)
+    used = lib().orc64_encode_block(_f64(block64).reshape(64), int(rate), out)
+    return out, int(used)
+
+
+def decode_block64(words, rate: int):
+    x = np.zeros(64, np.float64)
+    used = lib().orc64_decode_block(np.ascontiguousarray(words, np.uint64), int(rate), x)
+    return x, int(used)
+
+
+def encode_ints64(u, budget_bits: int):
+    u = np.ascontiguousarray(u, np.uint64)
+    words = np.zeros((budget_bits + 63) // 64 + 1, np.uint64)
+    used = lib().orc64_encode_ints(u, int(budget_bits), words, 0)
+    return words, int(used)
+
+
+def decode_ints64(words, budget_bits: int):
+    u = np.zeros(64, np.uint64)
+    used = lib().orc64_decode_ints(np.ascontiguousarray(words, np.uint64), 0, int(budget_bits), u)
+    return u, int(used)
+
+
+def zfp_encode64(field, rate: int) -> np.ndarray:
+    f = _f64(field)
+    nx, ny, nz = _shape3(f)
+    out = np.zeros(zfp_bytes(nx, ny, nz, rate) // 8, np.uint64)
+    if lib().orc64_zfp_encode(f, nx, ny, nz, int(rate), out):
+        raise ValueError("orc64_zfp_encode: bad arguments")
+    return out
+
+
+def zfp_decode64(words, shape, rate: int) -> np.ndarray:
+    nz, ny, nx = shape
+    f = np.zeros((nz, ny, nx), np.float64)
+    if lib().orc64_zfp_decode(np.ascontiguousarray(words, np.uint64), nx, ny, nz, int(rate), f):
+        raise ValueError("orc64_zfp_decode: bad arguments")
+    return f
+
+
+def roundtrip64(field, rate: int) -> np.ndarray:
+    f = _f64(field).copy()
+    nx, ny, nz = _shape3(f)
+    if lib().orc64_roundtrip(f, nx, ny, nz, int(rate)):
+        raise ValueError("orc64_roundtrip: bad arguments")
+    return f
+
+
+def advance64(u, uprev, m, T: int, rates, nsteps: int, c=None):
+    u, uprev, m = _f64(u).copy(), _f64(uprev).copy(), _f64(m)
+    c = C64 if c is None else _f64(c)
+    nx, ny, nz = _shape3(u)
+    r = np.array(list(rates), np.int32)
+    if lib().orc64_advance(u, uprev, m, nx, ny, nz, c, int(T), r, int(nsteps)):
+        raise ValueError("orc64_advance: bad arguments")
+    return u, uprev
+
+
+def run64(u0, uprev0, m0, T: int, rates, nsteps: int, c=None):
+    """fp64 twin of run(): set_field round trips, then step(nsteps)."""
+    return advance64(roundtrip64(u0, rates[0]), roundtrip64(uprev0, rates[1]), roundtrip64(m0, rates[2]),
+                     T, rates, nsteps, c)

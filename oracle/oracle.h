@@ -55,6 +55,26 @@ int    orc_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int rate, floa
 /* RT_r(.) = decode(encode(.)), in place; identity for rate == 0 (raw) */
 int    orc_roundtrip(float* f, int nx, int ny, int nz, int rate);
 
+/* ---------------- the same codec for fp64 (zfp_ref64.c) ----------------
+ * The paper's precision and rates (32/64, 24/64: PAPER.md:213-215):
+ * EBITS 11, EBIAS 1023, 64 bit planes, q = trunc(x * 2^(62 - emax)). */
+int32_t  orc64_exponent_max(const double x[64]);
+void     orc64_fwd_cast(const double x[64], int emax, int64_t q[64]);
+void     orc64_inv_cast(const int64_t q[64], int emax, double x[64]);
+void     orc64_fwd_lift(int64_t v[4]);
+void     orc64_inv_lift(int64_t v[4]);
+void     orc64_fwd_xform(int64_t q[64]);
+void     orc64_inv_xform(int64_t q[64]);
+uint64_t orc64_int2uint(int64_t x);
+int64_t  orc64_uint2int(uint64_t u);
+int orc64_encode_ints(const uint64_t u[64], int budget_bits, uint64_t* words, int bit_offset);
+int orc64_decode_ints(const uint64_t* words, int bit_offset, int budget_bits, uint64_t u[64]);
+int orc64_encode_block(const double x[64], int rate, uint64_t* out);
+int orc64_decode_block(const uint64_t* in, int rate, double x[64]);
+int orc64_zfp_encode(const double* f, int nx, int ny, int nz, int rate, uint64_t* out);
+int orc64_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int rate, double* f);
+int orc64_roundtrip(double* f, int nx, int ny, int nz, int rate);
+
 /* ---------------- 25-point leapfrog (stencil_ref.c) ----------------
  * PAPER.md:208 (Sec. VI: 25-point acoustic propagator, two read-write
  * datasets, one write-only intermediate, one read-only dataset),
@@ -75,6 +95,9 @@ void orc_step_planes(const float* u, const float* uprev, const float* m, float* 
  * (set_field's round trip of all three fields is orc_roundtrip, done by the caller.) */
 int orc_advance(float* u, float* uprev, const float* m, int nx, int ny, int nz,
                 const float c[5], int T, const int rate[3], long nsteps);
+/* the same schedule in fp64 (orc_step_f64 + orc64_roundtrip) */
+int orc64_advance(double* u, double* uprev, const double* m, int nx, int ny, int nz,
+                  const double c[5], int T, const int rate[3], long nsteps);
 
 /* ---------------- literal out-of-core emulator (ooc_emul.c) ----------------
  * PAPER.md:112-113 (Sec. III region sharing), PAPER.md:130-160 (Sec. V.A,
