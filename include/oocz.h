@@ -12,7 +12,8 @@
  *  - Every call returns oocz_status: 0 = OK, < 0 = error.  A failed call
  *    leaves the context unchanged unless it returns OOCZ_ECUDA / OOCZ_ENCCL,
  *    which poison the context (every later call returns OOCZ_ESTATE).
- *  - Fields are fp32, x fastest then y then z ("C order" [z][y][x]).
+ *  - Fields are fp32 (precision 32) or fp64 (precision 64: the paper's own,
+ *    PAPER.md:208), x fastest then y then z ("C order" [z][y][x]).
  *  - A context is used by one host thread at a time.
  *  - Pointers named d_* are device pointers on the context's device; all
  *    others are host pointers.  The caller owns every pointer it passes; the
@@ -29,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OOCZ_ABI_VERSION 1
+#define OOCZ_ABI_VERSION 2
 
 typedef enum {
     OOCZ_OK = 0,
@@ -66,9 +67,13 @@ typedef struct {
     int32_t  profile;      /* 1: record per-stage CUDA events (oocz_get_events)               */
     uint64_t device_bytes; /* device memory budget; 0 = whatever cudaMemGetInfo reports free  */
     int32_t  m_resident;   /* 1: decode the read-only m ONCE into HBM (nx*ny*(nz/world + 8T)
-                              fp32) and keep it, instead of streaming and decoding it every
+                              values) and keep it, instead of streaming and decoding it every
                               sweep: orchestration beyond the paper (the
                               paper's future work PAPER.md:254).  Results are identical.     */
+    int32_t  precision;    /* 32: fp32 fields, arithmetic and codec (uses c);  64: fp64 (uses
+                              c64; the paper's precision; rates 32/64 and 24/64,
+                              PAPER.md:213-215).  Raw rate 0 stores 4 resp. 8 B per value.   */
+    double   c64[5];       /* the weights for precision 64 (default: the exact decimals)      */
 } oocz_config;
 
 typedef struct {
@@ -105,11 +110,12 @@ typedef struct oocz_ctx oocz_ctx;
 /* ---------------------------------------------------------------- library */
 int32_t     oocz_abi_version(void);
 const char* oocz_status_string(oocz_status s);
-/* fills defaults: 8th-order c, tb = 4, rates 16, host store, 2 slots */
+/* fills defaults: precision 32, 8th-order c / c64, tb = 4, rates 16, host store, 2 slots */
 void        oocz_default_config(oocz_config* cfg, int32_t nx, int32_t ny, int32_t nz);
 /* m_max(c) = 4 / (3 max_theta |S(theta)|), S = c0 + 2 sum c_k cos(k theta); 105/512 for
  * the default c (R2).  oocz_set_field(M) rejects larger m with OOCZ_ECFL. */
 double      oocz_cfl_limit(const float c[5]);
+double      oocz_cfl_limit_f64(const double c[5]);
 /* validate a config for (rank, world) without allocating; msg (may be NULL) receives
  * the violated constraint, e.g. "P (36) < 2h (40)" */
 oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char* msg, size_t msg_len);
@@ -123,11 +129,12 @@ oocz_status oocz_get_nccl_id(uint8_t id[128]);
 oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world,
                         const uint8_t* nccl_id /* NULL if world == 1 */,
                         int32_t device, oocz_ctx** out);
-/* Copy this rank's slab (count = nx*ny*nz/world floats) of field f into the
+/* Copy this rank's slab (count = nx*ny*nz/world values: float for precision 32,
+ * double for precision 64) of field f into the
  * store, compressing it on the GPU (the initial round trip).
  * Rejects NaN/Inf (OOCZ_ENONFINITE) and, for OOCZ_M, m < 0 or m > m_max (OOCZ_ECFL). */
-oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const float* src, size_t count);
-oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const float* d_src, size_t count);
+oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const void* src, size_t count);
+oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const void* d_src, size_t count);
 /* Advance n steps: floor(n/T) sweeps of T steps, then one sweep of n mod T.
  * Every sweep streams each z-block through decode -> T cone-limited stencil
  * steps -> encode (Fig. 4), with copies, codec and stencil on
@@ -135,9 +142,9 @@ oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const float* d_s
  * Results depend on how n is split across calls (each sweep ends with a
  * re-encode); R16. */
 oocz_status oocz_step(oocz_ctx* ctx, int64_t nsteps);
-/* Decode this rank's slab of field f into dst (count floats). */
-oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, float* dst, size_t count);
-oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float* d_dst, size_t count);
+/* Decode this rank's slab of field f into dst (count values of the context's precision). */
+oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count);
+oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, void* d_dst, size_t count);
 /* Checkpoint / restore.  Between oocz_step calls the
  * compressed store IS the whole state; a decode -> encode round trip is not
  * idempotent, so a faithful checkpoint keeps the compressed bytes.
@@ -150,6 +157,8 @@ size_t      oocz_store_bytes(const oocz_ctx* ctx, int32_t field);
 oocz_status oocz_save_store(oocz_ctx* ctx, int32_t field, void* dst, size_t bytes);
 oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void* src, size_t bytes);
 oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out);
+/* the configuration the context was created with */
+oocz_status oocz_get_config(const oocz_ctx* ctx, oocz_config* out);
 /* In-process z-partitioned group on ONE device: `world` contexts (ranks 0..world-1)
  * that exchange their halos with device copies instead of NCCL, stepped in
  * lockstep by oocz_step_local_group.  Same engine, same halo protocol as the
@@ -192,6 +201,22 @@ oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev, const flo
                                      int32_t nx, int32_t ny, int32_t nz, const float c[5],
                                      int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
                                      void* stream);
+/* fp64 twins (the paper's own precision; rates 32/64 and 24/64 at
+ * PAPER.md:213-215).  Format: the same layout with an 11-bit exponent (bias 1023),
+ * a 12-bit header and 64 bit planes, q = trunc(x 2^(62 - emax)) (DESIGN.md
+ * "Codec", fp64).  Same sizes (8 * rate bytes per 4^3 block), same block order. */
+oocz_status oocz_zfp_encode_f64(const double* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                int32_t rate, uint64_t* d_out, void* stream);
+oocz_status oocz_zfp_decode_f64(const uint64_t* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                int32_t rate, double* d_out, void* stream);
+/* fp64 stencil: the same step in fp64 arithmetic (same order, fl64(3 c0)) */
+oocz_status oocz_stencil_steps_f64(double* d_u, double* d_uprev, const double* d_m,
+                                   int32_t nx, int32_t ny, int32_t nz, const double c[5],
+                                   int32_t nsteps, void* stream);
+oocz_status oocz_stencil_step_planes_f64(const double* d_u, double* d_uprev, const double* d_m,
+                                         int32_t nx, int32_t ny, int32_t nz, const double c[5],
+                                         int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
+                                         void* stream);
 /* number of this library's kernels launched by this process so far */
 uint64_t    oocz_kernel_launch_count(void);
 

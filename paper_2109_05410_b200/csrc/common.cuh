@@ -29,12 +29,28 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
                               uint64_t* out, cudaStream_t s);
 cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int rate,
                               float* out, cudaStream_t s);
+cudaError_t launch_zfp_encode64(const double* in, int nx, int ny, int nz, int rate,
+                                uint64_t* out, cudaStream_t s);
+cudaError_t launch_zfp_decode64(const uint64_t* in, int nx, int ny, int nz, int rate,
+                                double* out, cudaStream_t s);
+// nplanes of an nx*ny field of element size esz (4: fp32, 8: fp64): fixed-rate
+// encode / decode, or a raw device copy for rate 0
+cudaError_t field_encode(const void* src, int esz, int nx, int ny, int nplanes, int rate, void* dst,
+                         cudaStream_t s);
+cudaError_t field_decode(const void* src, int esz, int nx, int ny, int nplanes, int rate, void* dst,
+                         cudaStream_t s);
 // one cone-limited step: planes [z0, z1) of uprev <- u+; u planes outside
 // [zv0, zv1) read as zero
 cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m,
                                 int nx, int ny, int nz, const float c[5],
                                 int z0, int z1, int zv0, int zv1, cudaStream_t s);
+cudaError_t launch_stencil_step(const double* u, double* uprev, const double* m,
+                                int nx, int ny, int nz, const double c[5],
+                                int z0, int z1, int zv0, int zv1, cudaStream_t s);
 // checks used by set_field: flags[0] |= non-finite seen; flags[1] = max(bits of m) (m >= 0)
 cudaError_t launch_scan_field(const float* in, size_t n, unsigned int* flags, cudaStream_t s);
+// fp64: flags[0] as above; *mx64 = max(bits of |x|) as a 64-bit word
+cudaError_t launch_scan_field(const double* in, size_t n, unsigned int* flags, unsigned long long* mx64,
+                              cudaStream_t s);
 
 }  // namespace oocz

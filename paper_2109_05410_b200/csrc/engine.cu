@@ -76,7 +76,39 @@ __global__ void scan_field_kernel(const float* __restrict__ in, size_t n, unsign
     }
 }
 
+__global__ void scan_field64_kernel(const double* __restrict__ in, size_t n, unsigned int* flags,
+                                    unsigned long long* mx64)
+{
+    unsigned int nonfinite = 0, neg = 0;
+    unsigned long long mx = 0;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = (unsigned long long)__double_as_longlong(in[i]);
+        const unsigned long long a = b & 0x7fffffffffffffffull;
+        nonfinite |= a >= 0x7ff0000000000000ull;
+        neg |= (b >> 63) && a;
+        mx = max(mx, a);
+    }
+    nonfinite = __reduce_or_sync(0xffffffffu, nonfinite);
+    neg = __reduce_or_sync(0xffffffffu, neg);
+    for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) {
+        if (nonfinite) atomicOr(&flags[0], 1u);
+        if (neg) atomicOr(&flags[0], 2u);
+        atomicMax(mx64, mx);
+    }
+}
+
 }  // namespace
+
+cudaError_t launch_scan_field(const double* in, size_t n, unsigned int* flags, unsigned long long* mx64,
+                              cudaStream_t s)
+{
+    if (n == 0) return cudaSuccess;
+    size_t blocks = std::min<size_t>((n + 255) / 256, (size_t)kNumSMs * 8);
+    scan_field64_kernel<<<(unsigned)blocks, 256, 0, s>>>(in, n, flags, mx64);
+    note_launches(1);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_scan_field(const float* in, size_t n, unsigned int* flags, cudaStream_t s)
 {
@@ -104,7 +136,8 @@ struct oocz_ctx {
     int rank = 0, world = 1, device = 0;
     int S = 0, P = 0, D = 0, h = 0, T = 0, L = 0;   // slab planes, block, blocks, halo, depth, slab len
     int nx = 0, ny = 0;
-    size_t plane_elems = 0;
+    int esz = 4;                            // element size: 4 (precision 32) or 8 (precision 64)
+    size_t plane_elems = 0, pb = 0;         // elements / bytes per plane
     size_t row_bytes[3] = {0, 0, 0};       // bytes per 4-plane block-row in the store
     bool field_set[3] = {false, false, false};
     bool poisoned = false;
@@ -112,13 +145,14 @@ struct oocz_ctx {
 
     std::vector<Geom> geom;
     // device buffers
-    float* slab[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
-    float* ccopy[3] = {nullptr, nullptr, nullptr};
-    float* m_full = nullptr;                // m_resident: decoded m, planes [-h, S + h)
+    // (byte pointers: fp32 or fp64 planes of pb bytes)
+    uint8_t* slab[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    uint8_t* ccopy[3] = {nullptr, nullptr, nullptr};
+    uint8_t* m_full = nullptr;              // m_resident: decoded m, planes [-h, S + h)
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
     size_t in_slot_bytes = 0, out_slot_bytes = 0;
-    unsigned int* d_flags = nullptr;
+    unsigned int* d_flags = nullptr;        // [0] scan flags, [1] fp32 max bits, [2..3] fp64 max bits
     // store
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
     size_t store_bytes[3] = {0, 0, 0};
@@ -165,12 +199,15 @@ oocz_status fail(oocz_ctx* c, oocz_status s, const char* fmt, ...)
                         __FILE__, __LINE__);                                            \
     } while (0)
 
-size_t row_bytes_for(int nx, int ny, int rate)
+size_t row_bytes_for(int nx, int ny, int rate, int esz)
 {
-    return rate == 0 ? (size_t)nx * ny * 4 * sizeof(float) : (size_t)(nx / 4) * (ny / 4) * 8u * (size_t)rate;
+    return rate == 0 ? (size_t)nx * ny * 4 * esz : (size_t)(nx / 4) * (ny / 4) * 8u * (size_t)rate;
 }
 
-double cfl_limit(const float c[5])
+int esz_of(const oocz_config* cfg) { return cfg->precision == 64 ? 8 : 4; }
+
+template <class C>
+double cfl_limit(const C c[5])
 {
     // m_max = 4 / (3 max_theta |S(theta)|), S = c0 + 2 sum c_k cos(k theta) (R2)
     double mx = 0.0;
@@ -187,22 +224,26 @@ double cfl_limit(const float c[5])
 // one 4-aligned plane range of a field's store as a byte range
 inline size_t rows_off(const oocz_ctx* c, int f, int plane) { return (size_t)(plane / 4) * c->row_bytes[f]; }
 
-cudaError_t encode_or_copy(oocz_ctx* c, int f, const float* src, int nplanes, uint8_t* dst, cudaStream_t s)
+cudaError_t encode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, uint8_t* dst, cudaStream_t s)
 {
-    const int rate = c->cfg.rate[f];
-    if (rate == 0)
-        return cudaMemcpyAsync(dst, src, (size_t)nplanes * c->plane_elems * sizeof(float),
-                               cudaMemcpyDeviceToDevice, s);
-    return launch_zfp_encode(src, c->nx, c->ny, nplanes, rate, reinterpret_cast<uint64_t*>(dst), s);
+    return field_encode(src, c->esz, c->nx, c->ny, nplanes, c->cfg.rate[f], dst, s);
 }
 
-cudaError_t decode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, float* dst, cudaStream_t s)
+cudaError_t decode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, uint8_t* dst, cudaStream_t s)
 {
-    const int rate = c->cfg.rate[f];
-    if (rate == 0)
-        return cudaMemcpyAsync(dst, src, (size_t)nplanes * c->plane_elems * sizeof(float),
-                               cudaMemcpyDeviceToDevice, s);
-    return launch_zfp_decode(reinterpret_cast<const uint64_t*>(src), c->nx, c->ny, nplanes, rate, dst, s);
+    return field_decode(src, c->esz, c->nx, c->ny, nplanes, c->cfg.rate[f], dst, s);
+}
+
+// one cone-limited step in the context's precision
+cudaError_t stencil_step(oocz_ctx* c, uint8_t* u, uint8_t* uprev, const uint8_t* m, int z0, int z1, int zv0,
+                         int zv1, cudaStream_t s)
+{
+    if (c->esz == 8)
+        return launch_stencil_step(reinterpret_cast<const double*>(u), reinterpret_cast<double*>(uprev),
+                                   reinterpret_cast<const double*>(m), c->nx, c->ny, c->L, c->cfg.c64, z0, z1,
+                                   zv0, zv1, s);
+    return launch_stencil_step(reinterpret_cast<const float*>(u), reinterpret_cast<float*>(uprev),
+                               reinterpret_cast<const float*>(m), c->nx, c->ny, c->L, c->cfg.c, z0, z1, zv0, zv1, s);
 }
 
 cudaEvent_t pool_event(oocz_ctx* c)
@@ -260,6 +301,12 @@ extern "C" void oocz_default_config(oocz_config* cfg, int32_t nx, int32_t ny, in
     cfg->c[2] = (float)(-1.0 / 5.0);
     cfg->c[3] = (float)(8.0 / 315.0);
     cfg->c[4] = (float)(-1.0 / 560.0);
+    cfg->c64[0] = -205.0 / 72.0;
+    cfg->c64[1] = 8.0 / 5.0;
+    cfg->c64[2] = -1.0 / 5.0;
+    cfg->c64[3] = 8.0 / 315.0;
+    cfg->c64[4] = -1.0 / 560.0;
+    cfg->precision = 32;
     cfg->tb = 4;
     cfg->block_planes = nz;
     cfg->rate[0] = cfg->rate[1] = cfg->rate[2] = 16;
@@ -268,6 +315,7 @@ extern "C" void oocz_default_config(oocz_config* cfg, int32_t nx, int32_t ny, in
 }
 
 extern "C" double oocz_cfl_limit(const float c[5]) { return c ? cfl_limit(c) : 0.0; }
+extern "C" double oocz_cfl_limit_f64(const double c[5]) { return c ? cfl_limit(c) : 0.0; }
 
 extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char* msg, size_t msg_len)
 {
@@ -296,8 +344,11 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->store != OOCZ_STORE_HOST && cfg->store != OOCZ_STORE_DEVICE)
         BAD(OOCZ_EINVAL, "store (%d) unknown", cfg->store);
     if (cfg->store == OOCZ_STORE_HOST && cfg->slots < 2) BAD(OOCZ_EINVAL, "slots (%d) < 2", cfg->slots);
+    if (cfg->precision != 32 && cfg->precision != 64)
+        BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
-        if (!std::isfinite(cfg->c[k])) BAD(OOCZ_EINVAL, "c[%d] not finite", k);
+        if (cfg->precision == 32 ? !std::isfinite(cfg->c[k]) : !std::isfinite(cfg->c64[k]))
+            BAD(OOCZ_EINVAL, "c[%d] not finite", k);
 #undef BAD
 done:
     if (msg && msg_len) snprintf(msg, msg_len, "%s", buf);
@@ -330,7 +381,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     ctx->D = ctx->S / ctx->P;
     ctx->L = ctx->P + 2 * ctx->h;
     ctx->plane_elems = (size_t)cfg->nx * cfg->ny;
-    for (int f = 0; f < 3; f++) ctx->row_bytes[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f]);
+    ctx->esz = esz_of(cfg);
+    ctx->pb = ctx->plane_elems * ctx->esz;
+    for (int f = 0; f < 3; f++) ctx->row_bytes[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], ctx->esz);
 
     auto cleanup_fail = [&](oocz_status s) { oocz_destroy(ctx); return s; };
 #define CKC(call)                                                                                 \
@@ -360,7 +413,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         ctx->geom.push_back(g);
     }
     // memory plan and budget check
-    const size_t pb = ctx->plane_elems * sizeof(float);
+    const size_t pb = ctx->pb;
     size_t need = 2 * 3 * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
@@ -450,7 +503,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         ctx->halo = preset_halo;
     } else if (world > 1) {
         std::string herr;
-        ctx->halo = halo_create(rank, world, nccl_id, device, ctx->plane_elems, h, cfg->rate,
+        ctx->halo = halo_create(rank, world, nccl_id, device, ctx->plane_elems, ctx->esz, h, cfg->rate,
                                 ctx->row_bytes, &herr);
         if (!ctx->halo) {
             fprintf(stderr, "oocz_create: %s\n", herr.c_str());
@@ -480,11 +533,12 @@ extern "C" oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t w
     }
     if (cudaSetDevice(device) != cudaSuccess) return OOCZ_ECUDA;
     size_t rb[3];
-    for (int f = 0; f < 3; f++) rb[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f]);
+    for (int f = 0; f < 3; f++) rb[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], esz_of(cfg));
     HaloComm** hs = nullptr;
     if (world > 1) {
         std::string herr;
-        hs = halo_create_local_group(world, device, (size_t)cfg->nx * cfg->ny, 4 * cfg->tb, cfg->rate, rb, &herr);
+        hs = halo_create_local_group(world, device, (size_t)cfg->nx * cfg->ny, esz_of(cfg), 4 * cfg->tb, cfg->rate,
+                                     rb, &herr);
         if (!hs) {
             fprintf(stderr, "oocz_create_local_group: %s\n", herr.c_str());
             return OOCZ_ECAPACITY;
@@ -554,6 +608,13 @@ extern "C" oocz_status oocz_get_stats(const oocz_ctx* ctx, oocz_stats* out)
     return OOCZ_OK;
 }
 
+extern "C" oocz_status oocz_get_config(const oocz_ctx* ctx, oocz_config* out)
+{
+    if (!ctx || !out) return OOCZ_EINVAL;
+    *out = ctx->cfg;
+    return OOCZ_OK;
+}
+
 extern "C" oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, size_t cap, size_t* n)
 {
     if (!ctx || !n) return OOCZ_EINVAL;
@@ -563,28 +624,33 @@ extern "C" oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, siz
 }
 
 // ------------------------------------------------------------------ set / get
-static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src, size_t count, bool on_device)
+static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_v, size_t count, bool on_device)
 {
     if (!ctx) return OOCZ_EINVAL;
     if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
     if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
-    if (!src && count) return fail(ctx, OOCZ_EINVAL, "null source");
+    if (!src_v && count) return fail(ctx, OOCZ_EINVAL, "null source");
     const size_t want = ctx->plane_elems * (size_t)ctx->S;
     if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
     CK(cudaSetDevice(ctx->device));
     ctx->field_set[field] = false;
     cudaStream_t s = ctx->s_comp;
     const int chunk = ctx->P;                       // planes per pass, <= slab capacity
-    const double mmax = cfl_limit(ctx->cfg.c);
+    const double mmax = ctx->esz == 8 ? cfl_limit(ctx->cfg.c64) : cfl_limit(ctx->cfg.c);
+    const uint8_t* src = static_cast<const uint8_t*>(src_v);
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     CK(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(unsigned int), s));
     for (int z = 0; z < ctx->S; z += chunk) {
         const int np = std::min(chunk, ctx->S - z);
         const size_t n = (size_t)np * ctx->plane_elems;
-        float* buf = ctx->slab[0][field];
-        CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->plane_elems, n * sizeof(float),
+        uint8_t* buf = ctx->slab[0][field];
+        CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->pb, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-        CK(launch_scan_field(buf, n, ctx->d_flags, s));
+        if (ctx->esz == 8)
+            CK(launch_scan_field(reinterpret_cast<const double*>(buf), n, ctx->d_flags,
+                                 reinterpret_cast<unsigned long long*>(ctx->d_flags + 2), s));
+        else
+            CK(launch_scan_field(reinterpret_cast<const float*>(buf), n, ctx->d_flags, s));
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         const uint8_t* coded;
@@ -598,15 +664,21 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src
             coded = ctx->store[field] + off;
         }
         if (field == OOCZ_M && ctx->m_full)         // m_resident: keep the decoded RT(m)
-            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->plane_elems, s));
+            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->pb, s));
     }
-    unsigned int flags[2] = {0, 0};
+    unsigned int flags[4] = {0, 0, 0, 0};
     CK(cudaMemcpyAsync(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     if (flags[0] & 1u) return fail(ctx, OOCZ_ENONFINITE, "field %d contains NaN or Inf", field);
     if (field == OOCZ_M) {
-        float mx;
-        std::memcpy(&mx, &flags[1], sizeof mx);
+        double mx;
+        if (ctx->esz == 8) {
+            std::memcpy(&mx, &flags[2], sizeof mx);
+        } else {
+            float m32;
+            std::memcpy(&m32, &flags[1], sizeof m32);
+            mx = m32;
+        }
         if (flags[0] & 2u) return fail(ctx, OOCZ_ECFL, "m has negative values");
         if ((double)mx > mmax)
             return fail(ctx, OOCZ_ECFL, "max m (%.9g) > m_max(c) (%.9g)", (double)mx, mmax);
@@ -627,16 +699,16 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const float* src
     return OOCZ_OK;
 }
 
-extern "C" oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const float* src, size_t count)
+extern "C" oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const void* src, size_t count)
 {
     return set_field_impl(ctx, field, src, count, false);
 }
-extern "C" oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const float* d_src, size_t count)
+extern "C" oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const void* d_src, size_t count)
 {
     return set_field_impl(ctx, field, d_src, count, true);
 }
 
-static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, float* dst, size_t count, bool on_device)
+static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, void* dst_v, size_t count, bool on_device)
 {
     if (!ctx) return OOCZ_EINVAL;
     if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
@@ -644,17 +716,17 @@ static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, float* dst, size
     if (!ctx->field_set[field]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", field);
     const size_t want = ctx->plane_elems * (size_t)ctx->S;
     if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
-    if (!dst && count) return fail(ctx, OOCZ_EINVAL, "null destination");
+    if (!dst_v && count) return fail(ctx, OOCZ_EINVAL, "null destination");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->s_comp;
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int chunk = ctx->P;
+    uint8_t* dst = static_cast<uint8_t*>(dst_v);
     for (int z = 0; z < ctx->S; z += chunk) {
         const int np = std::min(chunk, ctx->S - z);
-        const size_t n = (size_t)np * ctx->plane_elems;
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
-        float* buf = ctx->slab[0][field];
+        uint8_t* buf = ctx->slab[0][field];
         if (host) {
             uint8_t* dev = ctx->in_slot[0];
             CK(cudaMemcpyAsync(dev, ctx->store[field] + off, bytes, cudaMemcpyHostToDevice, s));
@@ -662,18 +734,18 @@ static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, float* dst, size
         } else {
             CK(decode_or_copy(ctx, field, ctx->store[field] + off, np, buf, s));
         }
-        CK(cudaMemcpyAsync(dst + (size_t)z * ctx->plane_elems, buf, n * sizeof(float),
+        CK(cudaMemcpyAsync(dst + (size_t)z * ctx->pb, buf, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
     return OOCZ_OK;
 }
 
-extern "C" oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, float* dst, size_t count)
+extern "C" oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count)
 {
     return get_field_impl(ctx, field, dst, count, false);
 }
-extern "C" oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, float* d_dst, size_t count)
+extern "C" oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, void* d_dst, size_t count)
 {
     return get_field_impl(ctx, field, d_dst, count, true);
 }
@@ -721,7 +793,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
                                    cudaMemcpyHostToDevice, s));
                 coded = ctx->in_slot[0];
             }
-            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->plane_elems, s));
+            CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->pb, s));
         }
         CK(cudaStreamSynchronize(s));
     }
@@ -743,15 +815,15 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
 {
     const Geom& g = ctx->geom[i];
     const int h = ctx->h, P = ctx->P, D = ctx->D;
-    const size_t pb = ctx->plane_elems * sizeof(float);
+    const size_t pb = ctx->pb;
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
     const int set = (int)(ctx->seq % 2);         // slab set of this block
     // m_resident: m is read in place from the decoded copy, never streamed
     const int nf = ctx->m_full ? 2 : 3;
-    float* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
-                      ctx->m_full ? ctx->m_full + (size_t)(g.slab0 + h) * ctx->plane_elems : ctx->slab[set][2]};
+    uint8_t* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
+                        ctx->m_full ? ctx->m_full + (size_t)(g.slab0 + h) * pb : ctx->slab[set][2]};
     const int rd_planes = g.rd1 - g.rd0;
     const uint8_t* src[3];
     cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
@@ -797,10 +869,10 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     }
     // ---- (a3) decode the read unit into the slab
     for (int f = 0; f < nf; f++) {
-        // algorithmic bytes: compressed (or raw) read unit in + fp32 planes out
+        // algorithmic bytes: compressed (or raw) read unit in + decoded planes out
         const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
-        CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(g.rd0 - g.slab0) * ctx->plane_elems, sd));
+        CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(g.rd0 - g.slab0) * pb, sd));
         prof_end(ctx, sd);
     }
     if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
@@ -808,7 +880,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
     if (i < D - 1) {
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < nf; f++)
-            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + (size_t)P * ctx->plane_elems, (size_t)(2 * h) * pb,
+            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + (size_t)P * pb, (size_t)(2 * h) * pb,
                                cudaMemcpyDeviceToDevice, sd));
         prof_end(ctx, sd);
     }
@@ -816,21 +888,20 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
 
     // ---- (a5) T cone-limited steps, in place, roles swapping (compute stream)
     CK(cudaStreamWaitEvent(sc, ctx->ev_decoded[set], 0));
-    float* cu = slab[OOCZ_U];
-    float* cp = slab[OOCZ_UPREV];
+    uint8_t* cu = slab[OOCZ_U];
+    uint8_t* cp = slab[OOCZ_UPREV];
     for (int s = 1; s <= ts; s++) {
         const int z0 = std::max(4 * s, g.vlo);
         const int z1 = std::min(ctx->L - 4 * s, g.vhi);
         // algorithmic bytes: read u, u-, m and write u+ once per updated cell
-        prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 16ull * (uint64_t)std::max(z1 - z0, 0) * ctx->plane_elems);
-        CK(launch_stencil_step(cu, cp, slab[OOCZ_M], ctx->nx, ctx->ny, ctx->L, ctx->cfg.c, z0, z1, g.vlo,
-                               g.vhi, sc));
+        prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 4ull * (uint64_t)std::max(z1 - z0, 0) * pb);
+        CK(stencil_step(ctx, cu, cp, slab[OOCZ_M], z0, z1, g.vlo, g.vhi, sc));
         prof_end(ctx, sc);
         std::swap(cu, cp);
     }
 
     // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-
-    const float* own[2] = {cu + (size_t)h * ctx->plane_elems, cp + (size_t)h * ctx->plane_elems};
+    const uint8_t* own[2] = {cu + (size_t)h * pb, cp + (size_t)h * pb};
     if (ctx->halo) {
         std::string herr;
         if (!halo_capture(ctx->halo, i == 0, i == D - 1, own, P, ctx->nx, ctx->ny, sc, &herr))

@@ -63,6 +63,7 @@ struct HaloComm {
     ncclComm_t comm = nullptr;
     int h = 0;
     size_t plane_elems = 0;
+    int esz = 4;                          // element size: 4 fp32, 8 fp64
     int rate[3] = {0, 0, 0};
     size_t bytes[3] = {0, 0, 0};          // h planes of each field, as stored
     uint8_t* send_top[3] = {};
@@ -90,11 +91,11 @@ bool nccl_ok(ncclResult_t r, std::string* err, const char* what)
     return set_err(err, std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "?"));
 }
 
-HaloComm* alloc_halo(int rank, int world, int device, size_t plane_elems, int h, const int rate[3],
+HaloComm* alloc_halo(int rank, int world, int device, size_t plane_elems, int esz, int h, const int rate[3],
                      const size_t row_bytes[3], std::string* err)
 {
     HaloComm* hc = new HaloComm;
-    hc->rank = rank; hc->world = world; hc->h = h; hc->plane_elems = plane_elems;
+    hc->rank = rank; hc->world = world; hc->h = h; hc->plane_elems = plane_elems; hc->esz = esz;
     bool ok = cuda_ok(cudaSetDevice(device), err, "cudaSetDevice");
     for (int f = 0; f < 3 && ok; f++) {
         hc->rate[f] = rate[f];
@@ -112,18 +113,14 @@ HaloComm* alloc_halo(int rank, int world, int device, size_t plane_elems, int h,
     return hc;
 }
 
-cudaError_t code(const HaloComm* hc, int f, const float* src, int nx, int ny, uint8_t* dst, cudaStream_t s)
+cudaError_t code(const HaloComm* hc, int f, const uint8_t* src, int nx, int ny, uint8_t* dst, cudaStream_t s)
 {
-    if (hc->rate[f] == 0)
-        return cudaMemcpyAsync(dst, src, (size_t)hc->h * nx * ny * sizeof(float), cudaMemcpyDeviceToDevice, s);
-    return launch_zfp_encode(src, nx, ny, hc->h, hc->rate[f], reinterpret_cast<uint64_t*>(dst), s);
+    return field_encode(src, hc->esz, nx, ny, hc->h, hc->rate[f], dst, s);
 }
 
-cudaError_t uncode(const HaloComm* hc, int f, const uint8_t* src, int nx, int ny, float* dst, cudaStream_t s)
+cudaError_t uncode(const HaloComm* hc, int f, const uint8_t* src, int nx, int ny, uint8_t* dst, cudaStream_t s)
 {
-    if (hc->rate[f] == 0)
-        return cudaMemcpyAsync(dst, src, (size_t)hc->h * nx * ny * sizeof(float), cudaMemcpyDeviceToDevice, s);
-    return launch_zfp_decode(reinterpret_cast<const uint64_t*>(src), nx, ny, hc->h, hc->rate[f], dst, s);
+    return field_decode(src, hc->esz, nx, ny, hc->h, hc->rate[f], dst, s);
 }
 
 bool fill_from_store(HaloComm* hc, int f, const uint8_t* store, bool host_store, int S, size_t row_bytes,
@@ -155,11 +152,11 @@ size_t halo_device_bytes(size_t, int h, const int[3], const size_t row_bytes[3])
     return t;
 }
 
-HaloComm* halo_create(int rank, int world, const uint8_t* id, int device, size_t plane_elems, int h,
+HaloComm* halo_create(int rank, int world, const uint8_t* id, int device, size_t plane_elems, int esz, int h,
                       const int rate[3], const size_t row_bytes[3], std::string* err)
 {
     if (!nccl().ok) { set_err(err, "libnccl.so.2 not loadable"); return nullptr; }
-    HaloComm* hc = alloc_halo(rank, world, device, plane_elems, h, rate, row_bytes, err);
+    HaloComm* hc = alloc_halo(rank, world, device, plane_elems, esz, h, rate, row_bytes, err);
     if (!hc) return nullptr;
     ncclUniqueId u;
     std::memcpy(&u, id, 128);
@@ -170,12 +167,12 @@ HaloComm* halo_create(int rank, int world, const uint8_t* id, int device, size_t
     return hc;
 }
 
-HaloComm** halo_create_local_group(int world, int device, size_t plane_elems, int h, const int rate[3],
+HaloComm** halo_create_local_group(int world, int device, size_t plane_elems, int esz, int h, const int rate[3],
                                    const size_t row_bytes[3], std::string* err)
 {
     LocalGroup* g = new LocalGroup;
     for (int r = 0; r < world; r++) {
-        HaloComm* hc = alloc_halo(r, world, device, plane_elems, h, rate, row_bytes, err);
+        HaloComm* hc = alloc_halo(r, world, device, plane_elems, esz, h, rate, row_bytes, err);
         if (!hc) {
             for (auto* m : g->members) halo_destroy(m);
             delete g;
@@ -269,7 +266,7 @@ bool halo_sweep_begin(HaloComm* hc, cudaStream_t s, std::string* err)
     return true;
 }
 
-bool halo_insert(HaloComm* hc, bool first_block, bool last_block, float* const slab[3], int slab0, int S,
+bool halo_insert(HaloComm* hc, bool first_block, bool last_block, uint8_t* const slab[3], int slab0, int S,
                  int nx, int ny, cudaStream_t s, std::string* err)
 {
     if (first_block && hc->rank > 0)
@@ -277,13 +274,13 @@ bool halo_insert(HaloComm* hc, bool first_block, bool last_block, float* const s
             if (!cuda_ok(uncode(hc, f, hc->recv_top[f], nx, ny, slab[f], s), err, "halo decode")) return false;
     if (last_block && hc->rank < hc->world - 1)
         for (int f = 0; f < 3; f++)
-            if (!cuda_ok(uncode(hc, f, hc->recv_bot[f], nx, ny, slab[f] + (size_t)(S - slab0) * hc->plane_elems, s),
+            if (!cuda_ok(uncode(hc, f, hc->recv_bot[f], nx, ny, slab[f] + (size_t)(S - slab0) * hc->plane_elems * hc->esz, s),
                          err, "halo decode"))
                 return false;
     return true;
 }
 
-bool halo_capture(HaloComm* hc, bool first_block, bool last_block, const float* const own[2], int P, int nx,
+bool halo_capture(HaloComm* hc, bool first_block, bool last_block, const uint8_t* const own[2], int P, int nx,
                   int ny, cudaStream_t s, std::string* err)
 {
     if (first_block && hc->rank > 0) {
@@ -297,7 +294,7 @@ bool halo_capture(HaloComm* hc, bool first_block, bool last_block, const float* 
         if (hc->group && !cuda_ok(cudaStreamWaitEvent(s, hc->group->members[hc->rank + 1]->ev_recv_top, 0), err, "wait"))
             return false;
         for (int f = 0; f < 2; f++)
-            if (!cuda_ok(code(hc, f, own[f] + (size_t)(P - hc->h) * hc->plane_elems, nx, ny, hc->send_bot[f], s), err,
+            if (!cuda_ok(code(hc, f, own[f] + (size_t)(P - hc->h) * hc->plane_elems * hc->esz, nx, ny, hc->send_bot[f], s), err,
                          "halo encode"))
                 return false;
         if (!cuda_ok(cudaEventRecord(hc->ev_capt_bot, s), err, "event")) return false;

@@ -28,11 +28,11 @@ struct HaloComm;
 
 bool halo_get_unique_id(uint8_t id[128]);
 size_t halo_device_bytes(size_t plane_elems, int h, const int rate[3], const size_t row_bytes[3]);
-// NCCL transport (one process per GPU)
-HaloComm* halo_create(int rank, int world, const uint8_t* id, int device, size_t plane_elems, int h,
+// NCCL transport (one process per GPU); esz = element size (4: fp32, 8: fp64)
+HaloComm* halo_create(int rank, int world, const uint8_t* id, int device, size_t plane_elems, int esz, int h,
                       const int rate[3], const size_t row_bytes[3], std::string* err);
 // in-process transport: `world` halves sharing one registry (local group)
-HaloComm** halo_create_local_group(int world, int device, size_t plane_elems, int h, const int rate[3],
+HaloComm** halo_create_local_group(int world, int device, size_t plane_elems, int esz, int h, const int rate[3],
                                    const size_t row_bytes[3], std::string* err);
 void halo_destroy(HaloComm* hc);
 
@@ -43,9 +43,9 @@ bool halo_capture_store(HaloComm* hc, int field, const uint8_t* store, bool host
 bool halo_exchange_m(HaloComm* hc, const uint8_t* store_m, bool host_store, int S, size_t row_bytes,
                      cudaStream_t s, std::string* err);
 bool halo_sweep_begin(HaloComm* hc, cudaStream_t s, std::string* err);
-bool halo_insert(HaloComm* hc, bool first_block, bool last_block, float* const slab[3], int slab0, int S,
+bool halo_insert(HaloComm* hc, bool first_block, bool last_block, uint8_t* const slab[3], int slab0, int S,
                  int nx, int ny, cudaStream_t s, std::string* err);
-bool halo_capture(HaloComm* hc, bool first_block, bool last_block, const float* const own[2], int P, int nx,
+bool halo_capture(HaloComm* hc, bool first_block, bool last_block, const uint8_t* const own[2], int P, int nx,
                   int ny, cudaStream_t s, std::string* err);
 uint64_t halo_bytes_sent(const HaloComm* hc);
 

@@ -38,30 +38,66 @@
 namespace oocz {
 namespace {
 
-constexpr int TX = 128, TY = 16;
-constexpr int SW = TX + 8, SH = TY + 8;          // u tile incl. halo
-constexpr int kUStageFloats = SW * SH;          // 3264 floats = 13056 B (128 B multiple)
-constexpr int kRStageFloats = 2 * TX * TY;      // u- tile then m tile, 16 KiB
 #ifndef OOCZ_STENCIL_NU
 #define OOCZ_STENCIL_NU 10
 #endif
 #ifndef OOCZ_STENCIL_NR
 #define OOCZ_STENCIL_NR 5
 #endif
-constexpr int NU = OOCZ_STENCIL_NU;             // u ring stages (NU - 5 ahead of the plane in use)
-constexpr int NR = OOCZ_STENCIL_NR;             // u-/m ring stages
-static_assert(NU >= 6 && NR >= 2, "the u ring holds planes z..z+4 plus at least one in flight");
 #ifndef OOCZ_STENCIL_CTAS
 #define OOCZ_STENCIL_CTAS 148
 #endif
 constexpr int kStencilCTAs = OOCZ_STENCIL_CTAS;  // persistent CTAs (one per SM at most)
-constexpr int kConsumerWarps = TY;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
-constexpr unsigned kUBytes = kUStageFloats * sizeof(float);
-constexpr unsigned kRTileBytes = TX * TY * sizeof(float);
-constexpr size_t kSmemBytes = (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 2 * (NU + NR) * sizeof(uint64_t);
+constexpr int TX = 128;                           // 32 lanes x 4 consecutive x
 
-struct Coeffs { float c0x3, c1, c2, c3, c4; };
+// Tile shape per element type.  fp32: 128 x 16 cells, 16 consumer warps, ring
+// depths NU / NR.  fp64 (the paper's precision): 128 x 8 cells,
+// 8 consumer warps (the register queue is twice as wide; 288 threads leave
+// 224 registers per thread), u ring 8, u-/m ring 4: 203 KiB of shared memory.
+template <class T> struct Tile;
+template <> struct Tile<float> { static constexpr int TY = 16, NU = OOCZ_STENCIL_NU, NR = OOCZ_STENCIL_NR; };
+template <> struct Tile<double> { static constexpr int TY = 8, NU = 8, NR = 4; };
+
+template <class T> struct K {
+    static constexpr int TY = Tile<T>::TY, NU = Tile<T>::NU, NR = Tile<T>::NR;
+    static_assert(NU >= 6 && NR >= 2, "the u ring holds planes z..z+4 plus at least one in flight");
+    static constexpr int SW = TX + 8, SH = TY + 8;            // u tile incl. halo
+    static constexpr int kUStage = SW * SH;                   // elements (a 128 B multiple in bytes)
+    static constexpr int kRStage = 2 * TX * TY;               // u- tile then m tile
+    static constexpr int kConsumerWarps = TY;
+    static constexpr int kThreads = 32 * (1 + kConsumerWarps);
+    static constexpr unsigned kUBytes = kUStage * sizeof(T);
+    static constexpr unsigned kRTileBytes = TX * TY * sizeof(T);
+    static constexpr size_t kSmemBytes =
+        (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 2 * (NU + NR) * sizeof(uint64_t);
+    static_assert(kUBytes % 128 == 0 && kRTileBytes % 128 == 0, "TMA destinations stay 128 B aligned");
+};
+
+template <class T> struct Coeffs { T c0x3, c1, c2, c3, c4; };
+
+// 4 consecutive values (one float4, or two double2) and round-to-nearest ops
+template <class T> struct V4 { T v[4]; };
+__device__ __forceinline__ V4<float> ld4(const float* p) {
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    return V4<float>{{a.x, a.y, a.z, a.w}};
+}
+__device__ __forceinline__ V4<double> ld4(const double* p) {
+    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    return V4<double>{{a.x, a.y, b.x, b.y}};
+}
+__device__ __forceinline__ void st4(float* p, const float r[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
+}
+__device__ __forceinline__ void st4(double* p, const double r[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(r[0], r[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(r[2], r[3]);
+}
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -98,6 +134,7 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 // and a tile's radius-4 y/x halo rows are L2 hits from its neighbours' loads.
 struct Seg { int x0, y0, zb, ze; };
 
+template <int TY>
 __device__ __forceinline__ bool next_seg(long& it, long items, long tiles, int ntx, int z0, int z1, int chunk,
                                          Seg& sg) {
     if (it >= items) return false;
@@ -110,17 +147,21 @@ __device__ __forceinline__ bool next_seg(long& it, long items, long tiles, int n
     return true;
 }
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <class T>
+__global__ void __launch_bounds__(K<T>::kThreads, 1)
 stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
-                 const __grid_constant__ CUtensorMap tm_m, float* __restrict__ uprev, int nx, int ny,
-                 int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs cf)
+                 const __grid_constant__ CUtensorMap tm_m, T* __restrict__ uprev, int nx, int ny,
+                 int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs<T> cf)
 {
+    constexpr int TY = K<T>::TY, NU = K<T>::NU, NR = K<T>::NR, SW = K<T>::SW;
+    constexpr int kUStage = K<T>::kUStage, kRStage = K<T>::kRStage, kConsumerWarps = K<T>::kConsumerWarps;
+    constexpr unsigned kUBytes = K<T>::kUBytes, kRTileBytes = K<T>::kRTileBytes;
     // dynamic smem only (no static shared variables before it), 1024-aligned, and
     // pointers derived from it directly so the compiler emits LDS, not generic LD
-    extern __shared__ __align__(1024) float smem_f[];
-    float* uring = smem_f;
-    float* rring = smem_f + NU * kUStageFloats;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem_f + NU * kUStageFloats + NR * kRStageFloats);
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    T* uring = reinterpret_cast<T*>(smem_raw);
+    T* rring = uring + NU * kUStage;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(uring + NU * kUStage + NR * kRStage);
     uint64_t* ufull = bars;
     uint64_t* uempty = bars + NU;
     uint64_t* rfull = bars + 2 * NU;
@@ -146,18 +187,18 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             long it = blockIdx.x;
             unsigned gu = 0, gr = 0;
             Seg sg;
-            while (next_seg(it, items, tiles, ntx, z0, z1, chunk, sg)) {
+            while (next_seg<TY>(it, items, tiles, ntx, z0, z1, chunk, sg)) {
                 for (int p = sg.zb - 4; p < sg.ze + 4; p++, gu++) {
                     const int s = gu % NU;
                     if (gu >= NU) mbar_wait(&uempty[s], ((gu / NU) & 1) ^ 1);
                     mbar_expect_tx(&ufull[s], kUBytes);
-                    tma_load_3d(uring + s * kUStageFloats, &tm_u, sg.x0 - 4, sg.y0 - 4, p - zv0, &ufull[s]);
+                    tma_load_3d(uring + s * kUStage, &tm_u, sg.x0 - 4, sg.y0 - 4, p - zv0, &ufull[s]);
                     const int z = p - 4;                   // u-, m of plane z go with u plane z+4
                     if (z >= sg.zb) {
                         const int r = gr % NR;
                         if (gr >= NR) mbar_wait(&rempty[r], ((gr / NR) & 1) ^ 1);
                         mbar_expect_tx(&rfull[r], 2 * kRTileBytes);
-                        float* dst = rring + r * kRStageFloats;
+                        T* dst = rring + r * kRStage;
                         tma_load_3d(dst, &tm_up, sg.x0, sg.y0, z, &rfull[r]);
                         tma_load_3d(dst + TX * TY, &tm_m, sg.x0, sg.y0, z, &rfull[r]);
                         gr++;
@@ -176,91 +217,84 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
     long it = blockIdx.x;
     unsigned gu0 = 0, gr0 = 0;                       // global index of the segment's first u / u- plane
     Seg sg;
-    while (next_seg(it, items, tiles, ntx, z0, z1, chunk, sg)) {
+    while (next_seg<TY>(it, items, tiles, ntx, z0, z1, chunk, sg)) {
         const int zb = sg.zb, ze = sg.ze, pfirst = zb - 4;
         const int gx = sg.x0 + 4 * lane, gy = sg.y0 + ty;
         const bool active = gx < nx && gy < ny;
         const size_t col = (size_t)gy * nx + gx;
         auto uslot = [&](int p) { return (gu0 + (unsigned)(p - pfirst)) % NU; };
-        auto wait_u = [&](int p) -> const float* {
+        auto wait_u = [&](int p) -> const T* {
             const unsigned g = gu0 + (unsigned)(p - pfirst);
             mbar_wait(&ufull[g % NU], (g / NU) & 1);
-            return uring + (g % NU) * kUStageFloats;
+            return uring + (g % NU) * kUStage;
         };
         auto release_u = [&](int p) {
             __syncwarp();
             if (lane == 0) mbar_arrive(&uempty[uslot(p)]);
         };
 
-        float4 q[9];
+        V4<T> q[9];
         // centres of planes zb-4 .. zb+3; a plane outside [zb, ze) is released as soon
         // as its centre is read (its only use), so the ring never needs more than
         // 5 stages to get through this prologue
 #pragma unroll
         for (int i = 0; i < 8; i++) {
             const int p = pfirst + i;
-            q[i] = *reinterpret_cast<const float4*>(wait_u(p) + cidx);
+            q[i] = ld4(wait_u(p) + cidx);
             if (p < zb || p >= ze) release_u(p);
         }
 
         for (int z = zb; z < ze; z++) {
-            q[8] = *reinterpret_cast<const float4*>(wait_u(z + 4) + cidx);
+            q[8] = ld4(wait_u(z + 4) + cidx);
             const unsigned g = gr0 + (unsigned)(z - zb);
-            const float* rt = rring + (g % NR) * kRStageFloats;
-            const float* crow = uring + uslot(z) * kUStageFloats + cidx;  // plane z already landed
-            const float4 xl = *reinterpret_cast<const float4*>(crow - 4);
-            const float4 xr = *reinterpret_cast<const float4*>(crow + 4);
+            const T* rt = rring + (g % NR) * kRStage;
+            const T* crow = uring + uslot(z) * kUStage + cidx;  // plane z already landed
+            const V4<T> xl = ld4(crow - 4);
+            const V4<T> xr = ld4(crow + 4);
             // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
             // which is the first addition of the prescribed order anyway
-            float ay[4][4];
+            T ay[4][4];
 #pragma unroll
             for (int d = 1; d <= 4; d++) {
-                const float4 a = *reinterpret_cast<const float4*>(crow - d * SW);
-                const float4 b = *reinterpret_cast<const float4*>(crow + d * SW);
-                ay[d - 1][0] = __fadd_rn(a.x, b.x);
-                ay[d - 1][1] = __fadd_rn(a.y, b.y);
-                ay[d - 1][2] = __fadd_rn(a.z, b.z);
-                ay[d - 1][3] = __fadd_rn(a.w, b.w);
+                const V4<T> a = ld4(crow - d * SW);
+                const V4<T> b = ld4(crow + d * SW);
+#pragma unroll
+                for (int o = 0; o < 4; o++) ay[d - 1][o] = add_rn(a.v[o], b.v[o]);
             }
             release_u(z);
             if (z + 4 >= ze) release_u(z + 4);
 
-            const float4 uc = q[4];
-            const float w[12] = {xl.x, xl.y, xl.z, xl.w, uc.x, uc.y, uc.z, uc.w, xr.x, xr.y, xr.z, xr.w};
-            const float ucv[4] = {uc.x, uc.y, uc.z, uc.w};
-            float Lv[4];
+            const V4<T> uc = q[4];
+            const T w[12] = {xl.v[0], xl.v[1], xl.v[2], xl.v[3], uc.v[0], uc.v[1], uc.v[2], uc.v[3],
+                             xr.v[0], xr.v[1], xr.v[2], xr.v[3]};
+            T Lv[4];
 #pragma unroll
             for (int o = 0; o < 4; o++) {
-                const float u0 = ucv[o];
-                float sd[4];
+                const T u0 = uc.v[o];
+                T sd[4];
 #pragma unroll
                 for (int d = 1; d <= 4; d++) {
-                    const float* zmd = reinterpret_cast<const float*>(&q[4 - d]);
-                    const float* zpd = reinterpret_cast<const float*>(&q[4 + d]);
-                    const float ax = __fadd_rn(w[4 + o - d], w[4 + o + d]);
-                    const float az = __fadd_rn(zmd[o], zpd[o]);
-                    sd[d - 1] = __fadd_rn(__fadd_rn(ax, ay[d - 1][o]), az);
+                    const T ax = add_rn(w[4 + o - d], w[4 + o + d]);
+                    const T az = add_rn(q[4 - d].v[o], q[4 + d].v[o]);
+                    sd[d - 1] = add_rn(add_rn(ax, ay[d - 1][o]), az);
                 }
-                float L = __fmul_rn(cf.c0x3, u0);
-                L = __fmaf_rn(cf.c1, sd[0], L);
-                L = __fmaf_rn(cf.c2, sd[1], L);
-                L = __fmaf_rn(cf.c3, sd[2], L);
-                L = __fmaf_rn(cf.c4, sd[3], L);
+                T L = mul_rn(cf.c0x3, u0);
+                L = fma_rn(cf.c1, sd[0], L);
+                L = fma_rn(cf.c2, sd[1], L);
+                L = fma_rn(cf.c3, sd[2], L);
+                L = fma_rn(cf.c4, sd[3], L);
                 Lv[o] = L;
             }
             // u- and m are read only now, when they are needed
             mbar_wait(&rfull[g % NR], (g / NR) & 1);
-            const float4 upv = *reinterpret_cast<const float4*>(rt + ridx);
-            const float4 mv = *reinterpret_cast<const float4*>(rt + TX * TY + ridx);
+            const V4<T> upv = ld4(rt + ridx);
+            const V4<T> mv = ld4(rt + TX * TY + ridx);
             __syncwarp();
             if (lane == 0) mbar_arrive(&rempty[g % NR]);
-            const float upa[4] = {upv.x, upv.y, upv.z, upv.w};
-            const float ma[4] = {mv.x, mv.y, mv.z, mv.w};
-            float res[4];
+            T res[4];
 #pragma unroll
-            for (int o = 0; o < 4; o++) res[o] = __fmaf_rn(ma[o], Lv[o], __fmaf_rn(2.0f, ucv[o], -upa[o]));
-            if (active)
-                *reinterpret_cast<float4*>(uprev + (size_t)z * plane + col) = make_float4(res[0], res[1], res[2], res[3]);
+            for (int o = 0; o < 4; o++) res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
+            if (active) st4(uprev + (size_t)z * plane + col, res);
             // shift the queue (an unroll by 9 to rotate by renaming measured slower:
             // 9x the code, instruction-cache and register pressure)
 #pragma unroll
@@ -284,38 +318,40 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode_fn() {
     return fn;
 }
 
-bool make_map(CUtensorMap* map, const float* base, int nx, int ny, int nplanes, int bx, int by) {
+template <class T>
+bool make_map(CUtensorMap* map, const T* base, int nx, int ny, int nplanes, int bx, int by) {
     auto encode = get_encode_fn();
     if (!encode) return false;
     const cuuint64_t gdim[3] = {(cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nplanes};
-    const cuuint64_t gstride[2] = {(cuuint64_t)nx * sizeof(float), (cuuint64_t)nx * ny * sizeof(float)};
+    const cuuint64_t gstride[2] = {(cuuint64_t)nx * sizeof(T), (cuuint64_t)nx * ny * sizeof(T)};
     const cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
     const cuuint32_t estride[3] = {1, 1, 1};
-    return encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), gdim, gstride, box,
+    const CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    return encode(map, dt, 3, const_cast<T*>(base), gdim, gstride, box,
                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-}  // namespace
-
-cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, int nx, int ny, int nz,
-                                const float c[5], int z0, int z1, int zv0, int zv1, cudaStream_t s)
+template <class T>
+cudaError_t launch_stencil_step_t(const T* u, T* uprev, const T* m, int nx, int ny, int nz,
+                                  const T c[5], int z0, int z1, int zv0, int zv1, cudaStream_t s)
 {
+    using KT = K<T>;
     if (nx <= 0 || ny <= 0 || nx % 4 || z0 < 0 || z1 > nz || zv0 < 0 || zv1 > nz || zv0 >= zv1)
         return cudaErrorInvalidValue;
     if (z1 <= z0) return cudaSuccess;
     CUtensorMap mu, mup, mm;
-    if (!make_map(&mu, u + (size_t)zv0 * nx * ny, nx, ny, zv1 - zv0, SW, SH) ||
-        !make_map(&mup, uprev, nx, ny, nz, TX, TY) || !make_map(&mm, m, nx, ny, nz, TX, TY))
+    if (!make_map(&mu, u + (size_t)zv0 * nx * ny, nx, ny, zv1 - zv0, KT::SW, KT::SH) ||
+        !make_map(&mup, (const T*)uprev, nx, ny, nz, TX, KT::TY) || !make_map(&mm, m, nx, ny, nz, TX, KT::TY))
         return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stencil25_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)kSmemBytes);
+        cudaError_t e = cudaFuncSetAttribute(stencil25_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)KT::kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    Coeffs cf{3.0f * c[0], c[1], c[2], c[3], c[4]};  // fl32(3 c0), as the oracle
+    Coeffs<T> cf{(T)3 * c[0], c[1], c[2], c[3], c[4]};  // fl(3 c0) in T, as the oracle
     // persistent CTAs.  If the plane's tiles fit on the SMs, one CTA per tile
     // marches the whole z range (no chunk prologues; the SMs left over run the
     // decode stream's kernels concurrently).  Otherwise kStencilCTAs CTAs and the
@@ -323,7 +359,7 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
     // (a chunk re-reads 8 halo planes and refills its pipeline).  Measured on
     // 512^2 (128 tiles): 128 CTAs x 1 chunk 108.6 us vs 148 CTAs x 8 chunks 114.7 us.
     const int ntx = (nx + TX - 1) / TX;
-    const long tiles = (long)ntx * ((ny + TY - 1) / TY);
+    const long tiles = (long)ntx * ((ny + KT::TY - 1) / KT::TY);
     const int nzu = z1 - z0;
     int chunk = nzu;
     if (tiles > kStencilCTAs) {
@@ -338,19 +374,58 @@ cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, in
     }
     const long items = tiles * ((nzu + chunk - 1) / chunk);
     const int grid = (int)std::min<long>(kStencilCTAs, items);
-    stencil25_kernel<<<grid, kThreads, kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, ntx, tiles,
-                                                        zv0, cf);
+    stencil25_kernel<T><<<grid, KT::kThreads, KT::kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, ntx,
+                                                                   tiles, zv0, cf);
     note_launches(1);
     return cudaGetLastError();
+}
+
+template <class T>
+oocz_status stencil_steps_t(T* d_u, T* d_uprev, const T* d_m, int nx, int ny, int nz, const T c[5], int nsteps,
+                            cudaStream_t s)
+{
+    T* a = d_u;
+    T* b = d_uprev;
+    for (int k = 0; k < nsteps; k++) {
+        cudaError_t e = launch_stencil_step_t<T>(a, b, d_m, nx, ny, nz, c, 0, nz, 0, nz, s);
+        if (e != cudaSuccess) return stateless_status(e, "oocz_stencil_steps");
+        T* t = a; a = b; b = t;  // newest level now in a
+    }
+    if (a != d_u) {  // odd count: move the levels back into the caller's roles
+        const size_t bytes = (size_t)nx * ny * nz * sizeof(T);
+        void* tmp = nullptr;
+        cudaError_t e = cudaMallocAsync(&tmp, bytes, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(tmp, d_u, bytes, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, d_uprev, bytes, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_uprev, tmp, bytes, cudaMemcpyDeviceToDevice, s);
+        if (e == cudaSuccess) e = cudaFreeAsync(tmp, s);
+        if (e != cudaSuccess) return stateless_status(e, "oocz_stencil_steps");
+    }
+    return OOCZ_OK;
+}
+
+}  // namespace
+
+cudaError_t launch_stencil_step(const float* u, float* uprev, const float* m, int nx, int ny, int nz,
+                                const float c[5], int z0, int z1, int zv0, int zv1, cudaStream_t s)
+{
+    return launch_stencil_step_t<float>(u, uprev, m, nx, ny, nz, c, z0, z1, zv0, zv1, s);
+}
+
+cudaError_t launch_stencil_step(const double* u, double* uprev, const double* m, int nx, int ny, int nz,
+                                const double c[5], int z0, int z1, int zv0, int zv1, cudaStream_t s)
+{
+    return launch_stencil_step_t<double>(u, uprev, m, nx, ny, nz, c, z0, z1, zv0, zv1, s);
 }
 
 }  // namespace oocz
 
 // ------------------------------------------------------------------ C ABI
-extern "C" oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev, const float* d_m,
-                                                int32_t nx, int32_t ny, int32_t nz, const float c[5],
-                                                int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
-                                                void* stream)
+namespace {
+template <class T>
+oocz_status step_planes_abi(const T* d_u, T* d_uprev, const T* d_m, int32_t nx, int32_t ny, int32_t nz,
+                            const T c[5], int32_t z0, int32_t z1, int32_t zv0, int32_t zv1, void* stream,
+                            const char* fn)
 {
     if (nx % 4) return OOCZ_EALIGN;
     if (!d_u || !d_uprev || !d_m || !c || nx <= 0 || ny <= 0 || nz <= 0 || z0 < 0 || z1 > nz ||
@@ -358,7 +433,24 @@ extern "C" oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev
         return OOCZ_EINVAL;
     cudaError_t e = oocz::launch_stencil_step(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1,
                                               (cudaStream_t)stream);
-    return oocz::stateless_status(e, __func__);
+    return oocz::stateless_status(e, fn);
+}
+}  // namespace
+
+extern "C" oocz_status oocz_stencil_step_planes(const float* d_u, float* d_uprev, const float* d_m,
+                                                int32_t nx, int32_t ny, int32_t nz, const float c[5],
+                                                int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
+                                                void* stream)
+{
+    return step_planes_abi(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1, stream, __func__);
+}
+
+extern "C" oocz_status oocz_stencil_step_planes_f64(const double* d_u, double* d_uprev, const double* d_m,
+                                                    int32_t nx, int32_t ny, int32_t nz, const double c[5],
+                                                    int32_t z0, int32_t z1, int32_t zv0, int32_t zv1,
+                                                    void* stream)
+{
+    return step_planes_abi(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1, stream, __func__);
 }
 
 extern "C" oocz_status oocz_stencil_steps(float* d_u, float* d_uprev, const float* d_m, int32_t nx,
@@ -367,23 +459,14 @@ extern "C" oocz_status oocz_stencil_steps(float* d_u, float* d_uprev, const floa
 {
     if (nx % 4) return OOCZ_EALIGN;
     if (!d_u || !d_uprev || !d_m || !c || nx <= 0 || ny <= 0 || nz <= 0 || nsteps < 0) return OOCZ_EINVAL;
-    cudaStream_t s = (cudaStream_t)stream;
-    float* a = d_u;
-    float* b = d_uprev;
-    for (int k = 0; k < nsteps; k++) {
-        cudaError_t e = oocz::launch_stencil_step(a, b, d_m, nx, ny, nz, c, 0, nz, 0, nz, s);
-        if (e != cudaSuccess) return OOCZ_ECUDA;
-        float* t = a; a = b; b = t;  // newest level now in a
-    }
-    if (a != d_u) {  // odd count: move the levels back into the caller's roles
-        const size_t bytes = (size_t)nx * ny * nz * sizeof(float);
-        void* tmp = nullptr;
-        if (cudaMallocAsync(&tmp, bytes, s) != cudaSuccess) return OOCZ_ECUDA;
-        if (cudaMemcpyAsync(tmp, d_u, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
-            cudaMemcpyAsync(d_u, d_uprev, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
-            cudaMemcpyAsync(d_uprev, tmp, bytes, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
-            cudaFreeAsync(tmp, s) != cudaSuccess)
-            return OOCZ_ECUDA;
-    }
-    return OOCZ_OK;
+    return oocz::stencil_steps_t<float>(d_u, d_uprev, d_m, nx, ny, nz, c, nsteps, (cudaStream_t)stream);
+}
+
+extern "C" oocz_status oocz_stencil_steps_f64(double* d_u, double* d_uprev, const double* d_m, int32_t nx,
+                                              int32_t ny, int32_t nz, const double c[5], int32_t nsteps,
+                                              void* stream)
+{
+    if (nx % 4) return OOCZ_EALIGN;
+    if (!d_u || !d_uprev || !d_m || !c || nx <= 0 || ny <= 0 || nz <= 0 || nsteps < 0) return OOCZ_EINVAL;
+    return oocz::stencil_steps_t<double>(d_u, d_uprev, d_m, nx, ny, nz, c, nsteps, (cudaStream_t)stream);
 }

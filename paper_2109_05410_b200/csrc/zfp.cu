@@ -202,6 +202,148 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     }
 }
 
+// ---------------------------------------------------------------- fp64
+// The paper's own precision.  Same shape as the fp32 kernels;
+// 64 bit planes of 64 coefficients each, formed by four 32x32 transposes
+// (coefficients 0-31 / 32-63 x integer bits 0-31 / 32-63).  Both kernels keep
+// the planes in dynamic shared memory, [64][kThreads].
+__device__ __forceinline__ void planes_from_ints64(const uint64_t u[64], uint64_t* planes, int t) {
+    uint32_t a[32], b[32];
+#pragma unroll
+    for (int half = 0; half < 2; half++) {     // integer bits 0-31, then 32-63
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            a[i] = (uint32_t)(u[i] >> (32 * half));
+            b[i] = (uint32_t)(u[i + 32] >> (32 * half));
+        }
+        zb::transpose32(a);
+        zb::transpose32(b);
+#pragma unroll
+        for (int k = 0; k < 32; k++) planes[(32 * half + k) * kThreads + t] = ((uint64_t)b[k] << 32) | a[k];
+    }
+}
+
+__global__ void __launch_bounds__(kThreads)
+zfp_encode64_kernel(const double* __restrict__ in, int nx, int ny, int nbx, int nby,
+                    long long nblocks, int rate, uint64_t* __restrict__ out)
+{
+    extern __shared__ __align__(16) uint64_t smem[];   // [64][kThreads]
+    const int t = threadIdx.x;
+    const long long b = (long long)blockIdx.x * kThreads + t;
+    if (b >= nblocks) return;
+    zb::BitWriter bw{out + (size_t)b * rate, 0ull, 0, 0};
+    const BlockPos p = block_pos(b, nbx, nby);
+    const double* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+    uint64_t v[64];
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const double2* row = reinterpret_cast<const double2*>(base + ((size_t)k * ny + j) * nx);
+            const double2 f0 = __ldg(row), f1 = __ldg(row + 1);
+            v[16 * k + 4 * j + 0] = (uint64_t)__double_as_longlong(f0.x);
+            v[16 * k + 4 * j + 1] = (uint64_t)__double_as_longlong(f0.y);
+            v[16 * k + 4 * j + 2] = (uint64_t)__double_as_longlong(f1.x);
+            v[16 * k + 4 * j + 3] = (uint64_t)__double_as_longlong(f1.y);
+        }
+    const int Emax = zb::block_exponent64(v);
+    if (Emax < 0) {                                    // all-zero block: one 0 bit
+        bw.put(0, 1);
+        bw.finish(rate);
+        return;
+    }
+    bw.put(2ull * (uint64_t)(Emax + 1) + 1ull, zb::kHeaderBits64);   // e = emax + 1023
+    int64_t q[64];
+#pragma unroll
+    for (int i = 0; i < 64; i++) q[i] = zb::quantize64(v[i], Emax);
+    zb::fwd_xform(q);
+    constexpr int perm[64] = OOCZ_PERM3;
+    uint64_t u[64];
+#pragma unroll
+    for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + zb::kNBMask64) ^ zb::kNBMask64;
+    planes_from_ints64(u, smem, t);
+    zb::encode_planes([&](int k) { return smem[k * kThreads + t]; }, 64 * rate - zb::kHeaderBits64, bw, 63);
+    bw.finish(rate);
+}
+
+__global__ void __launch_bounds__(kThreads)
+zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
+                    long long nblocks, int rate, double* __restrict__ out)
+{
+    extern __shared__ __align__(16) uint64_t smem[];   // planes [64][kThreads], then words
+    uint64_t* planes = smem;
+    uint64_t* words = smem + 64 * kThreads;            // [kThreads][rate + 1] + 1 spare
+    const int t = threadIdx.x;
+    const int stride = rate + 1;
+    const long long b0 = (long long)blockIdx.x * kThreads;
+    const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
+    {
+        const int total = (int)nb * rate;
+        const uint64_t* src = in + (size_t)b0 * rate;
+        for (int w = t; w < total; w += kThreads) {
+            const int bb = w / rate, ww = w - bb * rate;
+            words[bb * stride + ww] = __ldg(src + w);
+        }
+        if (t == 0) words[nb * stride] = 0ull;
+    }
+    __syncthreads();
+    if (t >= nb) return;
+    const BlockPos p = block_pos(b0 + t, nbx, nby);
+    double* base = out + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+    zb::BitReader br{words + (size_t)t * stride, 0};
+    if (!br.read(1)) {                                 // zero block -> +0.0
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
+                row[0] = make_double2(0.0, 0.0);
+                row[1] = make_double2(0.0, 0.0);
+            }
+        return;
+    }
+    const int emax = (int)br.read(zb::kEBits64) - 1023;
+    zb::decode_planes([&](int k, uint64_t x) { planes[k * kThreads + t] = x; },
+                      64 * rate - zb::kHeaderBits64, br, 63);
+    uint64_t u[64];
+    {
+        uint32_t a[32], b[32];
+#pragma unroll
+        for (int half = 0; half < 2; half++) {
+#pragma unroll
+            for (int k = 0; k < 32; k++) {
+                const uint64_t x = planes[(32 * half + k) * kThreads + t];
+                a[k] = (uint32_t)x;
+                b[k] = (uint32_t)(x >> 32);
+            }
+            zb::transpose32(a);
+            zb::transpose32(b);
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                if (half == 0) { u[i] = a[i]; u[i + 32] = b[i]; }
+                else { u[i] |= (uint64_t)a[i] << 32; u[i + 32] |= (uint64_t)b[i] << 32; }
+            }
+        }
+    }
+    constexpr int perm[64] = OOCZ_PERM3;
+    int64_t q[64];
+#pragma unroll
+    for (int i = 0; i < 64; i++) q[perm[i]] = (int64_t)((u[i] ^ zb::kNBMask64) - zb::kNBMask64);
+    zb::inv_xform(q);
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            const int l = 16 * k + 4 * j;
+            double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
+            row[0] = make_double2(zb::dequantize64(q[l], emax), zb::dequantize64(q[l + 1], emax));
+            row[1] = make_double2(zb::dequantize64(q[l + 2], emax), zb::dequantize64(q[l + 3], emax));
+        }
+}
+
+size_t encode64_smem_bytes() { return sizeof(uint64_t) * (size_t)(64 * kThreads); }
+size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(64 * kThreads + kThreads * (rate + 1) + 1); }
+
 size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
 // the 64-bit stream window reads up to one word past a block's last word: the
 // row padding, and one spare word after the last row
@@ -254,6 +396,68 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
     return cudaGetLastError();
 }
 
+cudaError_t launch_zfp_encode64(const double* in, int nx, int ny, int nz, int rate,
+                                uint64_t* out, cudaStream_t s)
+{
+    if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
+    const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
+    if (nblocks == 0) return cudaSuccess;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(zfp_encode64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)encode64_smem_bytes());
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const long long grid = (nblocks + kThreads - 1) / kThreads;
+    zfp_encode64_kernel<<<(unsigned)grid, kThreads, encode64_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
+                                                                               nblocks, rate, out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_zfp_decode64(const uint64_t* in, int nx, int ny, int nz, int rate,
+                                double* out, cudaStream_t s)
+{
+    if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
+    const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
+    if (nblocks == 0) return cudaSuccess;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(zfp_decode64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)decode64_smem_bytes(64));
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const long long grid = (nblocks + kThreads - 1) / kThreads;
+    zfp_decode64_kernel<<<(unsigned)grid, kThreads, decode64_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
+                                                                                   nblocks, rate, out);
+    note_launches(1);
+    return cudaGetLastError();
+}
+
+cudaError_t field_encode(const void* src, int esz, int nx, int ny, int nplanes, int rate, void* dst,
+                         cudaStream_t s)
+{
+    if (rate == 0)
+        return cudaMemcpyAsync(dst, src, (size_t)nplanes * nx * ny * esz, cudaMemcpyDeviceToDevice, s);
+    return esz == 8 ? launch_zfp_encode64(static_cast<const double*>(src), nx, ny, nplanes, rate,
+                                          static_cast<uint64_t*>(dst), s)
+                    : launch_zfp_encode(static_cast<const float*>(src), nx, ny, nplanes, rate,
+                                        static_cast<uint64_t*>(dst), s);
+}
+
+cudaError_t field_decode(const void* src, int esz, int nx, int ny, int nplanes, int rate, void* dst,
+                         cudaStream_t s)
+{
+    if (rate == 0)
+        return cudaMemcpyAsync(dst, src, (size_t)nplanes * nx * ny * esz, cudaMemcpyDeviceToDevice, s);
+    return esz == 8 ? launch_zfp_decode64(static_cast<const uint64_t*>(src), nx, ny, nplanes, rate,
+                                          static_cast<double*>(dst), s)
+                    : launch_zfp_decode(static_cast<const uint64_t*>(src), nx, ny, nplanes, rate,
+                                        static_cast<float*>(dst), s);
+}
+
 }  // namespace oocz
 
 // ------------------------------------------------------------------ C ABI
@@ -280,5 +484,25 @@ extern "C" oocz_status oocz_zfp_decode(const uint64_t* d_in, int32_t nx, int32_t
     if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
         return OOCZ_EINVAL;
     cudaError_t e = oocz::launch_zfp_decode(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
+    return oocz::stateless_status(e, __func__);
+}
+
+extern "C" oocz_status oocz_zfp_encode_f64(const double* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                           int32_t rate, uint64_t* d_out, void* stream)
+{
+    if (nx % 4 || ny % 4 || nz % 4) return OOCZ_EALIGN;
+    if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
+        return OOCZ_EINVAL;
+    cudaError_t e = oocz::launch_zfp_encode64(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
+    return oocz::stateless_status(e, __func__);
+}
+
+extern "C" oocz_status oocz_zfp_decode_f64(const uint64_t* d_in, int32_t nx, int32_t ny, int32_t nz,
+                                           int32_t rate, double* d_out, void* stream)
+{
+    if (nx % 4 || ny % 4 || nz % 4) return OOCZ_EALIGN;
+    if (nx < 0 || ny < 0 || nz < 0 || rate < 1 || rate > 64 || ((!d_in || !d_out) && (size_t)nx * ny * nz != 0))
+        return OOCZ_EINVAL;
+    cudaError_t e = oocz::launch_zfp_decode64(d_in, nx, ny, nz, rate, d_out, (cudaStream_t)stream);
     return oocz::stateless_status(e, __func__);
 }

@@ -17,6 +17,7 @@
 // this header (tests/native/zfp_host_check.cu) can exercise the same logic; the
 // library itself only calls them from CUDA kernels.
 #pragma once
+#include <cmath>
 #include <cstdint>
 #include <cstring>
 
@@ -56,13 +57,18 @@ ZB_HD int ctz64(uint64_t x) {
 ZB_HD uint64_t lowmask(int m) { return m >= 64 ? ~0ull : ((1ull << m) - 1ull); }
 ZB_HD uint64_t shr64(uint64_t x, int s) { return s >= 64 ? 0ull : (x >> s); }
 
-// 32-bit two's-complement wraparound arithmetic with arithmetic >> (App. A)
-ZB_HD int32_t add(int32_t a, int32_t b) { return (int32_t)((uint32_t)a + (uint32_t)b); }
-ZB_HD int32_t sub(int32_t a, int32_t b) { return (int32_t)((uint32_t)a - (uint32_t)b); }
-ZB_HD int32_t shl1(int32_t a) { return (int32_t)((uint32_t)a << 1); }
-ZB_HD int32_t asr1(int32_t a) { return a >> 1; }
+// Two's-complement wraparound arithmetic with arithmetic >> (App. A), on the
+// block's integer type I (int32_t for fp32 data, int64_t for fp64 data)
+template <class I> struct UnsignedOf;
+template <> struct UnsignedOf<int32_t> { using type = uint32_t; };
+template <> struct UnsignedOf<int64_t> { using type = uint64_t; };
+template <class I> ZB_HD I add(I a, I b) { using U = typename UnsignedOf<I>::type; return (I)((U)a + (U)b); }
+template <class I> ZB_HD I sub(I a, I b) { using U = typename UnsignedOf<I>::type; return (I)((U)a - (U)b); }
+template <class I> ZB_HD I shl1(I a) { using U = typename UnsignedOf<I>::type; return (I)((U)a << 1); }
+template <class I> ZB_HD I asr1(I a) { return a >> 1; }
 
-ZB_HD void fwd_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+template <class I>
+ZB_HD void fwd_lift(I& x, I& y, I& z, I& w) {
     x = add(x, w); x = asr1(x); w = sub(w, x);
     z = add(z, y); z = asr1(z); y = sub(y, z);
     x = add(x, z); x = asr1(x); z = sub(z, x);
@@ -70,7 +76,8 @@ ZB_HD void fwd_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
     w = add(w, asr1(y)); y = sub(y, asr1(w));
 }
 
-ZB_HD void inv_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
+template <class I>
+ZB_HD void inv_lift(I& x, I& y, I& z, I& w) {
     y = add(y, asr1(w)); w = sub(w, asr1(y));
     y = add(y, w); w = shl1(w); w = sub(w, y);
     z = add(z, x); x = shl1(x); x = sub(x, z);
@@ -79,7 +86,8 @@ ZB_HD void inv_lift(int32_t& x, int32_t& y, int32_t& z, int32_t& w) {
 }
 
 // q[i + 4j + 16k]; lines along x, then y, then z
-ZB_HD void fwd_xform(int32_t q[64]) {
+template <class I>
+ZB_HD void fwd_xform(I q[64]) {
 ZB_UNROLL
     for (int l = 0; l < 16; l++) { int b = 4 * l; fwd_lift(q[b], q[b + 1], q[b + 2], q[b + 3]); }
 ZB_UNROLL
@@ -88,7 +96,8 @@ ZB_UNROLL
     for (int l = 0; l < 16; l++) { int b = l; fwd_lift(q[b], q[b + 16], q[b + 32], q[b + 48]); }
 }
 
-ZB_HD void inv_xform(int32_t q[64]) {
+template <class I>
+ZB_HD void inv_xform(I q[64]) {
 ZB_UNROLL
     for (int l = 0; l < 16; l++) { int b = l; inv_lift(q[b], q[b + 16], q[b + 32], q[b + 48]); }
 ZB_UNROLL
@@ -148,6 +157,42 @@ ZB_HD float dequantize(int32_t q, int emax) {
     double s;
     std::memcpy(&s, &sb, sizeof s);
     return (float)((double)(float)q * s);
+#endif
+}
+
+// ---- fp64 (EBITS 11, EBIAS 1023, 64 bit planes, q = trunc(x * 2^(62 - emax)))
+constexpr uint64_t kNBMask64 = 0xaaaaaaaaaaaaaaaaull;
+constexpr int kEBits64 = 11;
+constexpr int kHeaderBits64 = 1 + kEBits64;
+
+// biased exponent E of the largest magnitude (emax = E - 1022, E = 0 for an
+// all-denormal block), or -1 for an all-zero block
+ZB_HD int block_exponent64(const uint64_t v[64]) {
+    uint64_t mx = 0;
+ZB_UNROLL
+    for (int i = 0; i < 64; i++) { uint64_t a = v[i] & 0x7fffffffffffffffull; mx = a > mx ? a : mx; }
+    return mx == 0 ? -1 : (int)(mx >> 52);
+}
+
+// q = trunc(x * 2^(62 - emax)) from the bit fields: x = mant * 2^(max(E,1) - 1075)
+ZB_HD int64_t quantize64(uint64_t bits, int Emax) {
+    int E = (int)((bits >> 52) & 0x7ffu);
+    uint64_t mant = (bits & 0xfffffffffffffull) | (E ? 0x10000000000000ull : 0ull);
+    int s = (E < 1 ? 1 : E) - Emax + 9;                         // <= 9
+    uint64_t a = s >= 0 ? (mant << s) : (s > -64 ? (mant >> (-s)) : 0ull);
+    return (bits >> 63) ? -(int64_t)a : (int64_t)a;
+}
+
+// x = fl64(fl64(q) * 2^(emax - 62)), one rounding of the exact product (ldexp)
+ZB_HD double dequantize64(int64_t q, int emax) {
+#if defined(__CUDA_ARCH__)
+    const double a = __ll2double_rn(q);
+    if (emax >= -960)            // every nonzero result is normal: the product is exact
+        return __dmul_rn(a, __longlong_as_double((long long)(emax - 62 + 1023) << 52));
+    // subnormal results: an exact scaling by 2^-64 first, then one rounding
+    return __dmul_rn(__dmul_rn(a, 0x1p-64), __longlong_as_double((long long)(emax - 62 + 64 + 1023) << 52));
+#else
+    return std::ldexp((double)q, emax - 62);
 #endif
 }
 
@@ -283,8 +328,8 @@ ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
 }
 
 template <class PlaneAt>
-ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw) {
-    EncState st{31, 0, bits, false};
+ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw, int top_plane = 31) {
+    EncState st{top_plane, 0, bits, false};
     while (st.active()) encode_event(st, plane_at, bw);
 }
 
@@ -340,8 +385,8 @@ ZB_HD void decode_event(DecState& st, BitReader& br, PlaneSet plane_set) {
 }
 
 template <class PlaneSet>
-ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br) {
-    DecState st{31, 0, bits, false, 0u, 0u};
+ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br, int top_plane = 31) {
+    DecState st{top_plane, 0, bits, false, 0u, 0u};
     while (st.active()) decode_event(st, br, plane_set);
     for (int k = st.k; k >= 0; --k) plane_set(k, 0ull);
 }

@@ -34,7 +34,8 @@ class oocz_config(C.Structure):
     _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("nz", C.c_int32),
                 ("c", C.c_float * 5), ("tb", C.c_int32), ("block_planes", C.c_int32),
                 ("rate", C.c_int32 * 3), ("store", C.c_int32), ("slots", C.c_int32),
-                ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32)]
+                ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32),
+                ("precision", C.c_int32), ("c64", C.c_double * 5)]
 
 
 class oocz_stats(C.Structure):
@@ -63,6 +64,8 @@ _SIGS = {
     "oocz_status_string": (C.c_char_p, [C.c_int]),
     "oocz_default_config": (None, [C.POINTER(oocz_config), _i32, _i32, _i32]),
     "oocz_cfl_limit": (C.c_double, [C.POINTER(C.c_float)]),
+    "oocz_cfl_limit_f64": (C.c_double, [C.POINTER(C.c_double)]),
+    "oocz_get_config": (C.c_int, [_ctx_p, C.POINTER(oocz_config)]),
     "oocz_validate": (C.c_int, [C.POINTER(oocz_config), _i32, C.c_char_p, C.c_size_t]),
     "oocz_get_nccl_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "oocz_create": (C.c_int, [C.POINTER(oocz_config), _i32, _i32, C.POINTER(C.c_uint8), _i32, C.POINTER(_ctx_p)]),
@@ -86,6 +89,11 @@ _SIGS = {
     "oocz_stencil_steps": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, C.POINTER(C.c_float), _i32, _vp]),
     "oocz_stencil_step_planes": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, C.POINTER(C.c_float),
                                            _i32, _i32, _i32, _i32, _vp]),
+    "oocz_zfp_encode_f64": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "oocz_zfp_decode_f64": (C.c_int, [_vp, _i32, _i32, _i32, _i32, _vp, _vp]),
+    "oocz_stencil_steps_f64": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, C.POINTER(C.c_double), _i32, _vp]),
+    "oocz_stencil_step_planes_f64": (C.c_int, [_vp, _vp, _vp, _i32, _i32, _i32, C.POINTER(C.c_double),
+                                               _i32, _i32, _i32, _i32, _vp]),
     "oocz_kernel_launch_count": (C.c_uint64, []),
 }
 for _name, (_res, _args) in _SIGS.items():
@@ -141,6 +149,10 @@ def _c5(c) -> C.Array:
     return arr
 
 
+def _c5d(c) -> C.Array:
+    return (C.c_double * 5)(*[float(v) for v in np.asarray(c, np.float64)])
+
+
 # ------------------------------------------------------------------ library
 def oocz_abi_version() -> int:
     return _lib.oocz_abi_version()
@@ -155,6 +167,8 @@ def oocz_default_config(nx: int, ny: int, nz: int, **kw) -> oocz_config:
             cfg.rate = (C.c_int32 * 3)(*v)
         elif k == "c":
             cfg.c = _c5(v)
+        elif k == "c64":
+            cfg.c64 = _c5d(v)
         else:
             setattr(cfg, k, v)
     return cfg
@@ -162,6 +176,21 @@ def oocz_default_config(nx: int, ny: int, nz: int, **kw) -> oocz_config:
 
 def oocz_cfl_limit(c) -> float:
     return float(_lib.oocz_cfl_limit(_c5(c)))
+
+
+def oocz_cfl_limit_f64(c) -> float:
+    return float(_lib.oocz_cfl_limit_f64(_c5d(c)))
+
+
+def oocz_get_config(ctx: int) -> oocz_config:
+    cfg = oocz_config()
+    _check(_lib.oocz_get_config(ctx, C.byref(cfg)), ctx)
+    return cfg
+
+
+def field_dtype(ctx: int):
+    """numpy dtype of the context's fields (precision 32 -> float32, 64 -> float64)."""
+    return np.float64 if oocz_get_config(ctx).precision == 64 else np.float32
 
 
 def oocz_validate(cfg: oocz_config, world: int = 1) -> tuple[int, str]:
@@ -199,7 +228,7 @@ def oocz_step_local_group(ctxs: list[int], nsteps: int) -> None:
 
 
 def oocz_set_field(ctx: int, field: int, src: np.ndarray) -> None:
-    a = np.ascontiguousarray(src, np.float32)
+    a = np.ascontiguousarray(src, field_dtype(ctx))
     _check(_lib.oocz_set_field(ctx, field, a.ctypes.data, a.size), ctx)
 
 
@@ -212,7 +241,7 @@ def oocz_step(ctx: int, nsteps: int) -> None:
 
 
 def oocz_get_field(ctx: int, field: int, dst: np.ndarray) -> np.ndarray:
-    assert dst.dtype == np.float32 and dst.flags.c_contiguous
+    assert dst.dtype == field_dtype(ctx) and dst.flags.c_contiguous
     _check(_lib.oocz_get_field(ctx, field, dst.ctypes.data, dst.size), ctx)
     return dst
 
@@ -281,6 +310,24 @@ def oocz_stencil_step_planes(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1,
                                          z0, z1, zv0, zv1, _stream(stream)))
 
 
+def oocz_zfp_encode_f64(d_in, nx, ny, nz, rate, d_out, stream=None) -> None:
+    _check(_lib.oocz_zfp_encode_f64(_ptr(d_in), nx, ny, nz, rate, _ptr(d_out), _stream(stream)))
+
+
+def oocz_zfp_decode_f64(d_in, nx, ny, nz, rate, d_out, stream=None) -> None:
+    _check(_lib.oocz_zfp_decode_f64(_ptr(d_in), nx, ny, nz, rate, _ptr(d_out), _stream(stream)))
+
+
+def oocz_stencil_steps_f64(d_u, d_uprev, d_m, nx, ny, nz, c, nsteps, stream=None) -> None:
+    _check(_lib.oocz_stencil_steps_f64(_ptr(d_u), _ptr(d_uprev), _ptr(d_m), nx, ny, nz, _c5d(c), nsteps,
+                                       _stream(stream)))
+
+
+def oocz_stencil_step_planes_f64(d_u, d_uprev, d_m, nx, ny, nz, c, z0, z1, zv0, zv1, stream=None) -> None:
+    _check(_lib.oocz_stencil_step_planes_f64(_ptr(d_u), _ptr(d_uprev), _ptr(d_m), nx, ny, nz, _c5d(c),
+                                             z0, z1, zv0, zv1, _stream(stream)))
+
+
 def oocz_kernel_launch_count() -> int:
     return int(_lib.oocz_kernel_launch_count())
 
@@ -288,6 +335,11 @@ def oocz_kernel_launch_count() -> int:
 def default_coeffs() -> np.ndarray:
     cfg = oocz_default_config(4, 4, 4)
     return np.array(list(cfg.c), np.float32)
+
+
+def default_coeffs64() -> np.ndarray:
+    cfg = oocz_default_config(4, 4, 4)
+    return np.array(list(cfg.c64), np.float64)
 
 
 # ------------------------------------------------------------------ convenience
@@ -300,6 +352,7 @@ class Stepper:
         self.world = world
         self.ctx = oocz_create(cfg, rank, world, nccl_id, device)
         self.shape = (cfg.nz // world, cfg.ny, cfg.nx)
+        self.dtype = np.float64 if cfg.precision == 64 else np.float32
 
     def set(self, u, uprev, m):
         for f, a in ((OOCZ_U, u), (OOCZ_UPREV, uprev), (OOCZ_M, m)):
@@ -309,7 +362,7 @@ class Stepper:
         oocz_step(self.ctx, n)
 
     def get(self, field: int) -> np.ndarray:
-        return oocz_get_field(self.ctx, field, np.empty(self.shape, np.float32))
+        return oocz_get_field(self.ctx, field, np.empty(self.shape, self.dtype))
 
     def stats(self) -> dict:
         return oocz_get_stats(self.ctx)

@@ -24,7 +24,7 @@ def test_every_header_symbol_is_exported(z):
 
 
 def test_abi_version(z):
-    assert z.oocz_abi_version() == 1
+    assert z.oocz_abi_version() == 2
 
 
 def test_zfp_bytes_closed_form(z):
@@ -35,6 +35,7 @@ def test_zfp_bytes_closed_form(z):
 
 def test_cfl_limit_default_coefficients(z):
     assert abs(z.oocz_cfl_limit(z.default_coeffs()) - float(Fraction(105, 512))) < 1e-6
+    assert abs(z.oocz_cfl_limit_f64(z.default_coeffs64()) - float(Fraction(105, 512))) < 1e-9
 
 
 @pytest.mark.parametrize("kw,world,code,msg", [
@@ -48,6 +49,8 @@ def test_cfl_limit_default_coefficients(z):
     (dict(block_planes=30), 1, -2, "P (30)"),
     (dict(slots=1), 1, -1, "slots"),
     (dict(store=7), 1, -1, "store"),
+    (dict(precision=16), 1, -1, "precision (16)"),
+    (dict(precision=64, block_planes=32), 1, 0, ""),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)
@@ -64,3 +67,4 @@ def test_default_config(z):
     assert list(cfg.rate) == [16, 16, 16] and cfg.store == 0 and cfg.slots == 2
     import oracle
     assert list(cfg.c) == list(oracle.default_coeffs())
+    assert cfg.precision == 32 and list(cfg.c64) == list(oracle.C64)

@@ -28,6 +28,9 @@ def zb():
     u64p = np.ctypeslib.ndpointer(np.uint64, flags="C_CONTIGUOUS")
     L.zb_encode_block.argtypes = [f32p, C.c_int, u64p]
     L.zb_decode_block.argtypes = [u64p, C.c_int, f32p]
+    f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
+    L.zb_encode_block64.argtypes = [f64p, C.c_int, u64p]
+    L.zb_decode_block64.argtypes = [u64p, C.c_int, f64p]
     return L
 
 
@@ -69,3 +72,52 @@ def test_decode_matches_oracle_on_arbitrary_bits(zb):
         got = np.zeros(64, np.float32)
         zb.zb_decode_block(words, rate, got)
         assert np.array_equal(got.view(np.uint32), want.view(np.uint32)), (n, rate)
+
+
+def _blocks64(n, seed):
+    """fp64 blocks: wide dynamic range, denormals, constants, fp32-promoted data."""
+    rng = np.random.default_rng(seed)
+    out = np.zeros((n, 64))
+    f32 = synth.random_blocks(n, seed=seed + 1)
+    for b in range(n):
+        kind = b % 6
+        if kind == 0:
+            out[b] = rng.standard_normal(64) * 2.0 ** rng.integers(-900, 900)
+        elif kind == 1:
+            out[b] = rng.standard_normal(64) * 2.0 ** rng.integers(-1000, 1000, 64)
+        elif kind == 2:
+            out[b] = rng.integers(-(1 << 52), 1 << 52, 64).astype(np.float64) * 2.0 ** -1074
+        elif kind == 3:
+            out[b] = rng.standard_normal() * 2.0 ** rng.integers(-1074, 1000)
+        elif kind == 4:
+            out[b] = rng.standard_normal(64) * 2.0 ** rng.integers(-1060, -940)   # slow dequant path
+        else:
+            out[b] = f32[b].astype(np.float64)
+    return out
+
+
+def test_encode64_matches_oracle(zb):
+    for n, b in enumerate(_blocks64(900, 41)):
+        for rate in RATES[n % 3::3]:
+            want, _ = oracle.encode_block64(b, rate)
+            got = np.zeros(rate, np.uint64)
+            zb.zb_encode_block64(np.ascontiguousarray(b), rate, got)
+            assert np.array_equal(got, want), (n, rate)
+
+
+def test_decode64_matches_oracle(zb):
+    rng = np.random.default_rng(42)
+    blocks = _blocks64(600, 43)
+    for n in range(1800):
+        rate = int(RATES[n % len(RATES)])
+        if n < 600:
+            words, _ = oracle.encode_block64(blocks[n], rate)
+        else:                  # arbitrary bit patterns (budget ends anywhere)
+            words = rng.integers(0, 1 << 63, rate, dtype=np.uint64) * 2 + rng.integers(0, 2, rate, dtype=np.uint64)
+            if n % 5 == 0:
+                words &= rng.integers(0, 1 << 63, rate, dtype=np.uint64)
+                words[0] |= 1
+        want, _ = oracle.decode_block64(words, rate)
+        got = np.zeros(64)
+        zb.zb_decode_block64(words, rate, got)
+        assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (n, rate)
