@@ -56,7 +56,18 @@ constexpr int TX = 128;                           // 32 lanes x 4 consecutive x
 // 224 registers per thread), u ring 8, u-/m ring 4: 203 KiB of shared memory.
 template <class T> struct Tile;
 template <> struct Tile<float> { static constexpr int TY = 16, NU = OOCZ_STENCIL_NU, NR = OOCZ_STENCIL_NR; };
-template <> struct Tile<double> { static constexpr int TY = 8, NU = 8, NR = 4; };
+#ifndef OOCZ_STENCIL64_TY
+#define OOCZ_STENCIL64_TY 8
+#endif
+#ifndef OOCZ_STENCIL64_NU
+#define OOCZ_STENCIL64_NU 8
+#endif
+#ifndef OOCZ_STENCIL64_NR
+#define OOCZ_STENCIL64_NR 4
+#endif
+template <> struct Tile<double> {
+    static constexpr int TY = OOCZ_STENCIL64_TY, NU = OOCZ_STENCIL64_NU, NR = OOCZ_STENCIL64_NR;
+};
 
 template <class T> struct K {
     static constexpr int TY = Tile<T>::TY, NU = Tile<T>::NU, NR = Tile<T>::NR;
@@ -92,6 +103,19 @@ __device__ __forceinline__ void st4(double* p, const double r[4]) {
     reinterpret_cast<double2*>(p)[0] = make_double2(r[0], r[1]);
     reinterpret_cast<double2*>(p)[1] = make_double2(r[2], r[3]);
 }
+// Ring-slot release discipline: a shared-memory load (LDS) may still be in
+// flight when a later mbarrier.arrive is executed (ptxas does not wait for the
+// load's scoreboard before SYNCS.ARRIVE), and the producer's next TMA write
+// into the slot is not ordered after it -- a WAR race, measured on B200 as
+// rare wrong neighbours.  So every value read from a slot is first CONSUMED:
+// passed to an empty volatile asm, which forces the load to have returned, and
+// volatile asms keep their order relative to the arrive.
+__device__ __forceinline__ void consumed(float v) { asm volatile("" ::"f"(v)); }
+__device__ __forceinline__ void consumed(double v) { asm volatile("" ::"d"(v)); }
+template <class T> __device__ __forceinline__ void consumed(const V4<T>& v) {
+    consumed(v.v[0]); consumed(v.v[1]); consumed(v.v[2]); consumed(v.v[3]);
+}
+
 __device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
 __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
@@ -241,7 +265,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
         for (int i = 0; i < 8; i++) {
             const int p = pfirst + i;
             q[i] = ld4(wait_u(p) + cidx);
-            if (p < zb || p >= ze) release_u(p);
+            if (p < zb || p >= ze) { consumed(q[i]); release_u(p); }
         }
 
         for (int z = zb; z < ze; z++) {
@@ -261,12 +285,22 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
 #pragma unroll
                 for (int o = 0; o < 4; o++) ay[d - 1][o] = add_rn(a.v[o], b.v[o]);
             }
-            release_u(z);
-            if (z + 4 >= ze) release_u(z + 4);
-
+            // x-neighbour pairs (the first addition of the prescribed order too)
             const V4<T> uc = q[4];
             const T w[12] = {xl.v[0], xl.v[1], xl.v[2], xl.v[3], uc.v[0], uc.v[1], uc.v[2], uc.v[3],
                              xr.v[0], xr.v[1], xr.v[2], xr.v[3]};
+            T ax[4][4];
+#pragma unroll
+            for (int o = 0; o < 4; o++)
+#pragma unroll
+                for (int d = 1; d <= 4; d++) ax[d - 1][o] = add_rn(w[4 + o - d], w[4 + o + d]);
+#pragma unroll
+            for (int d = 0; d < 4; d++)
+#pragma unroll
+                for (int o = 0; o < 4; o++) { consumed(ax[d][o]); consumed(ay[d][o]); }
+            release_u(z);
+            if (z + 4 >= ze) { consumed(q[8]); release_u(z + 4); }
+
             T Lv[4];
 #pragma unroll
             for (int o = 0; o < 4; o++) {
@@ -274,9 +308,8 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                 T sd[4];
 #pragma unroll
                 for (int d = 1; d <= 4; d++) {
-                    const T ax = add_rn(w[4 + o - d], w[4 + o + d]);
                     const T az = add_rn(q[4 - d].v[o], q[4 + d].v[o]);
-                    sd[d - 1] = add_rn(add_rn(ax, ay[d - 1][o]), az);
+                    sd[d - 1] = add_rn(add_rn(ax[d - 1][o], ay[d - 1][o]), az);
                 }
                 T L = mul_rn(cf.c0x3, u0);
                 L = fma_rn(cf.c1, sd[0], L);
@@ -289,11 +322,14 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             mbar_wait(&rfull[g % NR], (g / NR) & 1);
             const V4<T> upv = ld4(rt + ridx);
             const V4<T> mv = ld4(rt + TX * TY + ridx);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rempty[g % NR]);
             T res[4];
 #pragma unroll
-            for (int o = 0; o < 4; o++) res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
+            for (int o = 0; o < 4; o++) {
+                res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
+                consumed(res[o]);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&rempty[g % NR]);
             if (active) st4(uprev + (size_t)z * plane + col, res);
             // shift the queue (an unroll by 9 to rotate by renaming measured slower:
             // 9x the code, instruction-cache and register pressure)

@@ -214,3 +214,28 @@ def test_set_field64_checks():
         assert ei.value.status == z.OOCZ_ECFL
         s.set(u, up, m)
         assert np.array_equal(b64(s.get(z.OOCZ_U)), b64(oracle.roundtrip64(u, 32)))
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_stencil_ring_release_stress(dtype):
+    """Regression for a measured WAR race: a ring slot released while the
+    consumer's shared-memory loads were still in flight (stencil
+    "slot release").  Ragged last y-tiles made it visible in fp64 as wrong
+    neighbours in ~10% of launches; 40 launches per shape must all be exact."""
+    import torch
+    z = Z()
+    for (nx, ny, nz) in [(136, 10, 37), (264, 20, 30)]:
+        if dtype == "f64":
+            u, up, m = _state64(nx, ny, nz, 9)
+            want = oracle.step_f64(u, up, m)
+            fn, c = z.oocz_stencil_step_planes_f64, z.default_coeffs64()
+        else:
+            u, up, m = (a.astype(np.float32) for a in _state64(nx, ny, nz, 9))
+            want = oracle.step(u, up, m)
+            fn, c = z.oocz_stencil_step_planes, z.default_coeffs()
+        du, dm = to_dev(u), to_dev(m)
+        for _ in range(40):
+            dup = to_dev(up)
+            fn(du, dup, dm, nx, ny, nz, c, 0, nz, 0, nz, torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            assert np.array_equal(dup.cpu().numpy(), want), (nx, ny, nz)
