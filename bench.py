@@ -109,16 +109,16 @@ def make_fields(rank: int, S: int):
 
 
 def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
-             tb=T):
+             tb=T, precision=32):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
-                                m_resident=m_resident,
+                                m_resident=m_resident, precision=precision,
                                 slots=2, profile=profile)
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
-            Z.oocz_set_field(ctx, f, a)
+            Z.oocz_set_field(ctx, f, a.astype(np.float64) if precision == 64 else a)
         Z.oocz_step(ctx, warmup * tb)
         if dist:
             dist.barrier()
@@ -232,6 +232,22 @@ def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
         t = med(fn)
         res[name] = {"ms": round(t * 1e3, 4), "achieved_GBps": round(nbytes / t / 1e9, 1),
                      "frac": round(nbytes / t / 1e9 / peak_gbs, 4), "algorithmic_bytes": int(nbytes)}
+    # fp64 twins (the paper's precision) at its 2:1 rate 32/64
+    u64, m64 = u.double(), m.double()
+    up64, out64 = u64.clone(), torch.empty_like(u64)
+    r64 = 32
+    words64 = torch.empty(Z.oocz_zfp_bytes(NX, NY, planes, r64) // 8, dtype=torch.int64, device="cuda")
+    cb64 = cells // 64 * 8 * r64
+    for name, fn, nbytes in (
+            ("zfp_encode64_kernel", lambda: Z.oocz_zfp_encode_f64(u64, NX, NY, planes, r64, words64, s),
+             8 * cells + cb64),
+            ("zfp_decode64_kernel", lambda: Z.oocz_zfp_decode_f64(words64, NX, NY, planes, r64, out64, s),
+             8 * cells + cb64),
+            ("stencil25_kernel<double>", lambda: Z.oocz_stencil_step_planes_f64(
+                u64, up64, m64, NX, NY, planes, Z.default_coeffs64(), 4, planes - 4, 0, planes, s), 32 * upd)):
+        t = med(fn)
+        res[name] = {"ms": round(t * 1e3, 4), "achieved_GBps": round(nbytes / t / 1e9, 1),
+                     "frac": round(nbytes / t / 1e9 / peak_gbs, 4), "algorithmic_bytes": int(nbytes)}
     return res
 
 
@@ -317,21 +333,30 @@ def gpu_arm(args):
             # (PAPER.md:217), same P = 128: host bytes per step fall as 1/T, redundant
             # stencil work grows as 4(T-1)/P
             modes += [(f"t{t}_{k}", st, (RATE,) * 3) for t in (8, 12) for k, st in (("dev", 1), ("host", 0))]
+            # the paper's own precision (fp64) and rates 32/64, 24/64
+            # (PAPER.md:213-215): codes 1-4 out of core, plus all fields at 32/64
+            modes += [("f64raw_host", 0, (0, 0, 0)), ("f64pm2_host", 0, (0, 32, 0)),
+                      ("f64pm3_host", 0, (0, 0, 32)), ("f64pm4_host", 0, (0, 24, 24)),
+                      ("f64all_host", 0, (32, 32, 32)), ("f64all_dev", 1, (32, 32, 32)),
+                      ("f64raw_dev", 1, (0, 0, 0))]
         for label, store, rates in modes:
             tb = int(label[1:label.index("_")]) if label.startswith("t") and label[1].isdigit() else T
+            prec = 64 if label.startswith("f64") else 32
             dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
                                                      args.steps, args.warmup, dist,
                                                      profile=int(label in ("zfp_dev", "zfp_host")),
-                                                     m_resident=int(label.startswith("mres")), tb=tb)
+                                                     m_resident=int(label.startswith("mres")), tb=tb,
+                                                     precision=prec)
             sweeps_total = st["sweeps"]
             cells_mode = cells // T * tb
             out[label] = {"s": dev_s, "cups": cells_mode / dev_s, "launches": launches, "evs": evs,
                           "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
                           "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
                           "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
-            if store == 1 or label.startswith("pm") or (label == "raw_host" and not args.quick):
+            if store == 1 or "pm" in label or label.startswith("f64") or (label == "raw_host" and not args.quick):
                 # final u^t, for the compressed-vs-raw error (same step count)
-                out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX), np.float32))
+                out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX),
+                                                                           np.float64 if prec == 64 else np.float32))
             Z.oocz_destroy(ctx)
     clocks = clk.summary()
     if rank != 0:
@@ -354,6 +379,23 @@ def gpu_arm(args):
                                 "speedup": round(out[lab]["cups"] / ref["cups"], 3),
                                 "normwise_max_rel_error": er["normwise_max"],
                                 "mean_pointwise_rel_error": er["mean_pointwise"]}
+    paper_fp64 = None
+    if "f64raw_host" in out:
+        ref = out["f64raw_host"]
+        paper_fp64 = {"what": "the paper's precision and rates (fp64; PAPER.md:208, :212-215): codes 1-4 out of core "
+                              "and every field at 32/64; speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, "
+                              "V100-PCIe)",
+                      "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1),
+                                     "value": round(out["f64raw_dev"]["cups"], 1)}}
+        for key, lab, rates in (("2_rw_32", "f64pm2_host", [0, 32, 0]), ("3_ro_32", "f64pm3_host", [0, 0, 32]),
+                                ("4_rw_ro_24", "f64pm4_host", [0, 24, 24]), ("all_32", "f64all_host", [32, 32, 32])):
+            er = rel_errors(out[lab]["u"], ref["u"])
+            paper_fp64[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
+                               "speedup": round(out[lab]["cups"] / ref["cups"], 3),
+                               "e2e_h2d_bytes_per_step": int(out[lab]["h2d_per_sweep"]),
+                               "normwise_max_rel_error": er["normwise_max"],
+                               "mean_pointwise_rel_error": er["mean_pointwise"]}
+        paper_fp64["all_32"]["value"] = round(out["f64all_dev"]["cups"], 1)
     orch = None
     if "mres_dev" in out:
         orch = {"what": "m decoded once and kept in HBM (m_resident=1): SURVEY 8(f) row 2, beyond the paper",
@@ -420,6 +462,7 @@ def gpu_arm(args):
         "other_rates": per_rate,
         "orchestrated": orch,
         "paper_modes": paper_modes,
+        "paper_precision_fp64": paper_fp64,
         "temporal_blocking": {f"T={t}": {"value": round(out[f"t{t}_dev"]["cups"], 1),
                                          "e2e": round(out[f"t{t}_host"]["cups"], 1),
                                          "e2e_h2d_bytes_per_step": int(out[f"t{t}_host"]["h2d_per_sweep"]),
