@@ -86,23 +86,70 @@ template <class T> struct K {
 
 template <class T> struct Coeffs { T c0x3, c1, c2, c3, c4; };
 
-// 4 consecutive values (one float4, or two double2) and round-to-nearest ops
+// The 4 cells a lane owns, and how they are loaded / stored.
+//   fp32: x = x0 + 4 lane + {0,1,2,3}: one 16-B access, a warp covers 512
+//         contiguous bytes (4 shared-memory wavefronts, conflict-free).
+//   fp64: x = x0 + 2 lane + {0,1} and x0 + 64 + 2 lane + {0,1}: two 16-B
+//         accesses, each covering 512 contiguous bytes per warp.  (Four
+//         consecutive doubles per lane would put 32-B strides on the banks:
+//         twice the wavefronts; ncu measured the kernel shared-memory bound.)
 template <class T> struct V4 { T v[4]; };
+template <class T> struct Lanes;
+template <> struct Lanes<float> {
+    static constexpr int kLaneStride = 4;
+};
+template <> struct Lanes<double> {
+    static constexpr int kLaneStride = 2;
+};
 __device__ __forceinline__ V4<float> ld4(const float* p) {
     const float4 a = *reinterpret_cast<const float4*>(p);
     return V4<float>{{a.x, a.y, a.z, a.w}};
 }
 __device__ __forceinline__ V4<double> ld4(const double* p) {
-    const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+    const double2 a = *reinterpret_cast<const double2*>(p), b = *reinterpret_cast<const double2*>(p + 64);
     return V4<double>{{a.x, a.y, b.x, b.y}};
 }
-__device__ __forceinline__ void st4(float* p, const float r[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
+// store the lane's 4 results; gx = x of its first cell (columns >= nx are not stored)
+__device__ __forceinline__ void st4(float* p, const float r[4], int gx, int nx) {
+    if (gx < nx) *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
 }
-__device__ __forceinline__ void st4(double* p, const double r[4]) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(r[0], r[1]);
-    reinterpret_cast<double2*>(p)[1] = make_double2(r[2], r[3]);
+__device__ __forceinline__ void st4(double* p, const double r[4], int gx, int nx) {
+    if (gx < nx) *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);
+    if (gx + 64 < nx) *reinterpret_cast<double2*>(p + 64) = make_double2(r[2], r[3]);
 }
+
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// x-neighbour pairs ax[d-1][o] = u[x_o - d] + u[x_o + d] of the lane's cells;
+// crow points at the lane's first cell in the u stage, uc holds its centres
+__device__ __forceinline__ void x_pairs(const float* crow, const V4<float>& uc, float ax[4][4]) {
+    const V4<float> xl = ld4(crow - 4), xr = ld4(crow + 4);
+    const float w[12] = {xl.v[0], xl.v[1], xl.v[2], xl.v[3], uc.v[0], uc.v[1], uc.v[2], uc.v[3],
+                         xr.v[0], xr.v[1], xr.v[2], xr.v[3]};
+#pragma unroll
+    for (int o = 0; o < 4; o++)
+#pragma unroll
+        for (int d = 1; d <= 4; d++) ax[d - 1][o] = add_rn(w[4 + o - d], w[4 + o + d]);
+}
+__device__ __forceinline__ void x_pairs(const double* crow, const V4<double>& uc, double ax[4][4]) {
+#pragma unroll
+    for (int g = 0; g < 2; g++) {                  // the two 2-cell groups, 64 apart
+        const double* c = crow + 64 * g;
+        const double2 a = *reinterpret_cast<const double2*>(c - 4), b = *reinterpret_cast<const double2*>(c - 2);
+        const double2 e = *reinterpret_cast<const double2*>(c + 2), f = *reinterpret_cast<const double2*>(c + 4);
+        const double w[10] = {a.x, a.y, b.x, b.y, uc.v[2 * g], uc.v[2 * g + 1], e.x, e.y, f.x, f.y};
+#pragma unroll
+        for (int o = 0; o < 2; o++)
+#pragma unroll
+            for (int d = 1; d <= 4; d++) ax[d - 1][2 * g + o] = add_rn(w[4 + o - d], w[4 + o + d]);
+    }
+}
+
 // Ring-slot release discipline: a shared-memory load (LDS) may still be in
 // flight when a later mbarrier.arrive is executed (ptxas does not wait for the
 // load's scoreboard before SYNCS.ARRIVE), and the producer's next TMA write
@@ -116,12 +163,6 @@ template <class T> __device__ __forceinline__ void consumed(const V4<T>& v) {
     consumed(v.v[0]); consumed(v.v[1]); consumed(v.v[2]); consumed(v.v[3]);
 }
 
-__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
-__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
-__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
-__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ float fma_rn(float a, float b, float c) { return __fmaf_rn(a, b, c); }
-__device__ __forceinline__ double fma_rn(double a, double b, double c) { return __fma_rn(a, b, c); }
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -236,15 +277,16 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
     // ---------------------------------------------------------------- consumers
     const int ty = warp - 1;
     const size_t plane = (size_t)nx * ny;
-    const int cidx = (ty + 4) * SW + 4 + 4 * lane;  // this thread's centre in a u stage
-    const int ridx = ty * TX + 4 * lane;             // ... in a u- / m tile
+    constexpr int LS = Lanes<T>::kLaneStride;
+    const int cidx = (ty + 4) * SW + 4 + LS * lane;  // this thread's (first) centre in a u stage
+    const int ridx = ty * TX + LS * lane;            // ... in a u- / m tile
     long it = blockIdx.x;
     unsigned gu0 = 0, gr0 = 0;                       // global index of the segment's first u / u- plane
     Seg sg;
     while (next_seg<TY>(it, items, tiles, ntx, z0, z1, chunk, sg)) {
         const int zb = sg.zb, ze = sg.ze, pfirst = zb - 4;
-        const int gx = sg.x0 + 4 * lane, gy = sg.y0 + ty;
-        const bool active = gx < nx && gy < ny;
+        const int gx = sg.x0 + LS * lane, gy = sg.y0 + ty;
+        const bool active = gy < ny;                 // (columns: checked per store)
         const size_t col = (size_t)gy * nx + gx;
         auto uslot = [&](int p) { return (gu0 + (unsigned)(p - pfirst)) % NU; };
         auto wait_u = [&](int p) -> const T* {
@@ -273,8 +315,6 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             const unsigned g = gr0 + (unsigned)(z - zb);
             const T* rt = rring + (g % NR) * kRStage;
             const T* crow = uring + uslot(z) * kUStage + cidx;  // plane z already landed
-            const V4<T> xl = ld4(crow - 4);
-            const V4<T> xr = ld4(crow + 4);
             // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
             // which is the first addition of the prescribed order anyway
             T ay[4][4];
@@ -287,13 +327,8 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             }
             // x-neighbour pairs (the first addition of the prescribed order too)
             const V4<T> uc = q[4];
-            const T w[12] = {xl.v[0], xl.v[1], xl.v[2], xl.v[3], uc.v[0], uc.v[1], uc.v[2], uc.v[3],
-                             xr.v[0], xr.v[1], xr.v[2], xr.v[3]};
             T ax[4][4];
-#pragma unroll
-            for (int o = 0; o < 4; o++)
-#pragma unroll
-                for (int d = 1; d <= 4; d++) ax[d - 1][o] = add_rn(w[4 + o - d], w[4 + o + d]);
+            x_pairs(crow, uc, ax);
 #pragma unroll
             for (int d = 0; d < 4; d++)
 #pragma unroll
@@ -330,7 +365,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             }
             __syncwarp();
             if (lane == 0) mbar_arrive(&rempty[g % NR]);
-            if (active) st4(uprev + (size_t)z * plane + col, res);
+            if (active) st4(uprev + (size_t)z * plane + col, res, gx, nx);
             // shift the queue (an unroll by 9 to rotate by renaming measured slower:
             // 9x the code, instruction-cache and register pressure)
 #pragma unroll

@@ -24,3 +24,16 @@ for _ in range(int(os.environ.get("REPS", "3"))):
     Z.oocz_stencil_step_planes(u, up, m, n, n, planes, Z.default_coeffs(), 4, planes - 4, 0, planes, s)
 torch.cuda.synchronize()
 print("done")
+
+if os.environ.get("F64", "0") == "1":
+    r64 = int(os.environ.get("RATE64", "32"))
+    u64, m64 = u.double(), m.double()
+    up64, out64 = u64.clone(), torch.empty_like(u64)
+    w64 = torch.empty(Z.oocz_zfp_bytes(n, n, planes, r64) // 8, dtype=torch.int64, device="cuda")
+    for _ in range(int(os.environ.get("REPS", "3"))):
+        Z.oocz_zfp_encode_f64(u64, n, n, planes, r64, w64, s)
+        Z.oocz_zfp_decode_f64(w64, n, n, planes, r64, out64, s)
+        Z.oocz_stencil_step_planes_f64(u64, up64, m64, n, n, planes, Z.default_coeffs64(), 4, planes - 4, 0,
+                                       planes, s)
+    torch.cuda.synchronize()
+    print("done f64")
