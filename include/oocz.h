@@ -74,6 +74,11 @@ typedef struct {
                               c64; the paper's precision; rates 32/64 and 24/64,
                               PAPER.md:213-215).  Raw rate 0 stores 4 resp. 8 B per value.   */
     double   c64[5];       /* the weights for precision 64 (default: the exact decimals)      */
+    int32_t  serpentine;   /* 1: sweeps alternate ascending / descending inside one oocz_step,
+                              and the block at each turn is processed twice in a row on the
+                              device: its compressed rows never cross the host link in between
+                              (1/D of the traffic per sweep saved).  Orchestration beyond the
+                              paper (R22).  Results identical.  */
 } oocz_config;
 
 typedef struct {

@@ -162,6 +162,7 @@ struct oocz_ctx {
     cudaEvent_t ev_halo = nullptr, ev_join_dec = nullptr;
     std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written;
     long long seq = 0;                      // global block sequence number
+    std::vector<int> last_slot;             // staging slot of each block's latest encode (host store)
     // halo exchange (world > 1)
     HaloComm* halo = nullptr;
     // profiling
@@ -495,6 +496,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     CKC(mk(ctx->ev_out_ready, nslots));
     CKC(mk(ctx->ev_out_free, nslots));
     CKC(mk(ctx->ev_written, D));
+    ctx->last_slot.assign(D, 0);
     CKC(cudaEventCreate(&ctx->ev_t0));
     CKC(cudaEventCreate(&ctx->ev_t1));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_h2d, cudaEventDisableTiming));
@@ -811,77 +813,128 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
 
 // ------------------------------------------------------------------ step
 // Enqueue one block of one sweep (ts steps).
-static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
+//   dir  : +1 ascending (the paper's order, R17), -1 descending (serpentine
+//          sweeps, reading R22);
+//   turn : serpentine turnaround -- block i was the last block of the previous
+//          sweep of this call, so its read unit is on the device already: u, u-
+//          are decoded from the compressed rows just encoded into the staging
+//          slots (or from the device store), and m is still decoded in its slab;
+//   keep : block i is the last block of a sweep that is followed by a
+//          turnaround in this call -- its compressed rows stay in the staging
+//          slot (no D2H; the store rows are rewritten next sweep).
+static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int dir, bool turn, bool keep)
 {
     const Geom& g = ctx->geom[i];
-    const int h = ctx->h, P = ctx->P, D = ctx->D;
+    const int h = ctx->h, P = ctx->P, D = ctx->D, S = ctx->S;
     const size_t pb = ctx->pb;
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
-    const int set = (int)(ctx->seq % 2);         // slab set of this block
+    // slab set: blocks alternate between two; with serpentine sweeps by block
+    // parity, so a turnaround block finds its own slab (and its decoded m) again
+    const int set = ctx->cfg.serpentine ? (i & 1) : (int)(ctx->seq % 2);
     // m_resident: m is read in place from the decoded copy, never streamed
     const int nf = ctx->m_full ? 2 : 3;
     uint8_t* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
                         ctx->m_full ? ctx->m_full + (size_t)(g.slab0 + h) * pb : ctx->slab[set][2]};
-    const int rd_planes = g.rd1 - g.rd0;
+    // read unit: ascending [iP+h, (i+1)P+h) (block 0 from 0); descending
+    // [iP-h, (i+1)P-h) (block D-1 to S); both partition [0, S)
+    const int rd0 = dir > 0 ? g.rd0 : std::max(i * P - h, 0);
+    const int rd1 = dir > 0 ? g.rd1 : (i == D - 1 ? S : (i + 1) * P - h);
+    const int rd_planes = rd1 - rd0;
     const uint8_t* src[3];
     cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
-    // rows written back by blocks i and i+1 of the previous sweep must have landed
-    cudaEvent_t rows_final = ctx->ev_written[std::min(i + 1, D - 1)];
+    const int nb = dir > 0 ? std::min(i + 1, D - 1) : std::max(i - 1, 0);   // the read unit's other owner
 
-    // ---- (a2) H2D of the read unit (u, u-, m) into a staging slot
-    if (host) {
-        cudaStream_t sh = ctx->s_h2d;
-        CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
-        CK(cudaStreamWaitEvent(sh, rows_final, 0));
-        uint64_t bytes = 0;
-        for (int f = 0; f < nf; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
-        prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
-        for (int f = 0; f < nf; f++) {
-            const size_t nbytes = (size_t)(rd_planes / 4) * ctx->row_bytes[f];
-            CK(cudaMemcpyAsync(ctx->in_slot[slot] + ctx->in_off[f], ctx->store[f] + rows_off(ctx, f, g.rd0),
-                               nbytes, cudaMemcpyHostToDevice, sh));
-            src[f] = ctx->in_slot[slot] + ctx->in_off[f];
+    if (turn) {
+        // ---- (a2/a3, turnaround) nothing crosses the host link
+        CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
+        CK(cudaStreamWaitEvent(sd, ctx->ev_written[i], 0));
+        CK(cudaStreamWaitEvent(sd, ctx->ev_written[nb], 0));
+        if (ctx->halo) {
+            std::string herr;
+            CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
+            if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
+                return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
         }
-        prof_end(ctx, sh);
-        ctx->stats.h2d_bytes += bytes;
-        CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
-        CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
+        for (int f = 0; f < 2; f++) {
+            // own rows [iP, (i+1)P), then the neighbour's h rows next to them
+            const uint8_t* own = host ? ctx->out_slot[ctx->last_slot[i]] + ctx->out_off[f]
+                                      : ctx->store[f] + rows_off(ctx, f, g.own0);
+            prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] +
+                                                                 (uint64_t)rd_planes * pb);
+            CK(decode_or_copy(ctx, f, own, P, slab[f] + (size_t)h * pb, sd));
+            if (nb != i) {
+                const int z0 = dir > 0 ? (i + 1) * P : i * P - h;     // rank plane of the neighbour rows
+                const uint8_t* nbr = host
+                    ? ctx->out_slot[ctx->last_slot[nb]] + ctx->out_off[f] + (dir > 0 ? 0 : (size_t)((P - h) / 4) * ctx->row_bytes[f])
+                    : ctx->store[f] + rows_off(ctx, f, z0);
+                CK(decode_or_copy(ctx, f, nbr, h, slab[f] + (size_t)(z0 - g.slab0) * pb, sd));
+            }
+            prof_end(ctx, sd);
+        }
+        if (host) CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[i]], sd));   // the kept slot is read
     } else {
-        CK(cudaStreamWaitEvent(sd, rows_final, 0));
-        for (int f = 0; f < 3; f++) src[f] = ctx->store[f] + rows_off(ctx, f, g.rd0);
-    }
+        // ---- (a2) H2D of the read unit (u, u-, m) into a staging slot, once the
+        // previous sweep has written those rows back
+        if (host) {
+            cudaStream_t sh = ctx->s_h2d;
+            CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
+            CK(cudaStreamWaitEvent(sh, ctx->ev_written[i], 0));
+            CK(cudaStreamWaitEvent(sh, ctx->ev_written[nb], 0));
+            uint64_t bytes = 0;
+            for (int f = 0; f < nf; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
+            prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
+            for (int f = 0; f < nf; f++) {
+                const size_t nbytes = (size_t)(rd_planes / 4) * ctx->row_bytes[f];
+                CK(cudaMemcpyAsync(ctx->in_slot[slot] + ctx->in_off[f], ctx->store[f] + rows_off(ctx, f, rd0),
+                                   nbytes, cudaMemcpyHostToDevice, sh));
+                src[f] = ctx->in_slot[slot] + ctx->in_off[f];
+            }
+            prof_end(ctx, sh);
+            ctx->stats.h2d_bytes += bytes;
+            CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
+            CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
+        } else {
+            CK(cudaStreamWaitEvent(sd, ctx->ev_written[i], 0));
+            CK(cudaStreamWaitEvent(sd, ctx->ev_written[nb], 0));
+            for (int f = 0; f < 3; f++) src[f] = ctx->store[f] + rows_off(ctx, f, rd0);
+        }
 
-    // ---- (a4) slab assembly on the decode stream, once this slab set is free
-    CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
-    if (i > 0) {  // time-t C_{i-1}, kept by the previous block
+        // ---- (a4) slab assembly on the decode stream, once this slab set is free
+        CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
+        const bool has_c = dir > 0 ? i > 0 : i < D - 1;     // the shared region kept by the previous block
+        if (has_c) {
+            // ascending: C_{i-1} -> slab [0, 2h); descending: C_i -> slab [P, P+2h)
+            const size_t dst = dir > 0 ? 0 : (size_t)P * pb;
+            prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
+            for (int f = 0; f < nf; f++)
+                CK(cudaMemcpyAsync(slab[f] + dst, ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
+            prof_end(ctx, sd);
+        }
+        if (ctx->halo) {  // neighbour-rank halos received at the sweep start
+            std::string herr;
+            CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
+            if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
+                return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
+        }
+        // ---- (a3) decode the read unit into the slab
+        for (int f = 0; f < nf; f++) {
+            // algorithmic bytes: compressed (or raw) read unit in + decoded planes out
+            const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
+            prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
+            CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(rd0 - g.slab0) * pb, sd));
+            prof_end(ctx, sd);
+        }
+        if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
+    }
+    // keep the time-t shared region for the next block (reading R14):
+    // ascending C_i = slab [P, P+2h), descending C_{i-1} = slab [0, 2h)
+    if (dir > 0 ? i < D - 1 : i > 0) {
+        const size_t off = dir > 0 ? (size_t)P * pb : 0;
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
         for (int f = 0; f < nf; f++)
-            CK(cudaMemcpyAsync(slab[f], ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
-        prof_end(ctx, sd);
-    }
-    if (ctx->halo) {  // neighbour-rank halos received at the sweep start
-        std::string herr;
-        CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
-        if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, ctx->S, ctx->nx, ctx->ny, sd, &herr))
-            return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
-    }
-    // ---- (a3) decode the read unit into the slab
-    for (int f = 0; f < nf; f++) {
-        // algorithmic bytes: compressed (or raw) read unit in + decoded planes out
-        const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
-        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
-        CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(g.rd0 - g.slab0) * pb, sd));
-        prof_end(ctx, sd);
-    }
-    if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
-    // keep the time-t C_i for block i+1 (reading R14)
-    if (i < D - 1) {
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
-        for (int f = 0; f < nf; f++)
-            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + (size_t)P * pb, (size_t)(2 * h) * pb,
-                               cudaMemcpyDeviceToDevice, sd));
+            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + off, (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
         prof_end(ctx, sd);
     }
     CK(cudaEventRecord(ctx->ev_decoded[set], sd));
@@ -915,20 +968,26 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts)
             prof_end(ctx, sc);
         }
         CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
-        CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
-        // ---- (a7) D2H into the store, in place
-        cudaStream_t so = ctx->s_d2h;
-        CK(cudaStreamWaitEvent(so, ctx->ev_out_ready[slot], 0));
-        uint64_t bytes = 0;
-        for (int f = 0; f < 2; f++) bytes += (uint64_t)(P / 4) * ctx->row_bytes[f];
-        prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, so, bytes);
-        for (int f = 0; f < 2; f++)
-            CK(cudaMemcpyAsync(ctx->store[f] + rows_off(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
-                               (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, so));
-        prof_end(ctx, so);
-        ctx->stats.d2h_bytes += bytes;
-        CK(cudaEventRecord(ctx->ev_out_free[slot], so));
-        CK(cudaEventRecord(ctx->ev_written[i], so));
+        ctx->last_slot[i] = slot;
+        if (keep) {
+            // rows stay in the slot for the turnaround; its decode frees the slot
+            CK(cudaEventRecord(ctx->ev_written[i], sc));
+        } else {
+            CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
+            // ---- (a7) D2H into the store, in place
+            cudaStream_t so = ctx->s_d2h;
+            CK(cudaStreamWaitEvent(so, ctx->ev_out_ready[slot], 0));
+            uint64_t bytes = 0;
+            for (int f = 0; f < 2; f++) bytes += (uint64_t)(P / 4) * ctx->row_bytes[f];
+            prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, so, bytes);
+            for (int f = 0; f < 2; f++)
+                CK(cudaMemcpyAsync(ctx->store[f] + rows_off(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
+                                   (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, so));
+            prof_end(ctx, so);
+            ctx->stats.d2h_bytes += bytes;
+            CK(cudaEventRecord(ctx->ev_out_free[slot], so));
+            CK(cudaEventRecord(ctx->ev_written[i], so));
+        }
     } else {
         for (int f = 0; f < 2; f++) {
             prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
@@ -1033,12 +1092,22 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
                 CK(cudaEventRecord(ctx->ev_halo, ctx->s_comp));   // the decode stream inserts them
             }
         }
+        const bool last_sweep = done + ts >= nsteps;
         for (int r = 0; r < n; r++) {
-            for (int i = 0; i < ctxs[r]->D; i++) {
-                oocz_status st = enqueue_block(ctxs[r], sweep, i, ts);
+            oocz_ctx* ctx = ctxs[r];
+            const int D = ctx->D;
+            // serpentine (reading R22): odd sweeps of the call descend, and the block
+            // at each turn is processed twice in a row without leaving the device
+            const bool serp = ctx->cfg.serpentine != 0;
+            const int dir = serp && (sweep & 1) ? -1 : 1;
+            for (int k = 0; k < D; k++) {
+                const int i = dir > 0 ? k : D - 1 - k;
+                const bool turn = serp && sweep > 0 && k == 0;
+                const bool keep = serp && !last_sweep && k == D - 1;
+                oocz_status st = enqueue_block(ctx, sweep, i, ts, dir, turn, keep);
                 if (st != OOCZ_OK) return st;
             }
-            ctxs[r]->stats.sweeps++;
+            ctx->stats.sweeps++;
         }
         done += ts;
         sweep++;

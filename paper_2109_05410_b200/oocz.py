@@ -35,7 +35,7 @@ class oocz_config(C.Structure):
                 ("c", C.c_float * 5), ("tb", C.c_int32), ("block_planes", C.c_int32),
                 ("rate", C.c_int32 * 3), ("store", C.c_int32), ("slots", C.c_int32),
                 ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32),
-                ("precision", C.c_int32), ("c64", C.c_double * 5)]
+                ("precision", C.c_int32), ("c64", C.c_double * 5), ("serpentine", C.c_int32)]
 
 
 class oocz_stats(C.Structure):

@@ -21,11 +21,11 @@ def _fields(nx, ny, nz, seed, kind="dense"):
     return u, up, synth.layered(nx, ny, nz)
 
 
-def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0):
+def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
-                                slots=slots, profile=profile)
+                                slots=slots, profile=profile, serpentine=serpentine, m_resident=m_resident)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -53,11 +53,12 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("serpentine", [0, 1])
 @pytest.mark.parametrize("store", [0, 1])
 @pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES)
-def test_stepper_matches_oracle(store, nx, ny, nz, T, P, rates, calls):
+def test_stepper_matches_oracle(store, serpentine, nx, ny, nz, T, P, rates, calls):
     u, up, m = _fields(nx, ny, nz, 3)
-    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, store, calls)
+    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, store, calls, serpentine=serpentine)
     ou, oup = _run_oracle(u, up, m, T, rates, calls)
     assert np.array_equal(bits(gu), bits(ou))
     assert np.array_equal(bits(gup), bits(oup))
@@ -204,3 +205,63 @@ def test_m_resident_partitioned_group(world):
             z.oocz_destroy(c)
     ou, _ = _run_oracle(u, up, m, T, rates, [7])
     assert np.array_equal(bits(gu), bits(ou))
+
+
+@pytest.mark.parametrize("m_resident", [0, 1])
+@pytest.mark.parametrize("slots", [2, 3])
+@pytest.mark.parametrize("D,calls", [(4, [12]), (3, [5, 7]), (1, [9]), (2, [4, 4, 1])])
+def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident):
+    """Serpentine sweeps (R22): same bits as the oracle, and the block at
+    each turn never crosses the host link: per call of k sweeps, (k - 1) read units
+    and (k - 1) write units fewer than ascending sweeps."""
+    nx, ny, T, P, rates = 32, 24, 2, 16, (16, 12, 8)
+    nz = D * P
+    u, up, m = _fields(nx, ny, nz, 11)
+    gu, gup, st, evs = _run_gpu(u, up, m, T, P, rates, 0, calls, slots=slots, profile=1, serpentine=1,
+                                m_resident=m_resident)
+    ou, oup = _run_oracle(u, up, m, T, rates, calls)
+    assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+    row = [oracle.zfp_bytes(nx, ny, 4, r) for r in rates]
+    nf = 2 if m_resident else 3
+    h = 4 * T
+    h2d = d2h = 0
+    for n in calls:
+        k = -(-n // T)                                 # sweeps in this call
+        field_rows = nz // 4
+        for s_ in range(k):
+            turn_block = None if s_ == 0 else (D - 1 if s_ % 2 else 0)
+            for i in range(D):
+                if i == turn_block:
+                    continue
+                if s_ % 2 == 0:                        # ascending read unit
+                    rd0, rd1 = (0 if i == 0 else i * P + h), min((i + 1) * P + h, nz)
+                else:                                  # descending
+                    rd0, rd1 = max(i * P - h, 0), (nz if i == D - 1 else (i + 1) * P - h)
+                h2d += (rd1 - rd0) // 4 * sum(row[:nf])
+            kept = 1 if s_ < k - 1 else 0
+            d2h += (D - kept) * (P // 4) * (row[0] + row[1])
+    assert st["h2d_bytes"] == h2d
+    assert st["d2h_bytes"] == d2h
+    _audit(evs)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_serpentine_partitioned_group(world):
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 24, 128, 2, 16, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz, 5)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0, serpentine=1)
+    ctxs = z.oocz_create_local_group(cfg, world)
+    S = nz // world
+    try:
+        for r, c in enumerate(ctxs):
+            for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                z.oocz_set_field(c, f, a[r * S:(r + 1) * S])
+        z.oocz_step_local_group(ctxs, 9)
+        gu = np.concatenate([z.oocz_get_field(c, z.OOCZ_U, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+        gup = np.concatenate([z.oocz_get_field(c, z.OOCZ_UPREV, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+    finally:
+        for c in ctxs:
+            z.oocz_destroy(c)
+    ou, oup = _run_oracle(u, up, m, T, rates, [9])
+    assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))

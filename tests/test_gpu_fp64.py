@@ -143,11 +143,11 @@ CASES64 = [
 ]
 
 
-def _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident=0):
+def _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident=0, serpentine=0):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
-                                precision=64, m_resident=m_resident)
+                                precision=64, m_resident=m_resident, serpentine=serpentine)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -162,14 +162,14 @@ def _run64_oracle(u, up, m, T, rates, calls):
     return a, b
 
 
-@pytest.mark.parametrize("store,m_resident", [(0, 0), (1, 0), (0, 1)])
+@pytest.mark.parametrize("store,m_resident,serp", [(0, 0, 0), (1, 0, 0), (0, 1, 0), (0, 0, 1), (1, 1, 1)])
 @pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES64)
-def test_stepper64_matches_oracle(store, m_resident, nx, ny, nz, T, P, rates, calls):
+def test_stepper64_matches_oracle(store, m_resident, serp, nx, ny, nz, T, P, rates, calls):
     u, up, m = _state64(nx, ny, nz, 3)
-    gu, gup, st = _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident)
+    gu, gup, st = _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident, serp)
     ou, oup = _run64_oracle(u, up, m, T, rates, calls)
     assert np.array_equal(b64(gu), b64(ou)) and np.array_equal(b64(gup), b64(oup))
-    if store == 0:
+    if store == 0 and not serp:
         stored = [oracle.zfp_bytes(nx, ny, nz, r) if r else 8 * nx * ny * nz for r in rates]
         nf = 2 if m_resident else 3
         assert st["h2d_bytes"] == st["sweeps"] * sum(stored[:nf])
