@@ -109,12 +109,12 @@ def make_fields(rank: int, S: int):
 
 
 def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
-             tb=T, precision=32, serpentine=0):
+             tb=T, precision=32, serpentine=0, slots=2):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=2, profile=profile)
+                                slots=slots, profile=profile)
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
@@ -337,7 +337,10 @@ def gpu_arm(args):
             modes += [("pf_zfp_dev", 1, (RATE,) * 3, PF), ("pf_zfp_host", 0, (RATE,) * 3, PF),
                       ("pf_raw_dev", 1, (0, 0, 0), PF), ("pf_raw_host", 0, (0, 0, 0), PF),
                       ("mres_dev", 1, (RATE,) * 3, dict(m_resident=1)), ("mres_host", 0, (RATE,) * 3, dict(m_resident=1)),
-                      ("serp_dev", 1, (RATE,) * 3, dict(serpentine=1)), ("serp_host", 0, (RATE,) * 3, dict(serpentine=1))]
+                      ("serp_dev", 1, (RATE,) * 3, dict(serpentine=1)), ("serp_host", 0, (RATE,) * 3, dict(serpentine=1)),
+                      # a third staging slot: the block after each turn decodes its own rows from
+                      # the device too (they were written back, but need not come back)
+                      ("slots3_host", 0, (RATE,) * 3, dict(O, slots=3))]
             # the paper's codes 2-4 as fp32 rate vectors, out of core,
             # paper-faithful schedule: one read-write field (u-, reading R7) at 16/32, the
             # read-only m at 16/32, one read-write field + m at 12/32 (the paper's 24/64)
@@ -364,7 +367,8 @@ def gpu_arm(args):
                                                      args.steps, args.warmup, dist,
                                                      profile=int(label in ("zfp_dev", "zfp_host")),
                                                      m_resident=opt.get("m_resident", 0), tb=tb,
-                                                     precision=prec, serpentine=opt.get("serpentine", 0))
+                                                     precision=prec, serpentine=opt.get("serpentine", 0),
+                                                     slots=opt.get("slots", 2))
             sweeps_total = st["sweeps"]
             cells_mode = cells // T * tb
             out[label] = {"s": dev_s, "cups": cells_mode / dev_s, "launches": launches, "evs": evs,
@@ -430,6 +434,12 @@ def gpu_arm(args):
                          "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
                          "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
                          "e2e_host_link_GBps": round(hs["h2d_per_sweep"] / (hs["s"] / args.steps) / 1e9, 2)}
+        if "slots3_host" in out:
+            hs = out["slots3_host"]
+            orch["serpentine+m_resident, 3 staging slots"] = {
+                "e2e": round(hs["cups"], 1), "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
+                "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
+                "e2e_d2h_GBps": round(hs["d2h_per_sweep"] / (hs["s"] / args.steps) / 1e9, 2)}
     per_rate = {}
     for r in (8, 24):
         if f"r{r}_dev" in out:

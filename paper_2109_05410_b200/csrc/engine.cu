@@ -160,9 +160,10 @@ struct oocz_ctx {
     cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_decoded[2] = {nullptr, nullptr}, ev_slab_free[2] = {nullptr, nullptr};
     cudaEvent_t ev_halo = nullptr, ev_join_dec = nullptr;
-    std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written;
+    std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written, ev_encoded;
     long long seq = 0;                      // global block sequence number
     std::vector<int> last_slot;             // staging slot of each block's latest encode (host store)
+    std::vector<long long> last_seq;        // ... and its block sequence number (-1: not in a slot)
     // halo exchange (world > 1)
     HaloComm* halo = nullptr;
     // profiling
@@ -496,7 +497,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     CKC(mk(ctx->ev_out_ready, nslots));
     CKC(mk(ctx->ev_out_free, nslots));
     CKC(mk(ctx->ev_written, D));
+    CKC(mk(ctx->ev_encoded, D));
     ctx->last_slot.assign(D, 0);
+    ctx->last_seq.assign(D, -1);
     CKC(cudaEventCreate(&ctx->ev_t0));
     CKC(cudaEventCreate(&ctx->ev_t1));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_h2d, cudaEventDisableTiming));
@@ -580,7 +583,8 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     for (auto p : ctx->out_slot) cudaFree(p);
     cudaFree(ctx->d_flags);
     cudaFree(ctx->m_full);
-    for (auto* v : {&ctx->ev_in_ready, &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free, &ctx->ev_written})
+    for (auto* v : {&ctx->ev_in_ready, &ctx->ev_in_free, &ctx->ev_out_ready, &ctx->ev_out_free, &ctx->ev_written,
+                    &ctx->ev_encoded})
         for (auto e : *v) cudaEventDestroy(e);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (cudaEvent_t e : {ctx->ev_t0, ctx->ev_t1, ctx->ev_join_h2d, ctx->ev_join_comp})
@@ -636,6 +640,7 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_
     if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
     CK(cudaSetDevice(ctx->device));
     ctx->field_set[field] = false;
+    std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     cudaStream_t s = ctx->s_comp;
     const int chunk = ctx->P;                       // planes per pass, <= slab capacity
     const double mmax = ctx->esz == 8 ? cfl_limit(ctx->cfg.c64) : cfl_limit(ctx->cfg.c);
@@ -783,6 +788,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     cudaStream_t s = ctx->s_comp;
     ctx->field_set[field] = false;
+    std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     if (host) std::memcpy(ctx->store[field], src, bytes);
     else CK(cudaMemcpy(ctx->store[field], src, bytes, cudaMemcpyHostToDevice));
     if (field == OOCZ_M && ctx->m_full) {       // m_resident: decode the loaded stream once
@@ -812,16 +818,29 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
 }
 
 // ------------------------------------------------------------------ step
+// Is block j's latest encoded own rows still intact in its staging slot for a
+// decode enqueued now?  (Slot k is next overwritten by the encode of block
+// sequence number last_seq + nslots, which is enqueued after this decode.)
+static bool rows_in_slot(const oocz_ctx* ctx, int j)
+{
+    if (!ctx->cfg.serpentine) return false;                  // the paper-faithful schedule stays literal
+    const long long ls = ctx->last_seq[j];
+    return ls >= 0 && ctx->seq <= ls + (long long)ctx->out_slot.size();
+}
+
 // Enqueue one block of one sweep (ts steps).
 //   dir  : +1 ascending (the paper's order, R17), -1 descending (serpentine
 //          sweeps, reading R22);
 //   turn : serpentine turnaround -- block i was the last block of the previous
-//          sweep of this call, so its read unit is on the device already: u, u-
-//          are decoded from the compressed rows just encoded into the staging
-//          slots (or from the device store), and m is still decoded in its slab;
+//          sweep of this call: m is still decoded in its slab;
 //   keep : block i is the last block of a sweep that is followed by a
 //          turnaround in this call -- its compressed rows stay in the staging
-//          slot (no D2H; the store rows are rewritten next sweep).
+//          slot (no D2H; the turnaround reads them and the store rows are
+//          rewritten next sweep).
+// Host store: rows of the read unit that are still in a staging slot (encoded
+// by a recent block -- always the turnaround's, and with slots >= 3 the next
+// block's own rows too) are decoded from the device; only the rest crosses the
+// host link (region sharing carried across the sweep boundary, reading R22).
 static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int dir, bool turn, bool keep)
 {
     const Geom& g = ctx->geom[i];
@@ -842,92 +861,105 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const int rd0 = dir > 0 ? g.rd0 : std::max(i * P - h, 0);
     const int rd1 = dir > 0 ? g.rd1 : (i == D - 1 ? S : (i + 1) * P - h);
     const int rd_planes = rd1 - rd0;
-    const uint8_t* src[3];
     cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
     const int nb = dir > 0 ? std::min(i + 1, D - 1) : std::max(i - 1, 0);   // the read unit's other owner
 
-    if (turn) {
-        // ---- (a2/a3, turnaround) nothing crosses the host link
-        CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
-        CK(cudaStreamWaitEvent(sd, ctx->ev_written[i], 0));
-        CK(cudaStreamWaitEvent(sd, ctx->ev_written[nb], 0));
-        if (ctx->halo) {
-            std::string herr;
-            CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
-            if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
-                return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
-        }
-        for (int f = 0; f < 2; f++) {
-            // own rows [iP, (i+1)P), then the neighbour's h rows next to them
-            const uint8_t* own = host ? ctx->out_slot[ctx->last_slot[i]] + ctx->out_off[f]
-                                      : ctx->store[f] + rows_off(ctx, f, g.own0);
-            prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] +
-                                                                 (uint64_t)rd_planes * pb);
-            CK(decode_or_copy(ctx, f, own, P, slab[f] + (size_t)h * pb, sd));
-            if (nb != i) {
-                const int z0 = dir > 0 ? (i + 1) * P : i * P - h;     // rank plane of the neighbour rows
-                const uint8_t* nbr = host
-                    ? ctx->out_slot[ctx->last_slot[nb]] + ctx->out_off[f] + (dir > 0 ? 0 : (size_t)((P - h) / 4) * ctx->row_bytes[f])
-                    : ctx->store[f] + rows_off(ctx, f, z0);
-                CK(decode_or_copy(ctx, f, nbr, h, slab[f] + (size_t)(z0 - g.slab0) * pb, sd));
+    // ---- the read unit as (at most) two parts per field: the own rows and the
+    // neighbour block's rows; each from the device (store or staging slot) or
+    // from the host store through the staging slot `in`
+    struct Part { int z0, z1; const uint8_t* src; bool h2d; };
+    Part part[3][2];
+    int nparts[3] = {0, 0, 0};
+    const int own0 = std::max(rd0, g.own0), own1 = std::min(rd1, g.own1);
+    for (int f = 0; f < nf; f++) {
+        if (f == OOCZ_M && turn) continue;                    // still decoded in this slab
+        auto add = [&](int z0, int z1, int owner) {
+            if (z1 <= z0) return;
+            Part q{z0, z1, nullptr, false};
+            if (!host) {
+                q.src = ctx->store[f] + rows_off(ctx, f, z0);
+            } else if (f != OOCZ_M && rows_in_slot(ctx, owner)) {
+                q.src = ctx->out_slot[ctx->last_slot[owner]] + ctx->out_off[f] +
+                        (size_t)((z0 - owner * P) / 4) * ctx->row_bytes[f];
+            } else {
+                q.src = ctx->in_slot[slot] + ctx->in_off[f] + (size_t)((z0 - rd0) / 4) * ctx->row_bytes[f];
+                q.h2d = true;
             }
-            prof_end(ctx, sd);
-        }
-        if (host) CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[i]], sd));   // the kept slot is read
-    } else {
-        // ---- (a2) H2D of the read unit (u, u-, m) into a staging slot, once the
-        // previous sweep has written those rows back
-        if (host) {
-            cudaStream_t sh = ctx->s_h2d;
-            CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
-            CK(cudaStreamWaitEvent(sh, ctx->ev_written[i], 0));
-            CK(cudaStreamWaitEvent(sh, ctx->ev_written[nb], 0));
-            uint64_t bytes = 0;
-            for (int f = 0; f < nf; f++) bytes += (uint64_t)(rd_planes / 4) * ctx->row_bytes[f];
-            prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
-            for (int f = 0; f < nf; f++) {
-                const size_t nbytes = (size_t)(rd_planes / 4) * ctx->row_bytes[f];
-                CK(cudaMemcpyAsync(ctx->in_slot[slot] + ctx->in_off[f], ctx->store[f] + rows_off(ctx, f, rd0),
-                                   nbytes, cudaMemcpyHostToDevice, sh));
-                src[f] = ctx->in_slot[slot] + ctx->in_off[f];
-            }
-            prof_end(ctx, sh);
-            ctx->stats.h2d_bytes += bytes;
-            CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
-            CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
-        } else {
-            CK(cudaStreamWaitEvent(sd, ctx->ev_written[i], 0));
-            CK(cudaStreamWaitEvent(sd, ctx->ev_written[nb], 0));
-            for (int f = 0; f < 3; f++) src[f] = ctx->store[f] + rows_off(ctx, f, rd0);
-        }
-
-        // ---- (a4) slab assembly on the decode stream, once this slab set is free
-        CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
-        const bool has_c = dir > 0 ? i > 0 : i < D - 1;     // the shared region kept by the previous block
-        if (has_c) {
-            // ascending: C_{i-1} -> slab [0, 2h); descending: C_i -> slab [P, P+2h)
-            const size_t dst = dir > 0 ? 0 : (size_t)P * pb;
-            prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
-            for (int f = 0; f < nf; f++)
-                CK(cudaMemcpyAsync(slab[f] + dst, ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
-            prof_end(ctx, sd);
-        }
-        if (ctx->halo) {  // neighbour-rank halos received at the sweep start
-            std::string herr;
-            CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
-            if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
-                return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
-        }
-        // ---- (a3) decode the read unit into the slab
-        for (int f = 0; f < nf; f++) {
-            // algorithmic bytes: compressed (or raw) read unit in + decoded planes out
-            const uint64_t bytes = (uint64_t)(rd_planes / 4) * ctx->row_bytes[f] + (uint64_t)rd_planes * pb;
-            prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
-            CK(decode_or_copy(ctx, f, src[f], rd_planes, slab[f] + (size_t)(rd0 - g.slab0) * pb, sd));
-            prof_end(ctx, sd);
-        }
-        if (host) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
+            part[f][nparts[f]++] = q;
+        };
+        if (dir > 0) { add(own0, own1, i); add(own1, rd1, nb); }
+        else { add(rd0, own0, nb); add(own0, own1, i); }
     }
+
+    // ---- (a2) H2D of the parts not on the device, once the previous sweep has
+    // written those rows back
+    bool any_h2d = false;
+    for (int f = 0; f < nf; f++)
+        for (int k = 0; k < nparts[f]; k++) any_h2d |= part[f][k].h2d;
+    auto owner_of = [&](const Part& q) { return q.z0 >= g.own0 && q.z0 < g.own1 ? i : nb; };
+    if (any_h2d) {
+        cudaStream_t sh = ctx->s_h2d;
+        CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
+        for (int f = 0; f < nf; f++)
+            for (int k = 0; k < nparts[f]; k++)
+                if (part[f][k].h2d) CK(cudaStreamWaitEvent(sh, ctx->ev_written[owner_of(part[f][k])], 0));
+        uint64_t bytes = 0;
+        for (int f = 0; f < nf; f++)
+            for (int k = 0; k < nparts[f]; k++)
+                if (part[f][k].h2d) bytes += (uint64_t)((part[f][k].z1 - part[f][k].z0) / 4) * ctx->row_bytes[f];
+        prof_begin(ctx, sweep, i, OOCZ_ST_H2D, 0, sh, bytes);
+        for (int f = 0; f < nf; f++)
+            for (int k = 0; k < nparts[f]; k++) {
+                const Part& q = part[f][k];
+                if (!q.h2d) continue;
+                CK(cudaMemcpyAsync(const_cast<uint8_t*>(q.src), ctx->store[f] + rows_off(ctx, f, q.z0),
+                                   (size_t)((q.z1 - q.z0) / 4) * ctx->row_bytes[f], cudaMemcpyHostToDevice, sh));
+            }
+        prof_end(ctx, sh);
+        ctx->stats.h2d_bytes += bytes;
+        CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
+        CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
+    }
+    // rows read from the device: the encodes that wrote them must be done
+    for (int f = 0; f < nf; f++)
+        for (int k = 0; k < nparts[f]; k++)
+            if (!part[f][k].h2d) CK(cudaStreamWaitEvent(sd, ctx->ev_encoded[owner_of(part[f][k])], 0));
+
+    // ---- (a4) slab assembly on the decode stream, once this slab set is free
+    CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
+    const bool has_c = !turn && (dir > 0 ? i > 0 : i < D - 1);   // the shared region kept by the previous block
+    if (has_c) {
+        // ascending: C_{i-1} -> slab [0, 2h); descending: C_i -> slab [P, P+2h)
+        const size_t dst = dir > 0 ? 0 : (size_t)P * pb;
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
+        for (int f = 0; f < nf; f++)
+            CK(cudaMemcpyAsync(slab[f] + dst, ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
+        prof_end(ctx, sd);
+    }
+    if (ctx->halo) {  // neighbour-rank halos received at the sweep start
+        std::string herr;
+        CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
+        if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
+            return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
+    }
+    // ---- (a3) decode the read unit into the slab
+    for (int f = 0; f < nf; f++) {
+        if (!nparts[f]) continue;
+        // algorithmic bytes: compressed (or raw) read unit in + decoded planes out
+        uint64_t bytes = 0;
+        for (int k = 0; k < nparts[f]; k++)
+            bytes += (uint64_t)((part[f][k].z1 - part[f][k].z0) / 4) * ctx->row_bytes[f] +
+                     (uint64_t)(part[f][k].z1 - part[f][k].z0) * pb;
+        prof_begin(ctx, sweep, i, OOCZ_ST_DECODE, 4, sd, bytes);
+        for (int k = 0; k < nparts[f]; k++) {
+            const Part& q = part[f][k];
+            CK(decode_or_copy(ctx, f, q.src, q.z1 - q.z0, slab[f] + (size_t)(q.z0 - g.slab0) * pb, sd));
+        }
+        prof_end(ctx, sd);
+    }
+    (void)rd_planes;
+    if (any_h2d) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
+    if (host && turn) CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[i]], sd));   // the kept slot is read
     // keep the time-t shared region for the next block (reading R14):
     // ascending C_i = slab [P, P+2h), descending C_{i-1} = slab [0, 2h)
     if (dir > 0 ? i < D - 1 : i > 0) {
@@ -969,6 +1001,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         }
         CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
         ctx->last_slot[i] = slot;
+        ctx->last_seq[i] = ctx->seq;
+        CK(cudaEventRecord(ctx->ev_encoded[i], sc));
         if (keep) {
             // rows stay in the slot for the turnaround; its decode frees the slot
             CK(cudaEventRecord(ctx->ev_written[i], sc));
@@ -996,6 +1030,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         }
         CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
         CK(cudaEventRecord(ctx->ev_written[i], sc));
+        CK(cudaEventRecord(ctx->ev_encoded[i], sc));
     }
     ctx->seq++;
     return OOCZ_OK;

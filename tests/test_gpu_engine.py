@@ -207,13 +207,55 @@ def test_m_resident_partitioned_group(world):
     assert np.array_equal(bits(gu), bits(ou))
 
 
+def _serpentine_bytes(D, P, h, T, calls, slots, nf, row):
+    """Host-link bytes of serpentine sweeps, modelled from the rule (DESIGN.md
+    R22): a read-unit part is decoded from a staging slot when the block that
+    encoded it is at most `slots` blocks back in the sequence; the kept block
+    at each turn skips its D2H; m rows (nf == 3) always cross, except at a turn."""
+    S = D * P
+    h2d = d2h = 0
+    seq, last = 0, [-1] * D
+    for n in calls:
+        k = -(-n // T)
+        for s_ in range(k):
+            asc = s_ % 2 == 0
+            for kk in range(D):
+                i = kk if asc else D - 1 - kk
+                turn = s_ > 0 and kk == 0
+                keep = s_ < k - 1 and kk == D - 1
+                if asc:
+                    rd0, rd1 = (0 if i == 0 else i * P + h), min((i + 1) * P + h, S)
+                    nb = min(i + 1, D - 1)
+                    parts = [(rd0, min(rd1, (i + 1) * P), i), ((i + 1) * P, rd1, nb)]
+                else:
+                    rd0, rd1 = max(i * P - h, 0), (S if i == D - 1 else (i + 1) * P - h)
+                    nb = max(i - 1, 0)
+                    parts = [(rd0, i * P, nb), (max(rd0, i * P), rd1, i)]
+                for z0, z1, owner in parts:
+                    if z1 <= z0:
+                        continue
+                    on_dev = last[owner] >= 0 and seq <= last[owner] + slots
+                    for f in range(nf):
+                        if f == 2:
+                            h2d += 0 if turn else (z1 - z0) // 4 * row[2]
+                        elif not on_dev:
+                            h2d += (z1 - z0) // 4 * row[f]
+                last[i] = seq
+                if not keep:
+                    d2h += (P // 4) * (row[0] + row[1])
+                seq += 1
+        last = [x if x >= 0 else -1 for x in last]
+    return h2d, d2h
+
+
 @pytest.mark.parametrize("m_resident", [0, 1])
 @pytest.mark.parametrize("slots", [2, 3])
 @pytest.mark.parametrize("D,calls", [(4, [12]), (3, [5, 7]), (1, [9]), (2, [4, 4, 1])])
 def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident):
-    """Serpentine sweeps (R22): same bits as the oracle, and the block at
-    each turn never crosses the host link: per call of k sweeps, (k - 1) read units
-    and (k - 1) write units fewer than ascending sweeps."""
+    """Serpentine sweeps (R22): same bits as the oracle, and exactly the
+    host-link bytes of the schedule's model: the block at each turn never crosses
+    the link, and with slots >= 3 the rows of recent blocks are decoded from the
+    staging slots instead of crossing twice."""
     nx, ny, T, P, rates = 32, 24, 2, 16, (16, 12, 8)
     nz = D * P
     u, up, m = _fields(nx, ny, nz, 11)
@@ -223,23 +265,7 @@ def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident):
     assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
     row = [oracle.zfp_bytes(nx, ny, 4, r) for r in rates]
     nf = 2 if m_resident else 3
-    h = 4 * T
-    h2d = d2h = 0
-    for n in calls:
-        k = -(-n // T)                                 # sweeps in this call
-        field_rows = nz // 4
-        for s_ in range(k):
-            turn_block = None if s_ == 0 else (D - 1 if s_ % 2 else 0)
-            for i in range(D):
-                if i == turn_block:
-                    continue
-                if s_ % 2 == 0:                        # ascending read unit
-                    rd0, rd1 = (0 if i == 0 else i * P + h), min((i + 1) * P + h, nz)
-                else:                                  # descending
-                    rd0, rd1 = max(i * P - h, 0), (nz if i == D - 1 else (i + 1) * P - h)
-                h2d += (rd1 - rd0) // 4 * sum(row[:nf])
-            kept = 1 if s_ < k - 1 else 0
-            d2h += (D - kept) * (P // 4) * (row[0] + row[1])
+    h2d, d2h = _serpentine_bytes(D, P, 4 * T, T, calls, slots, nf, row)
     assert st["h2d_bytes"] == h2d
     assert st["d2h_bytes"] == d2h
     _audit(evs)
