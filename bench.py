@@ -297,9 +297,19 @@ def roofline(evs, peak_gbs, peak_src):
     table = {k: {"ms": round(v[0], 4), "launches": v[2], "GB/s": round(v[1] / (v[0] / 1e3) / 1e9, 1)}
              for k, v in per.items()}
     kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
+    traffic, tsrc = None, None
+    try:   # DRAM bytes per launch from a committed ncu capture of the same in-step launches
+        with open(os.path.join(ROOT, "profiles", "r01_stencil_instep_traffic.json")) as fh:
+            tj = json.load(fh)
+        if dom == "stencil":
+            traffic = int(tj["traffic_over_algorithmic"] * nbytes / n)
+            tsrc = ("profiles/r01_stencil_instep_traffic.json: ncu dram read+write / algorithmic = "
+                    f"{tj['traffic_over_algorithmic']} on the same launches, x this run's algorithmic bytes per launch")
+    except Exception:
+        pass
     return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": peak_gbs,
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
-            "traffic": None, "avg_launch_ms": round(ms / n, 4),
+            "traffic": traffic, "traffic_source": tsrc, "avg_launch_ms": round(ms / n, 4),
             "algorithmic_bytes_per_launch": int(nbytes / n)}, table
 
 
