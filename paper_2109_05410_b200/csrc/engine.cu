@@ -34,6 +34,7 @@
 #include <cstdarg>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -473,8 +474,17 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     }
     ctx->stats.device_bytes_used = need;
     CKC(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
-    CKC(cudaStreamCreateWithFlags(&ctx->s_comp, cudaStreamNonBlocking));
-    CKC(cudaStreamCreateWithFlags(&ctx->s_dec, cudaStreamNonBlocking));
+    {
+        // Equal priorities.  Giving the compute stream (stencil, encode) the higher
+        // priority ran the in-step stencil at 5.2 instead of 4.3 TB/s but slowed the
+        // decodes more: 121 vs 124.5 G cell-updates/s over the sweep (A/B, tools/ab_prio.sh).
+        // OOCZ_STREAM_PRIORITY=1 turns it on for experiments.
+        int lo = 0, hi = 0;
+        const char* sp = getenv("OOCZ_STREAM_PRIORITY");
+        if (sp && sp[0] == '1') CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        CKC(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, hi));
+        CKC(cudaStreamCreateWithPriority(&ctx->s_dec, cudaStreamNonBlocking, lo));
+    }
     for (int k = 0; k < 2; k++) {
         CKC(cudaEventCreateWithFlags(&ctx->ev_decoded[k], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&ctx->ev_slab_free[k], cudaEventDisableTiming));
