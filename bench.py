@@ -109,12 +109,12 @@ def make_fields(rank: int, S: int):
 
 
 def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
-             tb=T, precision=32, serpentine=0, slots=2):
+             tb=T, precision=32, serpentine=0, slots=2, slab_sets=0):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=slots, profile=profile)
+                                slots=slots, profile=profile, slab_sets=slab_sets)
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
@@ -184,7 +184,7 @@ def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
 
 def lanes_summary(evs) -> dict:
     """Per-lane busy time over the profiled step (SPEC.md:352 'per-lane idle')."""
-    names = {0: "h2d", 1: "compute", 2: "d2h", 3: "comm", 4: "decode"}
+    names = {0: "h2d", 1: "compute", 2: "d2h", 3: "comm", 4: "decode", 5: "encode"}
     if not evs:
         return {}
     t0 = min(e["start_ms"] for e in evs)
@@ -337,7 +337,7 @@ def gpu_arm(args):
         # orchestration of the SAME computation (bit-identical results, tests):
         # serpentine sweeps + m resident in HBM (readings R22/R23);
         # "pf_*" are the paper-faithful schedule (ascending sweeps, m streamed).
-        O = dict(serpentine=1, m_resident=1)
+        O = dict(serpentine=1, m_resident=1, slots=3)
         PF = dict(serpentine=0, m_resident=0)
         modes = [("zfp_dev", 1, (RATE,) * 3, O), ("zfp_host", 0, (RATE,) * 3, O),
                  ("raw_dev", 1, (0, 0, 0), O), ("raw_host", 0, (0, 0, 0), O)]
@@ -378,7 +378,8 @@ def gpu_arm(args):
                                                      profile=int(label in ("zfp_dev", "zfp_host")),
                                                      m_resident=opt.get("m_resident", 0), tb=tb,
                                                      precision=prec, serpentine=opt.get("serpentine", 0),
-                                                     slots=opt.get("slots", 2))
+                                                     slots=opt.get("slots", 2),
+                                                     slab_sets=opt.get("slab_sets", 0))
             sweeps_total = st["sweeps"]
             cells_mode = cells // T * tb
             out[label] = {"s": dev_s, "cups": cells_mode / dev_s, "launches": launches, "evs": evs,

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OOCZ_ABI_VERSION 2
+#define OOCZ_ABI_VERSION 3
 
 typedef enum {
     OOCZ_OK = 0,
@@ -79,6 +79,10 @@ typedef struct {
                               device: its compressed rows never cross the host link in between
                               (1/D of the traffic per sweep saved).  Orchestration beyond the
                               paper (R22).  Results identical.  */
+    int32_t  slab_sets;    /* device slab sets the blocks rotate through: 0 (= 2), 2, 3 or 4.
+                              Each set is (P + 8T) planes per streamed field.  With more sets
+                              block i+1 decodes and block i-1 encodes while block i runs its
+                              stencil (the encode has its own stream).  Results identical. */
 } oocz_config;
 
 typedef struct {
@@ -105,7 +109,8 @@ enum { OOCZ_ST_H2D = 0, OOCZ_ST_DECODE = 1, OOCZ_ST_STENCIL = 2, OOCZ_ST_ENCODE 
  * "Roofline"): stencil 16 B per updated cell; decode/encode the compressed bytes
  * plus 4 B per value; copies and transfers the bytes moved. */
 typedef struct {
-    int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute, 2 = d2h, 3 = comm, 4 = decode */
+    int32_t  sweep, block, stage, lane;   /* lane: 0 = h2d, 1 = compute (stencil), 2 = d2h, 3 = comm,
+                                             4 = decode, 5 = encode */
     double   start_ms, end_ms;
     uint64_t bytes;
 } oocz_event;

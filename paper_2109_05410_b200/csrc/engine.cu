@@ -16,12 +16,13 @@
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
-//    compute (stencil + encode), d2h.  Blocks alternate between two slab sets,
-//    so the decode of block i+1 (integer-ALU bound) runs while block i's
-//    stencil (HBM bound) does.
+//    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
+//    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
+//    bound) run while block i's stencil (HBM bound) does.
 //
 // Device-side data layout (per rank):
-//   slab[s][f]: two sets (blocks alternate) of (P + 2h) planes of nx*ny fp32,
+//   slab[s][f]: `slab_sets` sets (blocks rotate through them; default 2) of
+//               (P + 2h) planes of nx*ny fp32,
 //               slab plane 0 = rank plane iP - h
 //   ccopy[f]  : 2h planes, time-t copy of C_i (u, u-, m)
 //   in[slot]  : H2D staging of one read unit (3 fields), `slots` deep
@@ -147,7 +148,9 @@ struct oocz_ctx {
     std::vector<Geom> geom;
     // device buffers
     // (byte pointers: fp32 or fp64 planes of pb bytes)
-    uint8_t* slab[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+    static constexpr int kMaxSets = 4;
+    int nsets = 2;                          // slab sets in rotation (cfg.slab_sets, default 2)
+    uint8_t* slab[kMaxSets][3] = {};
     uint8_t* ccopy[3] = {nullptr, nullptr, nullptr};
     uint8_t* m_full = nullptr;              // m_resident: decoded m, planes [-h, S + h)
     std::vector<uint8_t*> in_slot, out_slot;
@@ -158,8 +161,9 @@ struct oocz_ctx {
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
     size_t store_bytes[3] = {0, 0, 0};
     // streams / events
-    cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_d2h = nullptr;
-    cudaEvent_t ev_decoded[2] = {nullptr, nullptr}, ev_slab_free[2] = {nullptr, nullptr};
+    cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_enc = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_decoded[kMaxSets] = {}, ev_slab_free[kMaxSets] = {}, ev_stepped[kMaxSets] = {};
+    cudaEvent_t ev_join_enc = nullptr;
     cudaEvent_t ev_halo = nullptr, ev_join_dec = nullptr;
     std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written, ev_encoded;
     long long seq = 0;                      // global block sequence number
@@ -347,6 +351,8 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->store != OOCZ_STORE_HOST && cfg->store != OOCZ_STORE_DEVICE)
         BAD(OOCZ_EINVAL, "store (%d) unknown", cfg->store);
     if (cfg->store == OOCZ_STORE_HOST && cfg->slots < 2) BAD(OOCZ_EINVAL, "slots (%d) < 2", cfg->slots);
+    if (cfg->slab_sets != 0 && (cfg->slab_sets < 2 || cfg->slab_sets > 4))
+        BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 2, 3, 4}", cfg->slab_sets);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
@@ -384,6 +390,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     ctx->D = ctx->S / ctx->P;
     ctx->L = ctx->P + 2 * ctx->h;
     ctx->plane_elems = (size_t)cfg->nx * cfg->ny;
+    ctx->nsets = cfg->slab_sets ? cfg->slab_sets : 2;
     ctx->esz = esz_of(cfg);
     ctx->pb = ctx->plane_elems * ctx->esz;
     for (int f = 0; f < 3; f++) ctx->row_bytes[f] = row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], ctx->esz);
@@ -417,7 +424,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     }
     // memory plan and budget check
     const size_t pb = ctx->pb;
-    size_t need = 2 * 3 * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
+    // slab sets (m is not streamed into them when it is resident) + the C_i copy
+    const int slab_fields = cfg->m_resident ? 2 : 3;
+    size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
     if (host) {
@@ -445,7 +454,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         }
     }
     for (int f = 0; f < 3; f++) {
-        for (int k = 0; k < 2; k++) {
+        for (int k = 0; k < ctx->nsets && f < slab_fields; k++) {
             CKC(cudaMalloc(&ctx->slab[k][f], (size_t)ctx->L * pb));
             CKC(cudaMemset(ctx->slab[k][f], 0, (size_t)ctx->L * pb));
         }
@@ -484,11 +493,14 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         if (sp && sp[0] == '1') CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_dec, cudaStreamNonBlocking, lo));
+        CKC(cudaStreamCreateWithPriority(&ctx->s_enc, cudaStreamNonBlocking, lo));
     }
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < ctx->nsets; k++) {
         CKC(cudaEventCreateWithFlags(&ctx->ev_decoded[k], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&ctx->ev_slab_free[k], cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&ctx->ev_stepped[k], cudaEventDisableTiming));
     }
+    CKC(cudaEventCreateWithFlags(&ctx->ev_join_enc, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_dec, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
@@ -579,12 +591,12 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     cudaSetDevice(ctx->device);
     if (ctx->s_h2d) cudaStreamSynchronize(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamSynchronize(ctx->s_comp);
+    if (ctx->s_enc) cudaStreamSynchronize(ctx->s_enc);
     if (ctx->s_dec) cudaStreamSynchronize(ctx->s_dec);
     if (ctx->s_d2h) cudaStreamSynchronize(ctx->s_d2h);
     if (ctx->halo) halo_destroy(ctx->halo);
     for (int f = 0; f < 3; f++) {
-        cudaFree(ctx->slab[0][f]);
-        cudaFree(ctx->slab[1][f]);
+        for (int k = 0; k < oocz_ctx::kMaxSets; k++) cudaFree(ctx->slab[k][f]);
         cudaFree(ctx->ccopy[f]);
         if (ctx->cfg.store == OOCZ_STORE_HOST) cudaFreeHost(ctx->store[f]);
         else cudaFree(ctx->store[f]);
@@ -601,10 +613,13 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         if (e) cudaEventDestroy(e);
     if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
+    if (ctx->s_enc) cudaStreamDestroy(ctx->s_enc);
+    if (ctx->ev_join_enc) cudaEventDestroy(ctx->ev_join_enc);
     if (ctx->s_dec) cudaStreamDestroy(ctx->s_dec);
-    for (int k = 0; k < 2; k++) {
+    for (int k = 0; k < oocz_ctx::kMaxSets; k++) {
         if (ctx->ev_decoded[k]) cudaEventDestroy(ctx->ev_decoded[k]);
         if (ctx->ev_slab_free[k]) cudaEventDestroy(ctx->ev_slab_free[k]);
+        if (ctx->ev_stepped[k]) cudaEventDestroy(ctx->ev_stepped[k]);
     }
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->ev_join_dec) cudaEventDestroy(ctx->ev_join_dec);
@@ -660,7 +675,7 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_
     for (int z = 0; z < ctx->S; z += chunk) {
         const int np = std::min(chunk, ctx->S - z);
         const size_t n = (size_t)np * ctx->plane_elems;
-        uint8_t* buf = ctx->slab[0][field];
+        uint8_t* buf = ctx->slab[0][0];              // scratch between steps
         CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->pb, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         if (ctx->esz == 8)
@@ -743,7 +758,7 @@ static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, void* dst_v, siz
         const int np = std::min(chunk, ctx->S - z);
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
-        uint8_t* buf = ctx->slab[0][field];
+        uint8_t* buf = ctx->slab[0][0];              // scratch between steps
         if (host) {
             uint8_t* dev = ctx->in_slot[0];
             CK(cudaMemcpyAsync(dev, ctx->store[field] + off, bytes, cudaMemcpyHostToDevice, s));
@@ -859,9 +874,9 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
-    // slab set: blocks alternate between two; with serpentine sweeps by block
-    // parity, so a turnaround block finds its own slab (and its decoded m) again
-    const int set = ctx->cfg.serpentine ? (i & 1) : (int)(ctx->seq % 2);
+    // slab set: blocks rotate through nsets; with serpentine sweeps by block
+    // index, so a turnaround block finds its own slab (and its decoded m) again
+    const int set = ctx->cfg.serpentine ? i % ctx->nsets : (int)(ctx->seq % ctx->nsets);
     // m_resident: m is read in place from the decoded copy, never streamed
     const int nf = ctx->m_full ? 2 : 3;
     uint8_t* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
@@ -871,7 +886,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const int rd0 = dir > 0 ? g.rd0 : std::max(i * P - h, 0);
     const int rd1 = dir > 0 ? g.rd1 : (i == D - 1 ? S : (i + 1) * P - h);
     const int rd_planes = rd1 - rd0;
-    cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp;
+    cudaStream_t sd = ctx->s_dec, sc = ctx->s_comp, se = ctx->s_enc;
     const int nb = dir > 0 ? std::min(i + 1, D - 1) : std::max(i - 1, 0);   // the read unit's other owner
 
     // ---- the read unit as (at most) two parts per field: the own rows and the
@@ -995,29 +1010,32 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         std::swap(cu, cp);
     }
 
-    // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-
+    // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-, on
+    // the encode stream: the next block's stencil need not wait for it
+    CK(cudaEventRecord(ctx->ev_stepped[set], sc));
+    CK(cudaStreamWaitEvent(se, ctx->ev_stepped[set], 0));
     const uint8_t* own[2] = {cu + (size_t)h * pb, cp + (size_t)h * pb};
     if (ctx->halo) {
         std::string herr;
-        if (!halo_capture(ctx->halo, i == 0, i == D - 1, own, P, ctx->nx, ctx->ny, sc, &herr))
+        if (!halo_capture(ctx->halo, i == 0, i == D - 1, own, P, ctx->nx, ctx->ny, se, &herr))
             return fail(ctx, OOCZ_ENCCL, "halo capture: %s", herr.c_str());
     }
     if (host) {
-        CK(cudaStreamWaitEvent(sc, ctx->ev_out_free[slot], 0));
+        CK(cudaStreamWaitEvent(se, ctx->ev_out_free[slot], 0));
         for (int f = 0; f < 2; f++) {
-            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
-            CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], sc));
-            prof_end(ctx, sc);
+            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 5, se, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
+            CK(encode_or_copy(ctx, f, own[f], P, ctx->out_slot[slot] + ctx->out_off[f], se));
+            prof_end(ctx, se);
         }
-        CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
+        CK(cudaEventRecord(ctx->ev_slab_free[set], se));
         ctx->last_slot[i] = slot;
         ctx->last_seq[i] = ctx->seq;
-        CK(cudaEventRecord(ctx->ev_encoded[i], sc));
+        CK(cudaEventRecord(ctx->ev_encoded[i], se));
         if (keep) {
             // rows stay in the slot for the turnaround; its decode frees the slot
-            CK(cudaEventRecord(ctx->ev_written[i], sc));
+            CK(cudaEventRecord(ctx->ev_written[i], se));
         } else {
-            CK(cudaEventRecord(ctx->ev_out_ready[slot], sc));
+            CK(cudaEventRecord(ctx->ev_out_ready[slot], se));
             // ---- (a7) D2H into the store, in place
             cudaStream_t so = ctx->s_d2h;
             CK(cudaStreamWaitEvent(so, ctx->ev_out_ready[slot], 0));
@@ -1034,13 +1052,13 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         }
     } else {
         for (int f = 0; f < 2; f++) {
-            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 1, sc, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
-            CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), sc));
-            prof_end(ctx, sc);
+            prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 5, se, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
+            CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), se));
+            prof_end(ctx, se);
         }
-        CK(cudaEventRecord(ctx->ev_slab_free[set], sc));
-        CK(cudaEventRecord(ctx->ev_written[i], sc));
-        CK(cudaEventRecord(ctx->ev_encoded[i], sc));
+        CK(cudaEventRecord(ctx->ev_slab_free[set], se));
+        CK(cudaEventRecord(ctx->ev_written[i], se));
+        CK(cudaEventRecord(ctx->ev_encoded[i], se));
     }
     ctx->seq++;
     return OOCZ_OK;
@@ -1061,6 +1079,7 @@ static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
     *base = ctx->ev_t0;
     CK(cudaEventRecord(ctx->ev_t0, ctx->s_h2d));
     CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_t0, 0));
+    CK(cudaStreamWaitEvent(ctx->s_enc, ctx->ev_t0, 0));
     CK(cudaStreamWaitEvent(ctx->s_dec, ctx->ev_t0, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_t0, 0));
     return OOCZ_OK;
@@ -1069,9 +1088,11 @@ static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
 static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
 {
     CK(cudaSetDevice(ctx->device));
-    // join the three streams into s_d2h and stamp t1 there
+    // join the other streams into s_d2h and stamp t1 there
     CK(cudaEventRecord(ctx->ev_join_h2d, ctx->s_h2d));
     CK(cudaEventRecord(ctx->ev_join_comp, ctx->s_comp));
+    CK(cudaEventRecord(ctx->ev_join_enc, ctx->s_enc));
+    CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_enc, 0));
     CK(cudaEventRecord(ctx->ev_join_dec, ctx->s_dec));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_dec, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_h2d, 0));
@@ -1079,6 +1100,7 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
     CK(cudaEventRecord(ctx->ev_t1, ctx->s_d2h));
     CK(cudaStreamSynchronize(ctx->s_h2d));
     CK(cudaStreamSynchronize(ctx->s_comp));
+    CK(cudaStreamSynchronize(ctx->s_enc));
     CK(cudaStreamSynchronize(ctx->s_dec));
     CK(cudaStreamSynchronize(ctx->s_d2h));
     {
@@ -1132,6 +1154,9 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
             if (ctx->halo) {
                 std::string herr;
                 CK(cudaSetDevice(ctx->device));
+                // the previous sweep's halo captures ran on the encode stream
+                CK(cudaEventRecord(ctx->ev_join_enc, ctx->s_enc));
+                CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_join_enc, 0));
                 if (!halo_sweep_begin(ctx->halo, ctx->s_comp, &herr))
                     return fail(ctx, OOCZ_ENCCL, "halo exchange: %s", herr.c_str());
                 CK(cudaEventRecord(ctx->ev_halo, ctx->s_comp));   // the decode stream inserts them

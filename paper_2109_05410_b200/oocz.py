@@ -35,7 +35,8 @@ class oocz_config(C.Structure):
                 ("c", C.c_float * 5), ("tb", C.c_int32), ("block_planes", C.c_int32),
                 ("rate", C.c_int32 * 3), ("store", C.c_int32), ("slots", C.c_int32),
                 ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32),
-                ("precision", C.c_int32), ("c64", C.c_double * 5), ("serpentine", C.c_int32)]
+                ("precision", C.c_int32), ("c64", C.c_double * 5), ("serpentine", C.c_int32),
+                ("slab_sets", C.c_int32)]
 
 
 class oocz_stats(C.Structure):
@@ -101,6 +102,10 @@ for _name, (_res, _args) in _SIGS.items():
     _fn.restype = _res
     _fn.argtypes = _args
 
+ABI_VERSION = 3          # the oocz_config layout this binding marshals (include/oocz.h)
+if _lib.oocz_abi_version() != ABI_VERSION:
+    raise ImportError(f"{LIB_PATH} has ABI {_lib.oocz_abi_version()}, the binding expects {ABI_VERSION}: rebuild")
+
 
 def header_functions() -> list[str]:
     """Every function include/oocz.h declares (for the export test)."""
@@ -158,6 +163,9 @@ def oocz_abi_version() -> int:
     return _lib.oocz_abi_version()
 
 
+_CFG_FIELDS = {k for k, _ in oocz_config._fields_}
+
+
 def oocz_default_config(nx: int, ny: int, nz: int, **kw) -> oocz_config:
     cfg = oocz_config()
     _lib.oocz_default_config(C.byref(cfg), nx, ny, nz)
@@ -169,8 +177,10 @@ def oocz_default_config(nx: int, ny: int, nz: int, **kw) -> oocz_config:
             cfg.c = _c5(v)
         elif k == "c64":
             cfg.c64 = _c5d(v)
-        else:
+        elif k in _CFG_FIELDS:
             setattr(cfg, k, v)
+        else:
+            raise TypeError(f"oocz_config has no field {k!r}")
     return cfg
 
 

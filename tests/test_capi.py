@@ -24,7 +24,7 @@ def test_every_header_symbol_is_exported(z):
 
 
 def test_abi_version(z):
-    assert z.oocz_abi_version() == 2
+    assert z.oocz_abi_version() == z.ABI_VERSION == 3
 
 
 def test_zfp_bytes_closed_form(z):
@@ -51,6 +51,9 @@ def test_cfl_limit_default_coefficients(z):
     (dict(store=7), 1, -1, "store"),
     (dict(precision=16), 1, -1, "precision (16)"),
     (dict(precision=64, block_planes=32), 1, 0, ""),
+    (dict(slab_sets=3, block_planes=32), 1, 0, ""),
+    (dict(slab_sets=5, block_planes=32), 1, -1, "slab_sets (5)"),
+    (dict(slab_sets=1, block_planes=32), 1, -1, "slab_sets (1)"),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)

@@ -21,11 +21,12 @@ def _fields(nx, ny, nz, seed, kind="dense"):
     return u, up, synth.layered(nx, ny, nz)
 
 
-def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0):
+def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0, slab_sets=0):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
-                                slots=slots, profile=profile, serpentine=serpentine, m_resident=m_resident)
+                                slots=slots, profile=profile, serpentine=serpentine, m_resident=m_resident,
+                                slab_sets=slab_sets)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -53,12 +54,13 @@ CASES = [
 ]
 
 
+@pytest.mark.parametrize("slab_sets", [2, 3])
 @pytest.mark.parametrize("serpentine", [0, 1])
 @pytest.mark.parametrize("store", [0, 1])
 @pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES)
-def test_stepper_matches_oracle(store, serpentine, nx, ny, nz, T, P, rates, calls):
+def test_stepper_matches_oracle(store, serpentine, slab_sets, nx, ny, nz, T, P, rates, calls):
     u, up, m = _fields(nx, ny, nz, 3)
-    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, store, calls, serpentine=serpentine)
+    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, store, calls, serpentine=serpentine, slab_sets=slab_sets)
     ou, oup = _run_oracle(u, up, m, T, rates, calls)
     assert np.array_equal(bits(gu), bits(ou))
     assert np.array_equal(bits(gup), bits(oup))
@@ -100,14 +102,15 @@ def _audit(evs):
         assert starts == sorted(starts), key
 
 
+@pytest.mark.parametrize("slab_sets", [2, 3])
 @pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("rates", [(16, 16, 16), (0, 0, 0), (8, 24, 12)])
-def test_partitioned_group_bit_identical_to_single(world, rates):
+def test_partitioned_group_bit_identical_to_single(world, rates, slab_sets):
     """z-partitioned run (halos exchanged in compressed form) == world 1 == oracle."""
     z = Z()
     nx, ny, nz, T, P = 32, 24, 128, 2, 16
     u, up, m = _fields(nx, ny, nz, 5)
-    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0, slab_sets=slab_sets)
     ctxs = z.oocz_create_local_group(cfg, world)
     S = nz // world
     try:
@@ -248,10 +251,11 @@ def _serpentine_bytes(D, P, h, T, calls, slots, nf, row):
     return h2d, d2h
 
 
+@pytest.mark.parametrize("slab_sets", [2, 3, 4])
 @pytest.mark.parametrize("m_resident", [0, 1])
 @pytest.mark.parametrize("slots", [2, 3])
 @pytest.mark.parametrize("D,calls", [(4, [12]), (3, [5, 7]), (1, [9]), (2, [4, 4, 1])])
-def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident):
+def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident, slab_sets):
     """Serpentine sweeps (R22): same bits as the oracle, and exactly the
     host-link bytes of the schedule's model: the block at each turn never crosses
     the link, and with slots >= 3 the rows of recent blocks are decoded from the
@@ -260,7 +264,7 @@ def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident):
     nz = D * P
     u, up, m = _fields(nx, ny, nz, 11)
     gu, gup, st, evs = _run_gpu(u, up, m, T, P, rates, 0, calls, slots=slots, profile=1, serpentine=1,
-                                m_resident=m_resident)
+                                m_resident=m_resident, slab_sets=slab_sets)
     ou, oup = _run_oracle(u, up, m, T, rates, calls)
     assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
     row = [oracle.zfp_bytes(nx, ny, 4, r) for r in rates]
