@@ -24,6 +24,20 @@ constexpr int kNumSMs = 148;  // B200
 
 inline const char* cuda_str(cudaError_t e) { return cudaGetErrorString(e); }
 
+#ifndef OOCZ_CARVEOUT
+#define OOCZ_CARVEOUT 1
+#endif
+// Once per kernel: allow `dyn_bytes` of dynamic shared memory, and (unless
+// built with OOCZ_CARVEOUT=0) ask for the largest shared-memory carveout, so
+// an SM configured for one of the pipeline's kernels can take another's CTA.
+inline cudaError_t kernel_smem_setup(const void* fn, int dyn_bytes)
+{
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
+    if (e == cudaSuccess && OOCZ_CARVEOUT)
+        e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    return e;
+}
+
 // internal launchers (stream-ordered, no synchronisation)
 cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
                               uint64_t* out, cudaStream_t s);

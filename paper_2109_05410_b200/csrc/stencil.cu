@@ -7,15 +7,18 @@
 // it updates planes [z0, z1) of a z-slab in place (u+ overwrites u-).
 //
 // Design (HBM-bound: >= 16 B per cell-update: read u, u-, m, write u+):
-//  * CTA tile 128 (x) x 16 (y) cells marched along z; warp-specialised:
-//    warp 0 is a TMA producer (one elected lane), warps 1..16 compute one row
-//    each, 4 consecutive x per thread.
+//  * CTA tile 128 (x) x 15 (y) cells marched along z; warp-specialised:
+//    warp 0 is a TMA producer (one elected lane), warps 1..15 compute one row
+//    each, 4 consecutive x per thread.  16 warps of <= 96 registers: each SM
+//    sub-partition keeps room for one codec warp of the concurrent decode /
+//    encode streams, and a 512^2 plane is 140 tiles (<= 148 SMs).
 //  * Producer: cp.async.bulk.tensor.3d loads of
-//      - the u plane tile with its radius-4 x/y halo (136 x 24 floats) into an
+//      - the u plane tile with its radius-4 x/y halo (136 x 23 floats) into an
 //        8-stage ring; TMA out-of-bounds fill gives the zero Dirichlet ghost in
 //        x, y and z (the tensor map covers only the planes [zv0, zv1) that hold
 //        data);
-//      - the u- and m tiles (128 x 16 each) into a 4-stage ring.
+//      - the u- and m tiles (128 x 15 each) into a 4-stage ring (161 KiB of
+//        shared memory in all, so a codec CTA fits next to it).
 //    full/empty mbarrier pairs per stage: consumers release a stage as soon as
 //    every consumer warp is done with it (no CTA-wide barrier per plane), so
 //    the producer stays 3 u planes / 3 u-,m planes ahead.
@@ -39,10 +42,10 @@ namespace oocz {
 namespace {
 
 #ifndef OOCZ_STENCIL_NU
-#define OOCZ_STENCIL_NU 10
+#define OOCZ_STENCIL_NU 8
 #endif
 #ifndef OOCZ_STENCIL_NR
-#define OOCZ_STENCIL_NR 5
+#define OOCZ_STENCIL_NR 4
 #endif
 #ifndef OOCZ_STENCIL_CTAS
 #define OOCZ_STENCIL_CTAS 148
@@ -50,12 +53,24 @@ namespace {
 constexpr int kStencilCTAs = OOCZ_STENCIL_CTAS;  // persistent CTAs (one per SM at most)
 constexpr int TX = 128;                           // 32 lanes x 4 consecutive x
 
-// Tile shape per element type.  fp32: 128 x 16 cells, 16 consumer warps, ring
-// depths NU / NR.  fp64 (the paper's precision): 128 x 8 cells,
+// Tile shape per element type.  fp32: 128 x 15 cells, 15 consumer warps, ring
+// depths NU / NR (measured on one C2 slab: 128 x 16 with rings 10 / 5, 17 warps,
+// 111 us; 128 x 15 with rings 8 / 4, 16 warps, 106.5 us).  fp64 (the paper's precision): 128 x 8 cells,
 // 8 consumer warps (the register queue is twice as wide; 288 threads leave
 // 224 registers per thread), u ring 8, u-/m ring 4: 203 KiB of shared memory.
 template <class T> struct Tile;
-template <> struct Tile<float> { static constexpr int TY = 16, NU = OOCZ_STENCIL_NU, NR = OOCZ_STENCIL_NR; };
+#ifndef OOCZ_STENCIL_TY
+#define OOCZ_STENCIL_TY 15
+#endif
+#ifndef OOCZ_STENCIL_LB
+#define OOCZ_STENCIL_LB 640
+#endif
+// LB: the thread count __launch_bounds__ is given (0: the real one).  A larger
+// bound caps the registers (65536 / LB), e.g. 640 -> 96 with 16 warps, which
+// leaves each SM sub-partition room for one codec warp next to the stencil.
+template <> struct Tile<float> {
+    static constexpr int TY = OOCZ_STENCIL_TY, NU = OOCZ_STENCIL_NU, NR = OOCZ_STENCIL_NR, LB = OOCZ_STENCIL_LB;
+};
 #ifndef OOCZ_STENCIL64_TY
 #define OOCZ_STENCIL64_TY 8
 #endif
@@ -66,18 +81,21 @@ template <> struct Tile<float> { static constexpr int TY = 16, NU = OOCZ_STENCIL
 #define OOCZ_STENCIL64_NR 4
 #endif
 template <> struct Tile<double> {
-    static constexpr int TY = OOCZ_STENCIL64_TY, NU = OOCZ_STENCIL64_NU, NR = OOCZ_STENCIL64_NR;
+    static constexpr int TY = OOCZ_STENCIL64_TY, NU = OOCZ_STENCIL64_NU, NR = OOCZ_STENCIL64_NR, LB = 0;
 };
 
 template <class T> struct K {
     static constexpr int TY = Tile<T>::TY, NU = Tile<T>::NU, NR = Tile<T>::NR;
     static_assert(NU >= 6 && NR >= 2, "the u ring holds planes z..z+4 plus at least one in flight");
     static constexpr int SW = TX + 8, SH = TY + 8;            // u tile incl. halo
-    static constexpr int kUStage = SW * SH;                   // elements (a 128 B multiple in bytes)
+    // elements per u stage: the TMA box, padded to a 128 B multiple
+    static constexpr int kUStage = (int)(((SW * SH * sizeof(T) + 127) / 128 * 128) / sizeof(T));
     static constexpr int kRStage = 2 * TX * TY;               // u- tile then m tile
     static constexpr int kConsumerWarps = TY;
     static constexpr int kThreads = 32 * (1 + kConsumerWarps);
-    static constexpr unsigned kUBytes = kUStage * sizeof(T);
+    static constexpr int kBoundThreads = Tile<T>::LB ? Tile<T>::LB : kThreads;
+    static constexpr unsigned kUBytes = kUStage * sizeof(T);          // stage stride
+    static constexpr unsigned kUBoxBytes = SW * SH * sizeof(T);       // bytes one TMA box delivers
     static constexpr unsigned kRTileBytes = TX * TY * sizeof(T);
     static constexpr size_t kSmemBytes =
         (size_t)NU * kUBytes + (size_t)NR * 2 * kRTileBytes + 2 * (NU + NR) * sizeof(uint64_t);
@@ -213,14 +231,14 @@ __device__ __forceinline__ bool next_seg(long& it, long items, long tiles, int n
 }
 
 template <class T>
-__global__ void __launch_bounds__(K<T>::kThreads, 1)
+__global__ void __launch_bounds__(K<T>::kBoundThreads, 1)
 stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
                  const __grid_constant__ CUtensorMap tm_m, T* __restrict__ uprev, int nx, int ny,
                  int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs<T> cf)
 {
     constexpr int TY = K<T>::TY, NU = K<T>::NU, NR = K<T>::NR, SW = K<T>::SW;
     constexpr int kUStage = K<T>::kUStage, kRStage = K<T>::kRStage, kConsumerWarps = K<T>::kConsumerWarps;
-    constexpr unsigned kUBytes = K<T>::kUBytes, kRTileBytes = K<T>::kRTileBytes;
+    constexpr unsigned kUBoxBytes = K<T>::kUBoxBytes, kRTileBytes = K<T>::kRTileBytes;
     // dynamic smem only (no static shared variables before it), 1024-aligned, and
     // pointers derived from it directly so the compiler emits LDS, not generic LD
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -256,7 +274,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                 for (int p = sg.zb - 4; p < sg.ze + 4; p++, gu++) {
                     const int s = gu % NU;
                     if (gu >= NU) mbar_wait(&uempty[s], ((gu / NU) & 1) ^ 1);
-                    mbar_expect_tx(&ufull[s], kUBytes);
+                    mbar_expect_tx(&ufull[s], kUBoxBytes);
                     tma_load_3d(uring + s * kUStage, &tm_u, sg.x0 - 4, sg.y0 - 4, p - zv0, &ufull[s]);
                     const int z = p - 4;                   // u-, m of plane z go with u plane z+4
                     if (z >= sg.zb) {
@@ -417,8 +435,7 @@ cudaError_t launch_stencil_step_t(const T* u, T* uprev, const T* m, int nx, int 
         return cudaErrorInvalidValue;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(stencil25_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)KT::kSmemBytes);
+        cudaError_t e = kernel_smem_setup((const void*)stencil25_kernel<T>, (int)KT::kSmemBytes);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }

@@ -90,18 +90,14 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
         st[s] = zb::EncState{31, 0, 64 * rate - zb::kHeaderBits, false};
     }
-    // interleaved event streams
-    for (;;) {
-        bool any = false;
-#pragma unroll
-        for (int s = 0; s < NB; s++) any |= st[s].active();
-        if (!any) break;
-#pragma unroll
-        for (int s = 0; s < NB; s++)
-            if (st[s].active()) {
-                const uint64_t* planes = smem + s * 32 * kThreads;
-                zb::encode_event(st[s], [&](int k) { return planes[k * kThreads + t]; }, bw[s]);
-            }
+    // the event stream: no budget cut while >= 65 bits are left, then the
+    // (at most a few) events that may be cut
+    static_assert(NB == 1, "one event stream per thread");
+    {
+        const uint64_t* planes = smem;
+        auto plane_at = [&](int k) { return planes[k * kThreads + t]; };
+        while (st[0].k >= 0 && st[0].bits >= 65) zb::encode_event<true>(st[0], plane_at, bw[0]);
+        while (st[0].active()) zb::encode_event(st[0], plane_at, bw[0]);
     }
 #pragma unroll
     for (int s = 0; s < NB; s++)
@@ -145,17 +141,11 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
         emax[s] = (int)br[s].read(zb::kEBits) - 127;
         st[s] = zb::DecState{31, 0, 64 * rate - zb::kHeaderBits, false, 0u, 0u};
     }
-    for (;;) {
-        bool any = false;
-#pragma unroll
-        for (int s = 0; s < NB; s++) any |= st[s].active();
-        if (!any) break;
-#pragma unroll
-        for (int s = 0; s < NB; s++)
-            if (st[s].active()) {
-                uint64_t* planes = planes_all + s * 32 * kThreads;
-                zb::decode_event(st[s], br[s], [&](int k, uint64_t x) { planes[k * kThreads + t] = x; });
-            }
+    {
+        uint64_t* planes = planes_all + t;
+        auto plane_set = [&](int k, uint64_t x) { planes[k * kThreads] = x; };
+        while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event<true>(st[0], br[0], plane_set);
+        while (st[0].active()) zb::decode_event(st[0], br[0], plane_set);
     }
 #pragma unroll
     for (int s = 0; s < NB; s++) {
@@ -364,8 +354,7 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
     if (nblocks == 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(zfp_encode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)encode_smem_bytes());
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes());
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -384,8 +373,7 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
     if (nblocks == 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(zfp_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)decode_smem_bytes(64));
+        cudaError_t e = kernel_smem_setup((const void*)zfp_decode_kernel, (int)decode_smem_bytes(64));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -404,8 +392,7 @@ cudaError_t launch_zfp_encode64(const double* in, int nx, int ny, int nz, int ra
     if (nblocks == 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(zfp_encode64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)encode64_smem_bytes());
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode64_kernel, (int)encode64_smem_bytes());
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
@@ -424,8 +411,7 @@ cudaError_t launch_zfp_decode64(const uint64_t* in, int nx, int ny, int nz, int 
     if (nblocks == 0) return cudaSuccess;
     static bool attr_set = false;
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(zfp_decode64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)decode64_smem_bytes(64));
+        cudaError_t e = kernel_smem_setup((const void*)zfp_decode64_kernel, (int)decode64_smem_bytes(64));
         if (e != cudaSuccess) return e;
         attr_set = true;
     }

@@ -109,9 +109,30 @@ ZB_UNROLL
 // In-place 32x32 bit transpose, LSB = column 0: afterwards bit i of a[k] is
 // the former bit k of a[i].  5 butterfly levels of 16 masked swaps.
 ZB_HD void transpose32(uint32_t a[32]) {
-    uint32_t m = 0x0000ffffu;
+#if defined(__CUDA_ARCH__)
+    // the 16- and 8-bit levels are whole half-word / byte exchanges: one PRMT
+    // per output word instead of shift / xor / and / xor / shift / xor
 ZB_UNROLL
+    for (int k = 0; k < 16; k++) {
+        const uint32_t x = a[k], y = a[k + 16];
+        a[k] = __byte_perm(x, y, 0x5410);          // (x.lo, y.lo)
+        a[k + 16] = __byte_perm(x, y, 0x7632);     // (x.hi, y.hi)
+    }
+ZB_UNROLL
+    for (int k = 0; k < 32; k++) {
+        if ((k & 8) == 0) {
+            const uint32_t x = a[k], y = a[k + 8];
+            a[k] = __byte_perm(x, y, 0x6240);      // (x.b0, y.b0, x.b2, y.b2)
+            a[k + 8] = __byte_perm(x, y, 0x7351);  // (x.b1, y.b1, x.b3, y.b3)
+        }
+    }
+    uint32_t m = 0x0f0f0f0fu;
+ZB_UNROLL
+    for (int j = 4; j != 0; j >>= 1) {
+#else
+    uint32_t m = 0x0000ffffu;
     for (int j = 16; j != 0; j >>= 1) {
+#endif
 ZB_UNROLL
         for (int k = 0; k < 32; k++) {
             if ((k & j) == 0) {
@@ -275,8 +296,10 @@ ZB_HD uint32_t bit64(uint32_t lo, uint32_t hi, int p) {    // bit p (0..63) of h
 
 // Emit the low `len` bits of v (len <= 65: a 0 flag after a full word), cut at
 // the remaining budget.
+// FAST: the caller guarantees bits >= 65 (no event emits more), so no cut.
+template <bool FAST = false>
 ZB_HD void emit(BitWriter& bw, uint64_t v, int len, int& bits) {
-    if (len > bits) { len = bits; v &= lowmask(len); }
+    if (!FAST && len > bits) { len = bits; v &= lowmask(len); }
     if (len > 64) { bw.put(v, 64); bw.put(0, len - 64); }
     else if (len > 0) bw.put(v, len);
     bits -= len;
@@ -295,7 +318,7 @@ struct EncState {
     ZB_HD bool active() const { return k >= 0 && bits > 0; }
 };
 
-template <class PlaneAt>
+template <bool FAST = false, class PlaneAt>
 ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
     const int n = st.n;
     const uint64_t x = plane_at(st.k);
@@ -320,7 +343,7 @@ ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
     const bool doneA = n >= 64 || yz;
     const bool ip = st.inplane;
     const uint32_t vl = ip ? vBl : vAl, vh = ip ? vBh : vAh;
-    emit(bw, ((uint64_t)vh << 32) | vl, ip ? lenB : lenA, st.bits);
+    emit<FAST>(bw, ((uint64_t)vh << 32) | vl, ip ? lenB : lenA, st.bits);
     const bool done = ip ? doneB : doneA;
     st.n = ip ? nB : n;
     st.k -= done ? 1 : 0;
@@ -330,6 +353,8 @@ ZB_HD void encode_event(EncState& st, PlaneAt plane_at, BitWriter& bw) {
 template <class PlaneAt>
 ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw, int top_plane = 31) {
     EncState st{top_plane, 0, bits, false};
+    // no event emits more than 65 bits: while that many are left, no budget cut
+    while (st.k >= 0 && st.bits >= 65) encode_event<true>(st, plane_at, bw);
     while (st.active()) encode_event(st, plane_at, bw);
 }
 
@@ -347,9 +372,13 @@ struct DecState {
     ZB_HD bool active() const { return k >= 0 && (bits > 0 || inplane); }
 };
 
-template <class PlaneSet>
+// FAST: the caller guarantees bits >= 66 (an event consumes at most 65), so
+// every budget clamp below is the identity; the plane being assembled is then
+// stored on every event (plane_set is an unconditional shared-memory store:
+// the last store of plane k is its final value), with no branch.
+template <bool FAST = false, class PlaneSet>
 ZB_HD void decode_event(DecState& st, BitReader& br, PlaneSet plane_set) {
-    const int n = st.n, bits = st.bits;
+    const int n = st.n, bits = FAST ? 1 << 20 : st.bits;
     const uint32_t* p32 = reinterpret_cast<const uint32_t*>(br.p) + (br.pos >> 5);
     const int o = br.pos & 31;
     const uint32_t w0 = p32[0], w1 = p32[1], w2 = p32[2];
@@ -379,14 +408,21 @@ ZB_HD void decode_event(DecState& st, BitReader& br, PlaneSet plane_set) {
     const bool cont = (ip ? contB : contA) != 0u;
     st.n = ip ? nB + 1 : n;
     br.pos += c;
-    st.bits = bits - c;
-    if (!cont) { plane_set(st.k, ((uint64_t)st.xhi << 32) | st.xlo); st.k -= 1; }
+    st.bits -= c;
+    if (FAST) {
+        plane_set(st.k, ((uint64_t)st.xhi << 32) | st.xlo);
+        st.k -= cont ? 0 : 1;
+    } else if (!cont) {
+        plane_set(st.k, ((uint64_t)st.xhi << 32) | st.xlo);
+        st.k -= 1;
+    }
     st.inplane = cont;
 }
 
 template <class PlaneSet>
 ZB_HD void decode_planes(PlaneSet plane_set, int bits, BitReader& br, int top_plane = 31) {
     DecState st{top_plane, 0, bits, false, 0u, 0u};
+    while (st.k >= 0 && st.bits >= 66) decode_event<true>(st, br, plane_set);
     while (st.active()) decode_event(st, br, plane_set);
     for (int k = st.k; k >= 0; --k) plane_set(k, 0ull);
 }
