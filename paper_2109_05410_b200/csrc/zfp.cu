@@ -73,9 +73,20 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         }
         const uint32_t e = (uint32_t)Emax + 1u;        // emax + 127, emax = Emax - 126
         bw[s].put(2u * e + 1u, zb::kHeaderBits);
+        // q = trunc(x 2^(30 - emax)).  When 2^(30 - emax) is a normal fp32 (emax >= -97)
+        // and the block is finite, x * 2^(30 - emax) is exact wherever |q| >= 1 (an
+        // underflowing product is < 1 in magnitude and truncates to 0 either way):
+        // one FMUL + one F2I.TRUNC per value, off the integer ALU pipe that binds
+        // this kernel.  Otherwise the bit-field path.
         int32_t q[64];
+        if (Emax >= 29 && Emax < 255) {
+            const float sc = __int_as_float((283 - Emax) << 23);   // 2^(30 - emax), emax = Emax - 126
 #pragma unroll
-        for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+            for (int i = 0; i < 64; i++) q[i] = __float2int_rz(__fmul_rn(__uint_as_float(v[i]), sc));
+        } else {
+#pragma unroll
+            for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+        }
         zb::fwd_xform(q);
         constexpr int perm[64] = OOCZ_PERM3;
         uint32_t lo[32], hi[32];
@@ -144,7 +155,7 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     {
         uint64_t* planes = planes_all + t;
         auto plane_set = [&](int k, uint64_t x) { planes[k * kThreads] = x; };
-        while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event<true>(st[0], br[0], plane_set);
+        while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event_fast(st[0], br[0], plane_set);
         while (st[0].active()) zb::decode_event(st[0], br[0], plane_set);
     }
 #pragma unroll
