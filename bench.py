@@ -299,11 +299,11 @@ def roofline(evs, peak_gbs, peak_src):
     kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
     traffic, tsrc = None, None
     try:   # DRAM bytes per launch from a committed ncu capture of the same in-step launches
-        with open(os.path.join(ROOT, "profiles", "r01_stencil_instep_traffic.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)) as fh:
             tj = json.load(fh)
         if dom == "stencil":
             traffic = int(tj["traffic_over_algorithmic"] * nbytes / n)
-            tsrc = ("profiles/r01_stencil_instep_traffic.json: ncu dram read+write / algorithmic = "
+            tsrc = (f"profiles/{TRAFFIC_JSON}: ncu dram read+write / algorithmic = "
                     f"{tj['traffic_over_algorithmic']} on the same launches, x this run's algorithmic bytes per launch")
     except Exception:
         pass
@@ -311,6 +311,37 @@ def roofline(evs, peak_gbs, peak_src):
             "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
             "traffic": traffic, "traffic_source": tsrc, "avg_launch_ms": round(ms / n, 4),
             "algorithmic_bytes_per_launch": int(nbytes / n)}, table
+
+
+TRAFFIC_JSON = "r01_stencil_instep_traffic.json"
+ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
+
+
+def codec_alu_roofline(table) -> dict | None:
+    """The codec kernels are bound by the integer ALU pipe (IADD3/LOP3/SHF/PRMT,
+    DESIGN.md "Roofline"), not by HBM: their fraction is the ALU pipe's share of
+    its peak issue rate (148 SMs x 4 sub-partitions x one warp-instruction per
+    2 cycles at 1965 MHz = 581.6 G warp-instructions/s), measured by ncu
+    (sm__inst_executed_pipe_alu) on the committed capture of the same kernels."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_ncu_kernels.json")) as fh:
+            kj = json.load(fh)
+    except Exception:
+        return None
+    out = {}
+    for name, stage in (("zfp_decode_kernel", "decode"), ("zfp_encode_kernel", "encode")):
+        ks = [k for k in kj["kernels"] if k["kernel"].endswith(name)]
+        if not ks:
+            continue
+        k = ks[0]
+        frac = k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"] / 100.0
+        out[name] = {"bound": "alu", "achieved": round(frac * ALU_PEAK, 1), "peak": round(ALU_PEAK, 1),
+                     "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
+                     "issue_active": round(k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100, 4),
+                     "isolated_us": k["gpu__time_duration.sum"],
+                     "in_step_avg_ms": round(table[stage]["ms"] / table[stage]["launches"], 4) if stage in table else None,
+                     "source": "profiles/r01_ncu_kernels.json (ncu --set full, one C2 slab, rate 16)"}
+    return out or None
 
 
 def gpu_arm(args):
@@ -337,20 +368,25 @@ def gpu_arm(args):
         # orchestration of the SAME computation (bit-identical results, tests):
         # serpentine sweeps + m resident in HBM (readings R22/R23);
         # "pf_*" are the paper-faithful schedule (ascending sweeps, m streamed).
-        O = dict(serpentine=1, m_resident=1, slots=3)
+        # Each path runs its fastest schedule of the same computation: with the store
+        # in HBM m resident (serpentine sweeps save host-link bytes only, and the
+        # block at each turn serialises decode after its own encode); out of core
+        # serpentine + m resident + 3 staging slots.
+        OD = dict(m_resident=1)
+        OH = dict(serpentine=1, m_resident=1, slots=3)
         PF = dict(serpentine=0, m_resident=0)
-        modes = [("zfp_dev", 1, (RATE,) * 3, O), ("zfp_host", 0, (RATE,) * 3, O),
-                 ("raw_dev", 1, (0, 0, 0), O), ("raw_host", 0, (0, 0, 0), O)]
+        modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
+                 ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
         if not args.quick:   # configs[1]: rates 8/16/24
-            modes += [(f"r{r}_{k}", st, (r,) * 3, O) for r in (8, 24) for k, st in (("dev", 1), ("host", 0))]
+            modes += [(f"r{r}_{k}", st, (r,) * 3, o) for r in (8, 24) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
             # the paper-faithful schedule, and each orchestration alone
             modes += [("pf_zfp_dev", 1, (RATE,) * 3, PF), ("pf_zfp_host", 0, (RATE,) * 3, PF),
                       ("pf_raw_dev", 1, (0, 0, 0), PF), ("pf_raw_host", 0, (0, 0, 0), PF),
-                      ("mres_dev", 1, (RATE,) * 3, dict(m_resident=1)), ("mres_host", 0, (RATE,) * 3, dict(m_resident=1)),
+                      ("mres_host", 0, (RATE,) * 3, dict(m_resident=1)),
                       ("serp_dev", 1, (RATE,) * 3, dict(serpentine=1)), ("serp_host", 0, (RATE,) * 3, dict(serpentine=1)),
-                      # a third staging slot: the block after each turn decodes its own rows from
-                      # the device too (they were written back, but need not come back)
-                      ("slots3_host", 0, (RATE,) * 3, dict(O, slots=3))]
+                      ("sm_dev", 1, (RATE,) * 3, dict(serpentine=1, m_resident=1)),
+                      # two staging slots: the block after each turn re-reads its own rows
+                      ("sm2_host", 0, (RATE,) * 3, dict(serpentine=1, m_resident=1, slots=2))]
             # the paper's codes 2-4 as fp32 rate vectors, out of core,
             # paper-faithful schedule: one read-write field (u-, reading R7) at 16/32, the
             # read-only m at 16/32, one read-write field + m at 12/32 (the paper's 24/64)
@@ -359,7 +395,7 @@ def gpu_arm(args):
             # temporal-blocking depth: T = 8 and the paper's T = 12
             # (PAPER.md:217), same P = 128: host bytes per step fall as 1/T, redundant
             # stencil work grows as 4(T-1)/P
-            modes += [(f"t{t}_{k}", st, (RATE,) * 3, dict(O, tb=t)) for t in (8, 12) for k, st in (("dev", 1), ("host", 0))]
+            modes += [(f"t{t}_{k}", st, (RATE,) * 3, dict(o, tb=t)) for t in (8, 12) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
             # the paper's own precision (fp64) and rates 32/64, 24/64
             # (PAPER.md:213-215): codes 1-4 out of core (paper-faithful schedule), plus all
             # fields at 32/64 (paper-faithful and orchestrated)
@@ -368,8 +404,8 @@ def gpu_arm(args):
                       ("f64pm3_host", 0, (0, 0, 32), F), ("f64pm4_host", 0, (0, 24, 24), F),
                       ("f64all_host", 0, (32, 32, 32), F), ("f64all_dev", 1, (32, 32, 32), F),
                       ("f64raw_dev", 1, (0, 0, 0), F),
-                      ("f64allo_host", 0, (32, 32, 32), dict(O, precision=64)),
-                      ("f64allo_dev", 1, (32, 32, 32), dict(O, precision=64))]
+                      ("f64allo_host", 0, (32, 32, 32), dict(OH, precision=64)),
+                      ("f64allo_dev", 1, (32, 32, 32), dict(OD, precision=64))]
         for label, store, rates, opt in modes:
             tb = opt.get("tb", T)
             prec = opt.get("precision", 32)
@@ -432,21 +468,23 @@ def gpu_arm(args):
         paper_fp64["all_32_orchestrated"] = {"rates": [32, 32, 32], "e2e": round(out["f64allo_host"]["cups"], 1),
                                              "value": round(out["f64allo_dev"]["cups"], 1),
                                              "speedup": round(out["f64allo_host"]["cups"] / ref["cups"], 3),
-                                             "schedule": "serpentine + m resident"}
+                                             "schedule": "value: m resident; e2e: serpentine + m resident, 3 slots"}
     orch = None
-    if "mres_dev" in out:
+    if "mres_host" in out:
         orch = {"what": "SURVEY 8(f) row 2, beyond the paper, same bits: the paper-faithful schedule (ascending "
                         "sweeps, m streamed), m decoded once and kept in HBM (m_resident=1, R23), serpentine "
-                        "sweeps (serpentine=1, R22), both (= the headline)"}
-        for key, lab in (("paper_faithful", "pf_zfp"), ("m_resident", "mres"), ("serpentine", "serp"),
-                         ("serpentine+m_resident", "zfp")):
-            dv, hs = out[lab + "_dev"], out[lab + "_host"]
+                        "sweeps (serpentine=1, R22), both (2 staging slots); the headline value runs m_resident, "
+                        "the headline e2e serpentine + m_resident with 3 staging slots"}
+        for key, dlab, hlab in (("paper_faithful", "pf_zfp_dev", "pf_zfp_host"),
+                                ("m_resident", "zfp_dev", "mres_host"), ("serpentine", "serp_dev", "serp_host"),
+                                ("serpentine+m_resident", "sm_dev", "sm2_host")):
+            dv, hs = out[dlab], out[hlab]
             orch[key] = {"value": round(dv["cups"], 1), "e2e": round(hs["cups"], 1),
                          "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
                          "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
                          "e2e_host_link_GBps": round(hs["h2d_per_sweep"] / (hs["s"] / args.steps) / 1e9, 2)}
-        if "slots3_host" in out:
-            hs = out["slots3_host"]
+        if "zfp_host" in out:
+            hs = out["zfp_host"]
             orch["serpentine+m_resident, 3 staging slots"] = {
                 "e2e": round(hs["cups"], 1), "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
                 "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
@@ -477,8 +515,10 @@ def gpu_arm(args):
         "data": "synthetic (DENSE seed 1 wavefield, u- = u, LAYERED m; SURVEY 8(d))",
         "config": {"workload": f"C2: {NX}^3 fp32 per GPU, 25-point leapfrog, P={P} ({NZ // P} z-blocks), "
                                f"T={T}, ZFP rate {RATE} on u, u-, m; compressed store resident in HBM; "
-                               f"serpentine sweeps, m decoded once (same bits as the paper's schedule)",
-                   "schedule": "serpentine=1, m_resident=1 (paper-faithful schedule: orchestrated.paper_faithful)",
+                               f"m decoded once (same bits as the paper's schedule)",
+                   "schedule": "value: m_resident=1; e2e: serpentine=1, m_resident=1, slots=3 (each path's "
+                               "fastest schedule, all bit-identical; the paper-faithful schedule and each "
+                               "orchestration alone: orchestrated.*)",
                    "grid": [NX, NY, NZ * world], "tb": T, "block_planes": P, "rate": RATE,
                    "step": "one sweep = T leapfrog steps over the whole grid",
                    "l2": "inputs larger than L2 (compressed store 768 MiB + 480 MiB slab per GPU)",
@@ -503,7 +543,7 @@ def gpu_arm(args):
                 "lanes": lanes_summary(e["evs"])},
         "raw": {"value": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1),
                 "e2e_h2d_bytes_per_step": int(out["raw_host"]["h2d_per_sweep"]),
-                "schedule": "the headline's (serpentine, m resident)"},
+                "schedule": "the headline's (value: m resident; e2e: serpentine + m resident, 3 slots)"},
         "speedup_zfp_vs_raw": {"value": round(v["cups"] / out["raw_dev"]["cups"], 3),
                                "e2e": round(e["cups"] / out["raw_host"]["cups"], 3),
                                "paper_context": "1.20x (fp64, V100-PCIe, PAPER.md:227)",
@@ -512,6 +552,7 @@ def gpu_arm(args):
         "max_rel_error": err,
         "gpu_launches": int(v["launches"]),
         "roofline": roof,
+        "roofline_codec": codec_alu_roofline(table),
         "kernels_in_step": table,
         "lanes": lanes_summary(v["evs"]),
         "roofline_isolated": iso,
