@@ -295,3 +295,34 @@ def test_serpentine_partitioned_group(world):
             z.oocz_destroy(c)
     ou, oup = _run_oracle(u, up, m, T, rates, [9])
     assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+
+
+@pytest.fixture(scope="module")
+def c2_state():
+    """BASELINE configs[1] at full size: the bench's 512^3 DENSE(1) / LAYERED
+    workload, and the oracle's result after 2 sweeps (T = 4, rate 16)."""
+    n = 512
+    u = synth.dense(n, n, n, seed=1)
+    m = synth.layered(n, n, n)
+    ou, oup = oracle.run(u, u, m, 4, (16, 16, 16), 8)
+    return u, m, ou, oup
+
+
+@pytest.mark.parametrize("store,opts", [
+    (1, dict(m_resident=1)),                                  # bench value path
+    (0, dict(serpentine=1, m_resident=1, slots=3)),           # bench e2e path
+    (0, dict()),                                              # the paper-faithful schedule
+])
+def test_c2_full_size_bench_configs_bit_exact(c2_state, store, opts):
+    """The bench's own launch configurations (512^3, P = 128, T = 4, rate 16) for
+    2 sweeps -- covering a serpentine turn -- equal the oracle bit for bit over
+    the whole field."""
+    u, m, ou, oup = c2_state
+    z = Z()
+    cfg = z.oocz_default_config(512, 512, 512, tb=4, block_planes=128, rate=[16, 16, 16], store=store, **opts)
+    with z.Stepper(cfg) as s:
+        s.set(u, u, m)
+        s.step(8)
+        gu, gup = s.get(z.OOCZ_U), s.get(z.OOCZ_UPREV)
+    assert np.array_equal(bits(gu), bits(ou))
+    assert np.array_equal(bits(gup), bits(oup))

@@ -12,12 +12,12 @@ torch.cuda.set_device(0)
 fields = bench.make_fields(0, bench.NZ)
 cells = bench.NX * bench.NY * bench.NZ * bench.T * 10
 out = [os.path.basename(os.environ.get("OOCZ_LIB", "liboocz.so"))]
-for label, store, rates, slots in (("zfp_dev", 1, (16,) * 3, 2), ("raw_dev", 1, (0,) * 3, 2),
-                                   ("zfp_host", 0, (16,) * 3, 3)):
+for label, store, rates, serp, slots in (("zfp_dev", 1, (16,) * 3, 0, 2), ("raw_dev", 1, (0,) * 3, 0, 2),
+                                         ("zfp_host", 0, (16,) * 3, 1, 3)):
     best = 0.0
     for _ in range(2):
         dev_s, st, evs, launches, ctx = bench.run_mode(Z, store, rates, fields, 0, 1, None, 0, 10, 3, None, 0,
-                                                      m_resident=1, serpentine=1, slots=slots)
+                                                      m_resident=1, serpentine=serp, slots=slots)
         Z.oocz_destroy(ctx)
         best = max(best, cells / dev_s / 1e9)
     out.append(f"{label} {best:.1f} G")
