@@ -115,6 +115,8 @@ def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmu
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
                                 slots=slots, profile=profile, slab_sets=slab_sets)
+    if callable(nccl_id):   # a fresh NCCL unique id per communicator (an id bootstraps one init only)
+        nccl_id = nccl_id()
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
@@ -357,7 +359,7 @@ def gpu_arm(args):
         dist = td
     from paper_2109_05410_b200 import oocz as Z
     from paper_2109_05410_b200 import dist as D
-    nccl_id = D.share_nccl_id(dist, rank, Z.oocz_get_nccl_id, device="cuda") if world > 1 else None
+    nccl_id = (lambda: D.share_nccl_id(dist, rank, Z.oocz_get_nccl_id, device="cuda")) if world > 1 else None
     fields = make_fields(rank, NZ)
     cells = NX * NY * NZ * world * T * args.steps
     peak_gbs, peak_src = peaks()

@@ -22,5 +22,6 @@ for label, store, rates, serp, slots in (("zfp_dev", 1, (16,) * 3, 0, 2), ("raw_
         best = max(best, cells / dev_s / 1e9)
     out.append(f"{label} {best:.1f} G")
 iso = bench.isolated_kernels(Z, fields, 6457.1)
-out.append("stencil_iso_ms %.4f" % iso["stencil25_kernel"]["ms"])
+for k in ("stencil25_kernel", "zfp_encode_kernel", "zfp_decode_kernel", "zfp_encode64_kernel", "zfp_decode64_kernel"):
+    out.append("%s %.1f us" % (k.replace("_kernel", ""), iso[k]["ms"] * 1e3))
 print("  ".join(out), flush=True)
