@@ -154,6 +154,19 @@ oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const void* d_sr
 oocz_status oocz_step(oocz_ctx* ctx, int64_t nsteps);
 /* Decode this rank's slab of field f into dst (count values of the context's precision). */
 oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count);
+/* The same two calls on a z-range, for slabs too large to hold in host memory
+ * at once (3 x 103 GB raw per GPU).  Planes [z0, z0 + nplanes)
+ * of this rank's slab (rank-local, both multiples of 4: whole ZFP block-rows,
+ * else OOCZ_EALIGN; outside [0, nz/world): OOCZ_EINVAL); src / dst hold
+ * nplanes * nx * ny values (x fastest), in device memory if *_on_device != 0,
+ * else host memory (pageable or pinned).  A field counts as set once every
+ * block-row has been set (oocz_step needs all three; get_* needs the field);
+ * set_field_planes applies the same checks as set_field to its planes (NaN /
+ * Inf, m range) and, on failure, leaves those rows unset. */
+oocz_status oocz_set_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,
+                                  const void* src, int32_t src_on_device);
+oocz_status oocz_get_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,
+                                  void* dst, int32_t dst_on_device);
 oocz_status oocz_get_field_device(oocz_ctx* ctx, int32_t field, void* d_dst, size_t count);
 /* Checkpoint / restore.  Between oocz_step calls the
  * compressed store IS the whole state; a decode -> encode round trip is not

@@ -142,6 +142,7 @@ struct oocz_ctx {
     size_t plane_elems = 0, pb = 0;         // elements / bytes per plane
     size_t row_bytes[3] = {0, 0, 0};       // bytes per 4-plane block-row in the store
     bool field_set[3] = {false, false, false};
+    std::vector<uint8_t> rows_set[3];       // 4-plane rows of each field set so far
     bool poisoned = false;
     std::string err;
 
@@ -388,6 +389,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     ctx->S = cfg->nz / world;
     ctx->T = cfg->tb; ctx->h = 4 * cfg->tb; ctx->P = cfg->block_planes;
     ctx->D = ctx->S / ctx->P;
+    for (int f = 0; f < 3; f++) ctx->rows_set[f].assign(ctx->S / 4, 0);
     ctx->L = ctx->P + 2 * ctx->h;
     ctx->plane_elems = (size_t)cfg->nx * cfg->ny;
     ctx->nsets = cfg->slab_sets ? cfg->slab_sets : 2;
@@ -655,15 +657,22 @@ extern "C" oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, siz
 }
 
 // ------------------------------------------------------------------ set / get
-static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_v, size_t count, bool on_device)
+// Compress planes [z0, z0 + nplanes) (rank-local, 4-aligned) of field f from src
+// into the store (the initial round trip).  The field counts as set
+// once every 4-plane row has been set; then its halos are (re)published.
+static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes, const void* src_v,
+                                   bool on_device)
 {
     if (!ctx) return OOCZ_EINVAL;
     if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
     if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
-    if (!src_v && count) return fail(ctx, OOCZ_EINVAL, "null source");
-    const size_t want = ctx->plane_elems * (size_t)ctx->S;
-    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
+    if (z0 % 4 || nplanes % 4) return fail(ctx, OOCZ_EALIGN, "z0 (%d) and nplanes (%d) must be multiples of 4", z0, nplanes);
+    if (z0 < 0 || nplanes < 0 || z0 + nplanes > ctx->S)
+        return fail(ctx, OOCZ_EINVAL, "planes [%d, %d) outside [0, %d)", z0, z0 + nplanes, ctx->S);
+    if (!src_v && nplanes) return fail(ctx, OOCZ_EINVAL, "null source");
     CK(cudaSetDevice(ctx->device));
+    // rows of this range count as unset until the call succeeds
+    for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 0;
     ctx->field_set[field] = false;
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     cudaStream_t s = ctx->s_comp;
@@ -672,11 +681,11 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_
     const uint8_t* src = static_cast<const uint8_t*>(src_v);
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     CK(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(unsigned int), s));
-    for (int z = 0; z < ctx->S; z += chunk) {
-        const int np = std::min(chunk, ctx->S - z);
+    for (int z = z0; z < z0 + nplanes; z += chunk) {
+        const int np = std::min(chunk, z0 + nplanes - z);
         const size_t n = (size_t)np * ctx->plane_elems;
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
-        CK(cudaMemcpyAsync(buf, src + (size_t)z * ctx->pb, (size_t)np * ctx->pb,
+        CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
         if (ctx->esz == 8)
             CK(launch_scan_field(reinterpret_cast<const double*>(buf), n, ctx->d_flags,
@@ -715,7 +724,10 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_
         if ((double)mx > mmax)
             return fail(ctx, OOCZ_ECFL, "max m (%.9g) > m_max(c) (%.9g)", (double)mx, mmax);
     }
-    ctx->field_set[field] = true;
+    for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 1;
+    ctx->field_set[field] = std::all_of(ctx->rows_set[field].begin(), ctx->rows_set[field].end(),
+                                        [](uint8_t v) { return v != 0; });
+    if (!ctx->field_set[field]) return OOCZ_OK;
     if (field != OOCZ_M && ctx->halo) {
         std::string herr;
         if (!halo_capture_store(ctx->halo, field, ctx->store[field], host, ctx->S, ctx->row_bytes[field], s, &herr) ||
@@ -731,6 +743,14 @@ static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_
     return OOCZ_OK;
 }
 
+static oocz_status set_field_impl(oocz_ctx* ctx, int32_t field, const void* src_v, size_t count, bool on_device)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    const size_t want = ctx->plane_elems * (size_t)ctx->S;
+    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
+    return set_planes_impl(ctx, field, 0, ctx->S, src_v, on_device);
+}
+
 extern "C" oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const void* src, size_t count)
 {
     return set_field_impl(ctx, field, src, count, false);
@@ -739,23 +759,31 @@ extern "C" oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const
 {
     return set_field_impl(ctx, field, d_src, count, true);
 }
+extern "C" oocz_status oocz_set_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,
+                                             const void* src, int32_t src_on_device)
+{
+    return set_planes_impl(ctx, field, z0, nplanes, src, src_on_device != 0);
+}
 
-static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, void* dst_v, size_t count, bool on_device)
+// Decode planes [z0, z0 + nplanes) (rank-local, 4-aligned) of field f into dst.
+static oocz_status get_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes, void* dst_v,
+                                   bool on_device)
 {
     if (!ctx) return OOCZ_EINVAL;
     if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
     if (field < 0 || field > 2) return fail(ctx, OOCZ_EINVAL, "unknown field %d", field);
     if (!ctx->field_set[field]) return fail(ctx, OOCZ_ESTATE, "field %d was never set", field);
-    const size_t want = ctx->plane_elems * (size_t)ctx->S;
-    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
-    if (!dst_v && count) return fail(ctx, OOCZ_EINVAL, "null destination");
+    if (z0 % 4 || nplanes % 4) return fail(ctx, OOCZ_EALIGN, "z0 (%d) and nplanes (%d) must be multiples of 4", z0, nplanes);
+    if (z0 < 0 || nplanes < 0 || z0 + nplanes > ctx->S)
+        return fail(ctx, OOCZ_EINVAL, "planes [%d, %d) outside [0, %d)", z0, z0 + nplanes, ctx->S);
+    if (!dst_v && nplanes) return fail(ctx, OOCZ_EINVAL, "null destination");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->s_comp;
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int chunk = ctx->P;
     uint8_t* dst = static_cast<uint8_t*>(dst_v);
-    for (int z = 0; z < ctx->S; z += chunk) {
-        const int np = std::min(chunk, ctx->S - z);
+    for (int z = z0; z < z0 + nplanes; z += chunk) {
+        const int np = std::min(chunk, z0 + nplanes - z);
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
@@ -766,11 +794,25 @@ static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, void* dst_v, siz
         } else {
             CK(decode_or_copy(ctx, field, ctx->store[field] + off, np, buf, s));
         }
-        CK(cudaMemcpyAsync(dst + (size_t)z * ctx->pb, buf, (size_t)np * ctx->pb,
+        CK(cudaMemcpyAsync(dst + (size_t)(z - z0) * ctx->pb, buf, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
     }
     CK(cudaStreamSynchronize(s));
     return OOCZ_OK;
+}
+
+static oocz_status get_field_impl(oocz_ctx* ctx, int32_t field, void* dst_v, size_t count, bool on_device)
+{
+    if (!ctx) return OOCZ_EINVAL;
+    const size_t want = ctx->plane_elems * (size_t)ctx->S;
+    if (count != want) return fail(ctx, OOCZ_EINVAL, "count (%zu) != nx*ny*nz/world (%zu)", count, want);
+    return get_planes_impl(ctx, field, 0, ctx->S, dst_v, on_device);
+}
+
+extern "C" oocz_status oocz_get_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes, void* dst,
+                                             int32_t dst_on_device)
+{
+    return get_planes_impl(ctx, field, z0, nplanes, dst, dst_on_device != 0);
 }
 
 extern "C" oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count)
@@ -813,6 +855,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     cudaStream_t s = ctx->s_comp;
     ctx->field_set[field] = false;
+    std::fill(ctx->rows_set[field].begin(), ctx->rows_set[field].end(), 0);
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     if (host) std::memcpy(ctx->store[field], src, bytes);
     else CK(cudaMemcpy(ctx->store[field], src, bytes, cudaMemcpyHostToDevice));
@@ -830,6 +873,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
         }
         CK(cudaStreamSynchronize(s));
     }
+    std::fill(ctx->rows_set[field].begin(), ctx->rows_set[field].end(), 1);
     ctx->field_set[field] = true;
     if (ctx->halo) {                            // the neighbours' halos come from the store
         std::string herr;

@@ -75,6 +75,8 @@ _SIGS = {
     "oocz_step": (C.c_int, [_ctx_p, C.c_int64]),
     "oocz_get_field": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_get_field_device": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
+    "oocz_set_field_planes": (C.c_int, [_ctx_p, _i32, _i32, _i32, _vp, _i32]),
+    "oocz_get_field_planes": (C.c_int, [_ctx_p, _i32, _i32, _i32, _vp, _i32]),
     "oocz_get_stats": (C.c_int, [_ctx_p, C.POINTER(oocz_stats)]),
     "oocz_store_bytes": (C.c_size_t, [_ctx_p, _i32]),
     "oocz_save_store": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
@@ -244,6 +246,29 @@ def oocz_set_field(ctx: int, field: int, src: np.ndarray) -> None:
 
 def oocz_set_field_device(ctx: int, field: int, d_src, count: int) -> None:
     _check(_lib.oocz_set_field_device(ctx, field, _ptr(d_src), count), ctx)
+
+
+def oocz_set_field_planes(ctx: int, field: int, z0: int, src, nplanes: int | None = None) -> None:
+    """Planes [z0, z0 + nplanes) from a host array (nplanes, ny, nx) or a device
+    tensor / pointer (nplanes required for a raw pointer)."""
+    if isinstance(src, np.ndarray):
+        a = np.ascontiguousarray(src, field_dtype(ctx))
+        _check(_lib.oocz_set_field_planes(ctx, field, z0, a.shape[0], a.ctypes.data, 0), ctx)
+    else:
+        n = src.shape[0] if nplanes is None else nplanes
+        _check(_lib.oocz_set_field_planes(ctx, field, z0, n, _ptr(src), 1), ctx)
+
+
+def oocz_get_field_planes(ctx: int, field: int, z0: int, dst, nplanes: int | None = None):
+    """Planes [z0, z0 + nplanes) into a host array (nplanes, ny, nx) or a device
+    tensor / pointer."""
+    if isinstance(dst, np.ndarray):
+        assert dst.dtype == field_dtype(ctx) and dst.flags.c_contiguous
+        _check(_lib.oocz_get_field_planes(ctx, field, z0, dst.shape[0], dst.ctypes.data, 0), ctx)
+    else:
+        n = dst.shape[0] if nplanes is None else nplanes
+        _check(_lib.oocz_get_field_planes(ctx, field, z0, n, _ptr(dst), 1), ctx)
+    return dst
 
 
 def oocz_step(ctx: int, nsteps: int) -> None:

@@ -1,0 +1,84 @@
+"""Set / read back a field by z-ranges (oocz_set_field_planes /
+oocz_get_field_planes): the calls that let slabs larger than host memory be
+initialised and sampled.  Setting in chunks stores exactly the
+bytes a whole-field set stores, so the run equals the oracle bit for bit."""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2109_05410_b200 import synth
+from gpu_util import Z, bits
+
+pytestmark = pytest.mark.gpu
+
+
+def _fields(nx, ny, nz):
+    u = synth.dense(nx, ny, nz, seed=21)
+    return u, (u * np.float32(0.9)).astype(np.float32), synth.layered(nx, ny, nz)
+
+
+@pytest.mark.parametrize("store,m_resident,chunk", [(0, 0, 8), (1, 0, 12), (0, 1, 20), (1, 1, 4)])
+def test_chunked_set_equals_whole_set_and_oracle(store, m_resident, chunk):
+    import torch
+    z = Z()
+    nx, ny, nz, T, P, rates = 40, 24, 96, 2, 24, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
+                                m_resident=m_resident)
+    with z.Stepper(cfg) as a:
+        a.set(u, up, m)
+        whole = [z.oocz_save_store(a.ctx, f) for f in range(3)]
+    with z.Stepper(cfg) as b:
+        # u from host chunks, u- from device chunks, m in reverse order
+        for z0 in range(0, nz, chunk):
+            z.oocz_set_field_planes(b.ctx, z.OOCZ_U, z0, u[z0:z0 + chunk])
+            z.oocz_set_field_planes(b.ctx, z.OOCZ_UPREV, z0, torch.from_numpy(up[z0:z0 + chunk].copy()).cuda())
+        for z0 in reversed(range(0, nz, chunk)):
+            z.oocz_set_field_planes(b.ctx, z.OOCZ_M, z0, m[z0:z0 + chunk])
+        torch.cuda.synchronize()
+        for f in range(3):
+            assert np.array_equal(z.oocz_save_store(b.ctx, f), whole[f])
+        b.step(7)
+        gu = b.get(z.OOCZ_U)
+        # read back by ranges, to host and to device
+        parts = [z.oocz_get_field_planes(b.ctx, z.OOCZ_U, z0, np.empty((min(chunk, nz - z0), ny, nx), np.float32))
+                 for z0 in range(0, nz, chunk)]
+        assert np.array_equal(bits(np.concatenate(parts)), bits(gu))
+        d = torch.empty((8, ny, nx), dtype=torch.float32, device="cuda")
+        z.oocz_get_field_planes(b.ctx, z.OOCZ_U, 16, d)
+        assert np.array_equal(bits(d.cpu().numpy()), bits(gu[16:24]))
+    ou, _ = oracle.run(u, up, m, T, rates, 7)
+    assert np.array_equal(bits(gu), bits(ou))
+
+
+def test_plane_range_errors_and_partial_state():
+    z = Z()
+    nx, ny, nz = 16, 16, 32
+    u, up, m = _fields(nx, ny, nz)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=2, block_planes=16, rate=[16, 16, 16])
+    with z.Stepper(cfg) as s:
+        with pytest.raises(z.OoczError) as e:
+            z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 2, u[2:10])
+        assert e.value.status == z.OOCZ_EALIGN
+        with pytest.raises(z.OoczError) as e:
+            z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 28, u[:8])
+        assert e.value.status == z.OOCZ_EINVAL
+        z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 0, u[:16])
+        z.oocz_set_field(s.ctx, z.OOCZ_UPREV, up)
+        z.oocz_set_field(s.ctx, z.OOCZ_M, m)
+        with pytest.raises(z.OoczError) as e:            # u's rows [16, 32) never set
+            z.oocz_step(s.ctx, 2)
+        assert e.value.status == z.OOCZ_ESTATE
+        with pytest.raises(z.OoczError) as e:
+            z.oocz_get_field_planes(s.ctx, z.OOCZ_U, 0, np.empty((4, ny, nx), np.float32))
+        assert e.value.status == z.OOCZ_ESTATE
+        z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, u[16:])
+        bad = u[16:24].copy()
+        bad[3, 2, 1] = np.nan
+        with pytest.raises(z.OoczError) as e:            # a failed range leaves its rows unset
+            z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, bad)
+        assert e.value.status == z.OOCZ_ENONFINITE
+        with pytest.raises(z.OoczError):
+            z.oocz_step(s.ctx, 2)
+        z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, u[16:24])
+        z.oocz_step(s.ctx, 2)
