@@ -162,7 +162,9 @@ oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count
  * else host memory (pageable or pinned).  A field counts as set once every
  * block-row has been set (oocz_step needs all three; get_* needs the field);
  * set_field_planes applies the same checks as set_field to its planes (NaN /
- * Inf, m range) and, on failure, leaves those rows unset. */
+ * Inf, m range) and, on failure, leaves those rows unset.  A device source is
+ * read after a device-wide synchronisation (it may be produced on any stream);
+ * the calls return once dst is written. */
 oocz_status oocz_set_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,
                                   const void* src, int32_t src_on_device);
 oocz_status oocz_get_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,

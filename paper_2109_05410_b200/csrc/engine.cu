@@ -671,6 +671,9 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
         return fail(ctx, OOCZ_EINVAL, "planes [%d, %d) outside [0, %d)", z0, z0 + nplanes, ctx->S);
     if (!src_v && nplanes) return fail(ctx, OOCZ_EINVAL, "null source");
     CK(cudaSetDevice(ctx->device));
+    // a device source may still be being written on a stream of the caller's
+    // (the copies below run on the library's own non-blocking stream)
+    if (on_device) CK(cudaDeviceSynchronize());
     // rows of this range count as unset until the call succeeds
     for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 0;
     ctx->field_set[field] = false;
