@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstddef>
+#include <atomic>
 
 #include "../../include/oocz.h"
 
@@ -30,11 +31,20 @@ inline const char* cuda_str(cudaError_t e) { return cudaGetErrorString(e); }
 // Once per kernel: allow `dyn_bytes` of dynamic shared memory, and (unless
 // built with OOCZ_CARVEOUT=0) ask for the largest shared-memory carveout, so
 // an SM configured for one of the pipeline's kernels can take another's CTA.
-inline cudaError_t kernel_smem_setup(const void* fn, int dyn_bytes)
+// Function attributes belong to a device's context: `done` holds one bit per
+// device already configured (setting them twice is harmless, so concurrent
+// first calls need no lock).
+inline cudaError_t kernel_smem_setup(const void* fn, int dyn_bytes, std::atomic<uint64_t>& done)
 {
-    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return cudaSuccess;
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_bytes);
     if (e == cudaSuccess && OOCZ_CARVEOUT)
         e = cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    if (e == cudaSuccess) done.fetch_or(bit, std::memory_order_acq_rel);
     return e;
 }
 

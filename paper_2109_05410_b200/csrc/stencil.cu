@@ -433,11 +433,10 @@ cudaError_t launch_stencil_step_t(const T* u, T* uprev, const T* m, int nx, int 
     if (!make_map(&mu, u + (size_t)zv0 * nx * ny, nx, ny, zv1 - zv0, KT::SW, KT::SH) ||
         !make_map(&mup, (const T*)uprev, nx, ny, nz, TX, KT::TY) || !make_map(&mm, m, nx, ny, nz, TX, KT::TY))
         return cudaErrorInvalidValue;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = kernel_smem_setup((const void*)stencil25_kernel<T>, (int)KT::kSmemBytes);
+    static std::atomic<uint64_t> attr_done{0};
+    {
+        cudaError_t e = kernel_smem_setup((const void*)stencil25_kernel<T>, (int)KT::kSmemBytes, attr_done);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     Coeffs<T> cf{(T)3 * c[0], c[1], c[2], c[3], c[4]};  // fl(3 c0) in T, as the oracle
     // persistent CTAs.  If the plane's tiles fit on the SMs, one CTA per tile

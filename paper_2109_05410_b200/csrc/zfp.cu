@@ -365,11 +365,10 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes());
+    static std::atomic<uint64_t> attr_done{0};
+    {
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes(), attr_done);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
     zfp_encode_kernel<<<(unsigned)grid, kThreads, encode_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
@@ -384,11 +383,10 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_decode_kernel, (int)decode_smem_bytes(64));
+    static std::atomic<uint64_t> attr_done{0};
+    {
+        cudaError_t e = kernel_smem_setup((const void*)zfp_decode_kernel, (int)decode_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
     zfp_decode_kernel<<<(unsigned)grid, kThreads, decode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
@@ -403,11 +401,10 @@ cudaError_t launch_zfp_encode64(const double* in, int nx, int ny, int nz, int ra
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_encode64_kernel, (int)encode64_smem_bytes());
+    static std::atomic<uint64_t> attr_done{0};
+    {
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode64_kernel, (int)encode64_smem_bytes(), attr_done);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const long long grid = (nblocks + kThreads - 1) / kThreads;
     zfp_encode64_kernel<<<(unsigned)grid, kThreads, encode64_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
@@ -422,11 +419,10 @@ cudaError_t launch_zfp_decode64(const uint64_t* in, int nx, int ny, int nz, int 
     if (!codec_args_ok(nx, ny, nz, rate)) return cudaErrorInvalidValue;
     const long long nblocks = (long long)(nx / 4) * (ny / 4) * (nz / 4);
     if (nblocks == 0) return cudaSuccess;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_decode64_kernel, (int)decode64_smem_bytes(64));
+    static std::atomic<uint64_t> attr_done{0};
+    {
+        cudaError_t e = kernel_smem_setup((const void*)zfp_decode64_kernel, (int)decode64_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const long long grid = (nblocks + kThreads - 1) / kThreads;
     zfp_decode64_kernel<<<(unsigned)grid, kThreads, decode64_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
