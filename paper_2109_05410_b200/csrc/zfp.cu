@@ -269,13 +269,18 @@ zfp_encode64_kernel(const double* __restrict__ in, int nx, int ny, int nbx, int 
     bw.finish(rate);
 }
 
-__global__ void __launch_bounds__(kThreads)
+// Two phases of 32 planes so that only 32 planes (32 KiB) are in shared memory
+// at a time: planes 63..32 are decoded and transposed into the high halves of
+// the 64 coefficients (kept in registers), then planes 31..0 reuse the same
+// shared memory.  65 KiB per CTA at rate 32, three CTAs per SM (the 64-plane
+// layout, 97 KiB, allowed two: the kernel is occupancy-limited).
+__global__ void __launch_bounds__(kThreads, 3)
 zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                     long long nblocks, int rate, double* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t smem[];   // planes [64][kThreads], then words
+    extern __shared__ __align__(16) uint64_t smem[];   // planes [32][kThreads], then words
     uint64_t* planes = smem;
-    uint64_t* words = smem + 64 * kThreads;            // [kThreads][rate + 1] + 1 spare
+    uint64_t* words = smem + 32 * kThreads;            // [kThreads][rate + 1] + 1 spare
     const int t = threadIdx.x;
     const int stride = rate + 1;
     const long long b0 = (long long)blockIdx.x * kThreads;
@@ -306,46 +311,53 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
         return;
     }
     const int emax = (int)br.read(zb::kEBits64) - 1023;
-    zb::decode_planes([&](int k, uint64_t x) { planes[k * kThreads + t] = x; },
-                      64 * rate - zb::kHeaderBits64, br, 63);
-    uint64_t u[64];
-    {
+    uint64_t* pl = planes + t;
+    zb::DecState st{63, 0, 64 * rate - zb::kHeaderBits64, false, 0u, 0u};
+    uint32_t hi[64];                                   // bits 32..63 of the 64 coefficients
+#pragma unroll
+    for (int half = 1; half >= 0; half--) {
+        const int kmin = 32 * half;
+        auto set = [&](int k, uint64_t x) { pl[(k - kmin) * kThreads] = x; };
+        while (st.k >= kmin && st.bits >= 66) zb::decode_event_fast(st, br, set);
+        while (st.k >= kmin && st.active()) zb::decode_event(st, br, set);
+        for (; st.k >= kmin; --st.k) set(st.k, 0ull);      // planes past the budget
         uint32_t a[32], b[32];
 #pragma unroll
-        for (int half = 0; half < 2; half++) {
-#pragma unroll
-            for (int k = 0; k < 32; k++) {
-                const uint64_t x = planes[(32 * half + k) * kThreads + t];
-                a[k] = (uint32_t)x;
-                b[k] = (uint32_t)(x >> 32);
-            }
-            zb::transpose32(a);
-            zb::transpose32(b);
-#pragma unroll
-            for (int i = 0; i < 32; i++) {
-                if (half == 0) { u[i] = a[i]; u[i + 32] = b[i]; }
-                else { u[i] |= (uint64_t)a[i] << 32; u[i + 32] |= (uint64_t)b[i] << 32; }
-            }
+        for (int k = 0; k < 32; k++) {
+            const uint64_t x = pl[k * kThreads];
+            a[k] = (uint32_t)x;
+            b[k] = (uint32_t)(x >> 32);
         }
+        zb::transpose32(a);
+        zb::transpose32(b);
+        if (half == 1) {
+#pragma unroll
+            for (int i = 0; i < 32; i++) { hi[i] = a[i]; hi[i + 32] = b[i]; }
+            continue;
+        }
+        constexpr int perm[64] = OOCZ_PERM3;
+        int64_t q[64];
+#pragma unroll
+        for (int i = 0; i < 32; i++) {
+            const uint64_t u0 = ((uint64_t)hi[i] << 32) | a[i], u1 = ((uint64_t)hi[i + 32] << 32) | b[i];
+            q[perm[i]] = (int64_t)((u0 ^ zb::kNBMask64) - zb::kNBMask64);
+            q[perm[i + 32]] = (int64_t)((u1 ^ zb::kNBMask64) - zb::kNBMask64);
+        }
+        zb::inv_xform(q);
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+            for (int j = 0; j < 4; j++) {
+                const int l = 16 * k + 4 * j;
+                double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
+                row[0] = make_double2(zb::dequantize64(q[l], emax), zb::dequantize64(q[l + 1], emax));
+                row[1] = make_double2(zb::dequantize64(q[l + 2], emax), zb::dequantize64(q[l + 3], emax));
+            }
     }
-    constexpr int perm[64] = OOCZ_PERM3;
-    int64_t q[64];
-#pragma unroll
-    for (int i = 0; i < 64; i++) q[perm[i]] = (int64_t)((u[i] ^ zb::kNBMask64) - zb::kNBMask64);
-    zb::inv_xform(q);
-#pragma unroll
-    for (int k = 0; k < 4; k++)
-#pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const int l = 16 * k + 4 * j;
-            double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
-            row[0] = make_double2(zb::dequantize64(q[l], emax), zb::dequantize64(q[l + 1], emax));
-            row[1] = make_double2(zb::dequantize64(q[l + 2], emax), zb::dequantize64(q[l + 3], emax));
-        }
 }
 
 size_t encode64_smem_bytes() { return sizeof(uint64_t) * (size_t)(64 * kThreads); }
-size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(64 * kThreads + kThreads * (rate + 1) + 1); }
+size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * (rate + 1) + 1); }
 
 size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
 // the 64-bit stream window reads up to one word past a block's last word: the
