@@ -107,7 +107,7 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
     {
         const uint64_t* planes = smem;
         auto plane_at = [&](int k) { return planes[k * kThreads + t]; };
-        while (st[0].k >= 0 && st[0].bits >= 65) zb::encode_event<true>(st[0], plane_at, bw[0]);
+        while (st[0].k >= 0 && st[0].bits >= 65) zb::encode_event_merged(st[0], plane_at, bw[0]);
         while (st[0].active()) zb::encode_event(st[0], plane_at, bw[0]);
     }
 #pragma unroll
@@ -155,6 +155,7 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     {
         uint64_t* planes = planes_all + t;
         auto plane_set = [&](int k, uint64_t x) { planes[k * kThreads] = x; };
+        while (st[0].k >= 0 && st[0].bits >= 131) zb::decode_event_merged(st[0], br[0], plane_set);
         while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event_fast(st[0], br[0], plane_set);
         while (st[0].active()) zb::decode_event(st[0], br[0], plane_set);
     }
@@ -318,6 +319,7 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
     for (int half = 1; half >= 0; half--) {
         const int kmin = 32 * half;
         auto set = [&](int k, uint64_t x) { pl[(k - kmin) * kThreads] = x; };
+        while (st.k >= kmin && st.bits >= 131) zb::decode_event_merged(st, br, set);
         while (st.k >= kmin && st.bits >= 66) zb::decode_event_fast(st, br, set);
         while (st.k >= kmin && st.active()) zb::decode_event(st, br, set);
         for (; st.k >= kmin; --st.k) set(st.k, 0ull);      // planes past the budget
