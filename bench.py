@@ -379,7 +379,10 @@ def gpu_arm(args):
         PF = dict(serpentine=0, m_resident=0)
         modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
                  ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
-        if not args.quick:   # configs[1]: rates 8/16/24
+        # the single-GPU analyses (other rates, schedules, paper modes, fp64, T) run at
+        # N = 1; a multi-GPU run measures the headline paths only (each extra mode is
+        # another NCCL communicator and pinned store per rank)
+        if not args.quick and world == 1:   # configs[1]: rates 8/16/24
             modes += [(f"r{r}_{k}", st, (r,) * 3, o) for r in (8, 24) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
             # the paper-faithful schedule, and each orchestration alone
             modes += [("pf_zfp_dev", 1, (RATE,) * 3, PF), ("pf_zfp_host", 0, (RATE,) * 3, PF),

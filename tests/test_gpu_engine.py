@@ -326,3 +326,15 @@ def test_c2_full_size_bench_configs_bit_exact(c2_state, store, opts):
         gu, gup = s.get(z.OOCZ_U), s.get(z.OOCZ_UPREV)
     assert np.array_equal(bits(gu), bits(ou))
     assert np.array_equal(bits(gup), bits(oup))
+
+
+@pytest.mark.parametrize("store", [0, 1])
+def test_extreme_rates(store):
+    """Rate 1 (the smallest: 8 bytes per 4^3 block) and rate 64 (more bits than
+    the raw value) through the whole stepper, mixed with raw."""
+    nx, ny, nz, T, P = 32, 16, 48, 2, 16
+    u, up, m = _fields(nx, ny, nz, 9)
+    for rates in ((1, 64, 0), (64, 1, 2)):
+        gu, gup, _, _ = _run_gpu(u, up, m, T, P, rates, store, [6], serpentine=1, m_resident=1, slots=3)
+        ou, oup = _run_oracle(u, up, m, T, rates, [6])
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), rates

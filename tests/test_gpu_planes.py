@@ -82,3 +82,20 @@ def test_plane_range_errors_and_partial_state():
             z.oocz_step(s.ctx, 2)
         z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, u[16:24])
         z.oocz_step(s.ctx, 2)
+
+
+def test_chunked_set_fp64():
+    """The paper's precision through the plane-range calls."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 24, 20, 48, 2, 16, (32, 24, 40)
+    u, up, m = (a.astype(np.float64) for a in _fields(nx, ny, nz))
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), precision=64)
+    with z.Stepper(cfg) as s:
+        for z0 in range(0, nz, 8):
+            for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                z.oocz_set_field_planes(s.ctx, f, z0, a[z0:z0 + 8])
+        s.step(5)
+        got = np.concatenate([z.oocz_get_field_planes(s.ctx, z.OOCZ_U, z0, np.empty((8, ny, nx), np.float64))
+                              for z0 in range(0, nz, 8)])
+    want, _ = oracle.run64(u, up, m, T, rates, 5)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64))
