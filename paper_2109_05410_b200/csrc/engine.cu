@@ -427,15 +427,20 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     // memory plan and budget check
     const size_t pb = ctx->pb;
     // slab sets (m is not streamed into them when it is resident) + the C_i copy
-    const int slab_fields = cfg->m_resident ? 2 : 3;
-    size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb + 3 * (size_t)(2 * h) * pb;
+    const int slab_fields = cfg->m_resident ? 2 : 3;    // also the streamed fields
+    size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb + slab_fields * (size_t)(2 * h) * pb;
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
     if (host) {
-        for (int f = 0; f < 3; f++) {
+        // an input slot holds one read unit of each streamed field; set_field /
+        // get_field also stage P planes of any one field through slot 0
+        size_t one_field = 0;
+        for (int f = 0; f < slab_fields; f++) {
             ctx->in_off[f] = ctx->in_slot_bytes;
             ctx->in_slot_bytes += (size_t)(rd_max_planes / 4) * ctx->row_bytes[f];
         }
+        for (int f = 0; f < 3; f++) one_field = std::max(one_field, (size_t)(P / 4) * ctx->row_bytes[f]);
+        ctx->in_slot_bytes = std::max(ctx->in_slot_bytes, one_field);
         for (int f = 0; f < 2; f++) {
             ctx->out_off[f] = ctx->out_slot_bytes;
             ctx->out_slot_bytes += (size_t)(P / 4) * ctx->row_bytes[f];
@@ -460,7 +465,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             CKC(cudaMalloc(&ctx->slab[k][f], (size_t)ctx->L * pb));
             CKC(cudaMemset(ctx->slab[k][f], 0, (size_t)ctx->L * pb));
         }
-        CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
+        if (f < slab_fields) CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
     }
     CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
     if (cfg->m_resident) {

@@ -87,7 +87,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--sweeps", type=int, default=2)
     ap.add_argument("--samples", type=int, default=8)
-    ap.add_argument("--chunk", type=int, default=64)
+    ap.add_argument("--chunk", type=int, default=16)
     ap.add_argument("--schedules", default="paper_faithful,serpentine")
     args = ap.parse_args()
     nx = ny = args.nx
@@ -117,9 +117,14 @@ def main():
     pts = [(int(rng.integers(0, nx)), int(rng.integers(0, ny)), int(rng.integers(0, nz))) for _ in range(args.samples)]
     pts += [(3, 5, 1), (nx - 2, ny // 2, nz - 3)]          # next to the domain boundary
     nsteps = T * (args.warmup + args.sweeps)
-    for sched in args.schedules.split(","):
-        cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=[rate] * 3, store=Z.OOCZ_STORE_HOST,
-                                    serpentine=int(sched == "serpentine"), slots=2)
+    for spec in args.schedules.split(","):
+        # "name[:P]": paper_faithful, serpentine, or serpentine_mres (serpentine sweeps + m
+        # decoded once into HBM: 98 GiB at C3, so it needs a smaller P to fit)
+        sched, _, p_opt = spec.partition(":")
+        Pk = int(p_opt) if p_opt else P
+        cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=Pk, rate=[rate] * 3, store=Z.OOCZ_STORE_HOST,
+                                    serpentine=int(sched.startswith("serpentine")),
+                                    m_resident=int(sched.endswith("mres")), slots=2)
         t0 = time.time()
         ctx = Z.oocz_create(cfg)
         t_create = time.time() - t0
@@ -142,7 +147,7 @@ def main():
             h2d = st["h2d_bytes"] - s0["h2d_bytes"]
             d2h = st["d2h_bytes"] - s0["d2h_bytes"]
             cups = nx * ny * nz * T * args.sweeps / dev_s
-            run = {"cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
+            run = {"P": Pk, "cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
                    "h2d_bytes_per_sweep": h2d // args.sweeps, "d2h_bytes_per_sweep": d2h // args.sweeps,
                    "h2d_GBps": round(h2d / dev_s / 1e9, 2), "d2h_GBps": round(d2h / dev_s / 1e9, 2),
                    "device_bytes": st["device_bytes_used"], "pinned_host_bytes": st["host_bytes_pinned"],
@@ -171,7 +176,7 @@ def main():
                     print("MISMATCH", (x, y, zz), got, want, flush=True)
             run["sampled_parity"] = {"points": len(pts), "bit_exact": ok, "steps": nsteps,
                                      "oracle": f"oracle.run on the sub-box within {R} cells of each point"}
-            res["runs"][sched] = run
+            res["runs"][spec] = run
             print(sched, "parity", ok, "/", len(pts), flush=True)
         finally:
             Z.oocz_destroy(ctx)
