@@ -111,3 +111,38 @@ def test_impulse_response_matches_closed_form():
     z.oocz_stencil_step_planes(du, dup, dm, 16, 16, 16, z.default_coeffs(), 0, 16, 0, 16, None)
     torch.cuda.synchronize()
     assert np.array_equal(bits(dup.cpu().numpy()), bits(want))
+
+
+@pytest.mark.parametrize("shape,cone", [((1024, 304, 40), (4, 36, 0, 40)),   # 8 x 21 = 168 tiles > 148 SMs
+                                        ((512, 608, 28), (8, 20, 4, 24)),    # 4 x 41 tiles, ragged y
+                                        ((2048, 64, 20), (0, 20, 0, 20))])   # 16 x 5 = 80 tiles, one column each
+def test_chunked_persistent_schedule_bit_exact(shape, cone):
+    """More tiles than SMs: 148 persistent CTAs take (z chunk, tile) items in
+    chunk-major order (the schedule C3-sized planes use); fewer: one CTA per
+    tile column.  Both equal the oracle bit for bit, cone limits included."""
+    import torch
+    nx, ny, nz = shape
+    z0, z1, zv0, zv1 = cone
+    u, up, m = _state(nx, ny, nz, 12)
+    sub = oracle.step(u[zv0:zv1], up[zv0:zv1], m[zv0:zv1])
+    du, dup, dm = to_dev(u), to_dev(up), to_dev(m)
+    z = Z()
+    z.oocz_stencil_step_planes(du, dup, dm, nx, ny, nz, z.default_coeffs(), z0, z1, zv0, zv1,
+                               torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    got = dup.cpu().numpy()
+    assert np.array_equal(bits(got[z0:z1]), bits(sub[z0 - zv0:z1 - zv0]))
+    assert np.array_equal(bits(got[:z0]), bits(up[:z0])) and np.array_equal(bits(got[z1:]), bits(up[z1:]))
+
+
+def test_chunked_persistent_schedule_fp64():
+    import torch
+    nx, ny, nz = 1024, 160, 24                       # 8 x 20 = 160 tiles of 128 x 8 > 148
+    u, up, m = (a.astype(np.float64) for a in _state(nx, ny, nz, 13))
+    want = oracle.step_f64(u, up, m)
+    du, dup, dm = to_dev(u), to_dev(up), to_dev(m)
+    z = Z()
+    z.oocz_stencil_step_planes_f64(du, dup, dm, nx, ny, nz, z.default_coeffs64(), 0, nz, 0, nz,
+                                   torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(dup.cpu().numpy().view(np.uint64), want.view(np.uint64))
