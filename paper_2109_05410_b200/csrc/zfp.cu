@@ -62,7 +62,12 @@ __device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
     return p;
 }
 
-__global__ void __launch_bounds__(kThreads)
+// six CTAs per SM (<= 80 registers, 8 bytes of spill): more warps to hide the
+// latency of the block loads before the coder starts; measured 176 -> 168 us
+#ifndef OOCZ_ENC_MINB
+#define OOCZ_ENC_MINB 6
+#endif
+__global__ void __launch_bounds__(kThreads, OOCZ_ENC_MINB)
 zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, uint64_t* __restrict__ out)
 {
