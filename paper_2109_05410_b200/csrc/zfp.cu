@@ -24,6 +24,10 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int NB = 1;                       // blocks (event streams) per thread
 constexpr int kBlocksPerCTA = kThreads * NB;
+#ifndef OOCZ_DEC_THREADS
+#define OOCZ_DEC_THREADS 128
+#endif
+constexpr int kDecThreads = OOCZ_DEC_THREADS;       // fp32 decoder CTA size
 
 struct BlockPos { long long bx, by, bz; };
 
@@ -32,13 +36,14 @@ struct BlockPos { long long bx, by, bz; };
 // windows may touch): word w goes to words[(w / rate) (rate + 1) + w % rate].
 // The quotient and remainder advance with w instead of being recomputed (an
 // integer division per word was 7.5 % of the decoder's instructions).
+template <int NT>
 __device__ __forceinline__ void stage_words(uint64_t* words, const uint64_t* __restrict__ src, int total, int rate)
 {
     const int t = threadIdx.x;
-    const int dq = kThreads / rate, dr = kThreads - dq * rate;
+    const int dq = NT / rate, dr = NT - dq * rate;
     int q = t / rate, r = t - q * rate;
 #pragma unroll 4
-    for (int w = t; w < total; w += kThreads) {
+    for (int w = t; w < total; w += NT) {
         words[q * (rate + 1) + r] = __ldg(src + w);
         q += dq;
         r += dr;
@@ -146,17 +151,17 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         if (b0 + s * kThreads + t < nblocks) bw[s].finish(rate);
 }
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kDecThreads)
 zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, float* __restrict__ out)
 {
-    __shared__ uint64_t planes_all[NB * 32 * kThreads];   // [NB][32][kThreads]
-    extern __shared__ __align__(16) uint64_t words[];      // [NB*kThreads][rate + 1] + 1 spare
+    __shared__ uint64_t planes_all[NB * 32 * kDecThreads];   // [NB][32][kDecThreads]
+    extern __shared__ __align__(16) uint64_t words[];      // [NB*kDecThreads][rate + 1] + 1 spare
     const int t = threadIdx.x;
     const int stride = rate + 1;
-    const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
-    const long long nb = nblocks - b0 < kBlocksPerCTA ? nblocks - b0 : kBlocksPerCTA;
-    stage_words(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
+    const long long b0 = (long long)blockIdx.x * kDecThreads;
+    const long long nb = nblocks - b0 < kDecThreads ? nblocks - b0 : kDecThreads;
+    stage_words<kDecThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
     __syncthreads();
 
     zb::BitReader br[NB];
@@ -165,7 +170,7 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     bool zero[NB];
 #pragma unroll
     for (int s = 0; s < NB; s++) {
-        const int bb = s * kThreads + t;
+        const int bb = s * kDecThreads + t;
         br[s] = zb::BitReader{words + (size_t)bb * stride, 0};
         st[s] = zb::DecState{-1, 0, 0, false, 0u, 0u};
         emax[s] = 0;
@@ -178,14 +183,14 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
     }
     {
         uint64_t* planes = planes_all + t;
-        auto plane_set = [&](int k, uint64_t x) { planes[k * kThreads] = x; };
+        auto plane_set = [&](int k, uint64_t x) { planes[k * kDecThreads] = x; };
         while (st[0].k >= 0 && st[0].bits >= 131) zb::decode_event_merged(st[0], br[0], plane_set);
         while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event_fast(st[0], br[0], plane_set);
         while (st[0].active()) zb::decode_event(st[0], br[0], plane_set);
     }
 #pragma unroll
     for (int s = 0; s < NB; s++) {
-        const int bb = s * kThreads + t;
+        const int bb = s * kDecThreads + t;
         if (bb >= nb) continue;
         const BlockPos p = block_pos(b0 + bb, nbx, nby);
         float* base = out + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
@@ -197,12 +202,12 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
                     *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) = make_float4(0.f, 0.f, 0.f, 0.f);
             continue;
         }
-        uint64_t* planes = planes_all + s * 32 * kThreads;
-        for (int k = st[s].k; k >= 0; --k) planes[k * kThreads + t] = 0ull;   // planes past the budget
+        uint64_t* planes = planes_all + s * 32 * kDecThreads;
+        for (int k = st[s].k; k >= 0; --k) planes[k * kDecThreads + t] = 0ull;   // planes past the budget
         uint32_t lo[32], hi[32];
 #pragma unroll
         for (int k = 0; k < 32; k++) {
-            const uint64_t x = planes[k * kThreads + t];
+            const uint64_t x = planes[k * kDecThreads + t];
             lo[k] = (uint32_t)x;
             hi[k] = (uint32_t)(x >> 32);
         }
@@ -310,7 +315,7 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
     const int stride = rate + 1;
     const long long b0 = (long long)blockIdx.x * kThreads;
     const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
-    stage_words(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
+    stage_words<kThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
     if (t == 0) words[nb * stride] = 0ull;
     __syncthreads();
     if (t >= nb) return;
@@ -381,7 +386,7 @@ size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(32 * k
 size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
 // the 64-bit stream window reads up to one word past a block's last word: the
 // row padding, and one spare word after the last row
-size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(kBlocksPerCTA * (rate + 1) + 1); }
+size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(kDecThreads * (rate + 1) + 1); }
 
 bool codec_args_ok(int nx, int ny, int nz, int rate) {
     return nx >= 0 && ny >= 0 && nz >= 0 && nx % 4 == 0 && ny % 4 == 0 && nz % 4 == 0 &&
@@ -419,8 +424,8 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
         cudaError_t e = kernel_smem_setup((const void*)zfp_decode_kernel, (int)decode_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
     }
-    const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
-    zfp_decode_kernel<<<(unsigned)grid, kThreads, decode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
+    const long long grid = (nblocks + kDecThreads - 1) / kDecThreads;
+    zfp_decode_kernel<<<(unsigned)grid, kDecThreads, decode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
                                                                                nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
