@@ -120,11 +120,13 @@ def main():
     for spec in args.schedules.split(","):
         # "name[:P]": paper_faithful, serpentine, or serpentine_mres (serpentine sweeps + m
         # decoded once into HBM: 98 GiB at C3, so it needs a smaller P to fit)
-        sched, _, p_opt = spec.partition(":")
-        Pk = int(p_opt) if p_opt else P
+        parts = spec.split(":")                  # name[:P[:slots]]
+        sched = parts[0]
+        Pk = int(parts[1]) if len(parts) > 1 else P
+        slots = int(parts[2]) if len(parts) > 2 else 2
         cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=Pk, rate=[rate] * 3, store=Z.OOCZ_STORE_HOST,
                                     serpentine=int(sched.startswith("serpentine")),
-                                    m_resident=int(sched.endswith("mres")), slots=2)
+                                    m_resident=int(sched.endswith("mres")), slots=slots)
         t0 = time.time()
         ctx = Z.oocz_create(cfg)
         t_create = time.time() - t0
@@ -147,7 +149,7 @@ def main():
             h2d = st["h2d_bytes"] - s0["h2d_bytes"]
             d2h = st["d2h_bytes"] - s0["d2h_bytes"]
             cups = nx * ny * nz * T * args.sweeps / dev_s
-            run = {"P": Pk, "cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
+            run = {"P": Pk, "slots": slots, "cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
                    "h2d_bytes_per_sweep": h2d // args.sweeps, "d2h_bytes_per_sweep": d2h // args.sweeps,
                    "h2d_GBps": round(h2d / dev_s / 1e9, 2), "d2h_GBps": round(d2h / dev_s / 1e9, 2),
                    "device_bytes": st["device_bytes_used"], "pinned_host_bytes": st["host_bytes_pinned"],
