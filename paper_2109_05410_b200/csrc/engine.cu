@@ -500,7 +500,19 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         if (sp && sp[0] == '1') CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_dec, cudaStreamNonBlocking, lo));
+        // The encode runs on the compute stream.  A separate encode stream (so the
+        // next block's stencil overlaps this block's encode) measured 1.4 % faster
+        // but showed rare wrong results (tests/test_gpu_engine.py
+        // test_random_configurations_bit_exact; tools/stress_case*.py): ~1 in 3 runs
+        // of a 40x16x80 grid with rates (64, 3, 12) and m streamed, the first
+        // block-row of a block's u at t+T wrong, u- right, although every stage
+        // ordering in the profile holds.  Root cause not found; the knob stays for
+        // the investigation (-DOOCZ_SEPARATE_ENCODE_STREAM).
+#ifdef OOCZ_SEPARATE_ENCODE_STREAM
         CKC(cudaStreamCreateWithPriority(&ctx->s_enc, cudaStreamNonBlocking, lo));
+#else
+        ctx->s_enc = ctx->s_comp;
+#endif
     }
     for (int k = 0; k < ctx->nsets; k++) {
         CKC(cudaEventCreateWithFlags(&ctx->ev_decoded[k], cudaEventDisableTiming));
@@ -620,7 +632,7 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         if (e) cudaEventDestroy(e);
     if (ctx->s_h2d) cudaStreamDestroy(ctx->s_h2d);
     if (ctx->s_comp) cudaStreamDestroy(ctx->s_comp);
-    if (ctx->s_enc) cudaStreamDestroy(ctx->s_enc);
+    if (ctx->s_enc && ctx->s_enc != ctx->s_comp) cudaStreamDestroy(ctx->s_enc);
     if (ctx->ev_join_enc) cudaEventDestroy(ctx->ev_join_enc);
     if (ctx->s_dec) cudaStreamDestroy(ctx->s_dec);
     for (int k = 0; k < oocz_ctx::kMaxSets; k++) {
@@ -1112,6 +1124,14 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         CK(cudaEventRecord(ctx->ev_written[i], se));
         CK(cudaEventRecord(ctx->ev_encoded[i], se));
     }
+#ifdef OOCZ_DEBUG_SERIAL_ENC      // debugging: the next stencil waits for this encode
+    CK(cudaEventRecord(ctx->ev_join_enc, se));
+    CK(cudaStreamWaitEvent(sc, ctx->ev_join_enc, 0));
+#endif
+#ifdef OOCZ_DEBUG_SERIAL_DEC      // debugging: the next decode waits for this encode
+    CK(cudaEventRecord(ctx->ev_join_enc, se));
+    CK(cudaStreamWaitEvent(sd, ctx->ev_join_enc, 0));
+#endif
     ctx->seq++;
     return OOCZ_OK;
 }

@@ -96,7 +96,11 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         for (int k = 0; k < 4; k++)
 #pragma unroll
             for (int j = 0; j < 4; j++) {
+#ifdef OOCZ_DEBUG_LDCG
+                const float4 f = __ldcg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+#else
                 const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+#endif
                 v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
                 v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
                 v[16 * k + 4 * j + 2] = __float_as_uint(f.z);

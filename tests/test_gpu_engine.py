@@ -338,3 +338,27 @@ def test_extreme_rates(store):
         gu, gup, _, _ = _run_gpu(u, up, m, T, P, rates, store, [6], serpentine=1, m_resident=1, slots=3)
         ou, oup = _run_oracle(u, up, m, T, rates, [6])
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), rates
+
+
+def test_random_configurations_bit_exact():
+    """96 seeded random configurations of everything the stepper accepts --
+    grid shape, T, P, per-field rates (raw to 64), store location, slots,
+    slab sets, serpentine, m resident, split calls -- against the oracle."""
+    rng = np.random.default_rng(2024)
+    for case in range(96):
+        T = int(rng.integers(1, 4))
+        h = 4 * T
+        P = int(rng.choice([q for q in (8, 12, 16, 20, 24, 32) if q >= 2 * h]))
+        D = int(rng.integers(1, 5))
+        nz = P * D
+        nx, ny = 4 * int(rng.integers(2, 12)), 4 * int(rng.integers(1, 8))
+        rates = tuple(int(rng.choice([0, 1, 3, 8, 12, 16, 24, 33, 64])) for _ in range(3))
+        store = int(rng.integers(0, 2))
+        opts = dict(slots=int(rng.integers(2, 5)), slab_sets=int(rng.choice([0, 2, 3, 4])),
+                    serpentine=int(rng.integers(0, 2)), m_resident=int(rng.integers(0, 2)))
+        calls = [int(x) for x in rng.integers(1, 3 * T + 2, size=int(rng.integers(1, 4)))]
+        u, up, m = _fields(nx, ny, nz, 100 + case)
+        gu, gup, _, _ = _run_gpu(u, up, m, T, P, rates, store, calls, **opts)
+        ou, oup = _run_oracle(u, up, m, T, rates, calls)
+        cfg = (nx, ny, nz, T, P, rates, store, opts, calls)
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), cfg
