@@ -16,9 +16,10 @@
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
-//    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
-//    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
-//    bound) run while block i's stencil (HBM bound) does.
+//    compute (stencil, then encode; `se` aliases the compute stream unless
+//    built with OOCZ_SEPARATE_ENCODE_STREAM), d2h.  Blocks rotate through
+//    `slab_sets` slab sets, so the decode of block i+1 (integer-ALU bound) runs
+//    while block i's stencil (HBM bound) does.
 //
 // Device-side data layout (per rank):
 //   slab[s][f]: `slab_sets` sets (blocks rotate through them; default 2) of
@@ -1075,7 +1076,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     }
 
     // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-, on
-    // the encode stream: the next block's stencil need not wait for it
+    // the encode stream `se` (the compute stream itself by default)
     CK(cudaEventRecord(ctx->ev_stepped[set], sc));
     CK(cudaStreamWaitEvent(se, ctx->ev_stepped[set], 0));
     const uint8_t* own[2] = {cu + (size_t)h * pb, cp + (size_t)h * pb};

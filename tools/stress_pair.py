@@ -12,6 +12,9 @@ from paper_2109_05410_b200 import synth  # noqa: E402
 nx, ny, L = 40, 16, 36
 u = synth.dense(nx, ny, L, seed=3); up = (u * np.float32(0.7)).astype(np.float32); m = synth.layered(nx, ny, L)
 want_st = oracle.step(u[0:28], up[0:28], m[0:28])
+# two cone-limited steps as the engine runs them: step 1 on [4, 28) into up, step 2 on [8, 28) into u
+u1 = up.copy(); u1[4:28] = want_st[4:28]
+want2 = oracle.step(u1[0:28], u[0:28], m[0:28])
 e_in = synth.dense(nx, ny, 20, seed=9)
 want_e64 = oracle.zfp_encode(e_in, 64)
 want_e3 = oracle.zfp_encode(e_in, 3)
@@ -23,15 +26,17 @@ w3 = torch.empty(Z.oocz_zfp_bytes(nx, ny, 20, 3) // 8, dtype=torch.int64, device
 bad_s = bad_e = 0
 for rep in range(2000):
     dup = torch.from_numpy(up).cuda()
+    du2 = du.clone()
     w64.zero_(); w3.zero_()
     torch.cuda.synchronize()
     Z.oocz_zfp_encode(de, nx, ny, 20, 64, w64, s1)
     Z.oocz_zfp_encode(de, nx, ny, 20, 3, w3, s1)
-    Z.oocz_stencil_step_planes(du, dup, dm, nx, ny, L, Z.default_coeffs(), 4, 28, 0, 28, s2)
-    Z.oocz_stencil_step_planes(dup, du, dm, nx, ny, L, Z.default_coeffs(), 8, 28, 0, 28, s2) if False else None
+    Z.oocz_stencil_step_planes(du2, dup, dm, nx, ny, L, Z.default_coeffs(), 4, 28, 0, 28, s2)
+    Z.oocz_stencil_step_planes(dup, du2, dm, nx, ny, L, Z.default_coeffs(), 8, 28, 0, 28, s2)
     torch.cuda.synchronize()
-    got = dup.cpu().numpy()
-    if not np.array_equal(got[4:28].view(np.uint32), want_st[4:28].view(np.uint32)):
+    got = dup.cpu().numpy(); got2 = du2.cpu().numpy()
+    if not (np.array_equal(got[4:28].view(np.uint32), want_st[4:28].view(np.uint32)) and
+            np.array_equal(got2[8:28].view(np.uint32), want2[8:28].view(np.uint32))):
         bad_s += 1
     if not (np.array_equal(w64.cpu().numpy().view(np.uint64), want_e64) and
             np.array_equal(w3.cpu().numpy().view(np.uint64), want_e3)):
