@@ -16,10 +16,9 @@
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
-//    compute (stencil, then encode; `se` aliases the compute stream unless
-//    built with OOCZ_SEPARATE_ENCODE_STREAM), d2h.  Blocks rotate through
-//    `slab_sets` slab sets, so the decode of block i+1 (integer-ALU bound) runs
-//    while block i's stencil (HBM bound) does.
+//    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
+//    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
+//    bound) run while block i's stencil (HBM bound) does.
 //
 // Device-side data layout (per rank):
 //   slab[s][f]: `slab_sets` sets (blocks rotate through them; default 2) of
@@ -501,18 +500,14 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         if (sp && sp[0] == '1') CKC(cudaDeviceGetStreamPriorityRange(&lo, &hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_comp, cudaStreamNonBlocking, hi));
         CKC(cudaStreamCreateWithPriority(&ctx->s_dec, cudaStreamNonBlocking, lo));
-        // The encode runs on the compute stream.  A separate encode stream (so the
-        // next block's stencil overlaps this block's encode) measured 1.4 % faster
-        // but showed rare wrong results (tests/test_gpu_engine.py
-        // test_random_configurations_bit_exact; tools/stress_case*.py): ~1 in 3 runs
-        // of a 40x16x80 grid with rates (64, 3, 12) and m streamed, the first
-        // block-row of a block's u at t+T wrong, u- right, although every stage
-        // ordering in the profile holds.  Root cause not found; the knob stays for
-        // the investigation (-DOOCZ_SEPARATE_ENCODE_STREAM).
-#ifdef OOCZ_SEPARATE_ENCODE_STREAM
-        CKC(cudaStreamCreateWithPriority(&ctx->s_enc, cudaStreamNonBlocking, lo));
-#else
+        // The encode has its own stream, so the next block's stencil overlaps this
+        // block's encode (+1.5 %).  (-DOOCZ_ENCODE_ON_COMPUTE puts it back on the
+        // compute stream; the rare wrong results first blamed on this stream were
+        // a ring-slot race in the stencil, see stencil.cu "release discipline".)
+#ifdef OOCZ_ENCODE_ON_COMPUTE
         ctx->s_enc = ctx->s_comp;
+#else
+        CKC(cudaStreamCreateWithPriority(&ctx->s_enc, cudaStreamNonBlocking, lo));
 #endif
     }
     for (int k = 0; k < ctx->nsets; k++) {
@@ -1076,7 +1071,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     }
 
     // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-, on
-    // the encode stream `se` (the compute stream itself by default)
+    // the encode stream: the next block's stencil need not wait for it
     CK(cudaEventRecord(ctx->ev_stepped[set], sc));
     CK(cudaStreamWaitEvent(se, ctx->ev_stepped[set], 0));
     const uint8_t* own[2] = {cu + (size_t)h * pb, cp + (size_t)h * pb};

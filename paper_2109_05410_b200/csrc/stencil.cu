@@ -19,8 +19,9 @@
 //        data);
 //      - the u- and m tiles (128 x 15 each) into a 4-stage ring (161 KiB of
 //        shared memory in all, so a codec CTA fits next to it).
-//    full/empty mbarrier pairs per stage: consumers release a stage as soon as
-//    every consumer warp is done with it (no CTA-wide barrier per plane), so
+//    full/empty mbarrier pairs per stage: every consumer thread releases a
+//    stage once its own loads from it have returned (no CTA-wide barrier per
+//    plane; see "release discipline" below), so
 //    the producer stays 3 u planes / 3 u-,m planes ahead.
 //  * Persistent: one CTA per SM; work items (z chunk, tile) in chunk-major
 //    order, CTA b takes items b, b + G, ...: all CTAs stay in the same z chunk
@@ -168,19 +169,30 @@ __device__ __forceinline__ void x_pairs(const double* crow, const V4<double>& uc
     }
 }
 
-// Ring-slot release discipline: a shared-memory load (LDS) may still be in
-// flight when a later mbarrier.arrive is executed (ptxas does not wait for the
-// load's scoreboard before SYNCS.ARRIVE), and the producer's next TMA write
-// into the slot is not ordered after it -- a WAR race, measured on B200 as
-// rare wrong neighbours.  So every value read from a slot is first CONSUMED:
-// passed to an empty volatile asm, which forces the load to have returned, and
-// volatile asms keep their order relative to the arrive.
-__device__ __forceinline__ void consumed(float v) { asm volatile("" ::"f"(v)); }
-__device__ __forceinline__ void consumed(double v) { asm volatile("" ::"d"(v)); }
-template <class T> __device__ __forceinline__ void consumed(const V4<T>& v) {
-    consumed(v.v[0]); consumed(v.v[1]); consumed(v.v[2]); consumed(v.v[3]);
+// Ring-slot release discipline.  A shared-memory load (LDS) may still be in
+// flight when a later mbarrier.arrive issues: ptxas does not wait for a load's
+// scoreboard before SYNCS.ARRIVE unless the arrive depends on the loaded
+// register, and the producer's next TMA write into the slot is not ordered
+// after loads still in flight -- a write-after-read race, seen on B200 as rare
+// wrong neighbours (first in fp64 on ragged tiles; later, with 8-deep rings,
+// as wrong first planes of a segment on ragged tiles while a codec kernel ran
+// concurrently: the prologue's loads were released with no instruction
+// reading them -- an empty asm "use" emits no SASS).  So every release carries
+// a real data dependency on one register of every load from the slot: the
+// words are XORed into an accumulator (real instructions that wait for the
+// loads), ANDed with a kernel-parameter zero that ptxas cannot fold, OR-reduced
+// over the warp (REDUX reads every lane's value), and added to the barrier
+// address of the single arrive.
+__device__ __forceinline__ void dep_add(uint32_t& acc, float v) { acc ^= __float_as_uint(v); }
+__device__ __forceinline__ void dep_add(uint32_t& acc, double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    acc ^= (uint32_t)b ^ (uint32_t)(b >> 32);
 }
-
+// one register of each 16-B load behind a V4 (fp32: one load; fp64: two)
+template <class T> __device__ __forceinline__ void dep_add4(uint32_t& acc, const V4<T>& v) {
+    dep_add(acc, v.v[0]);
+    if (sizeof(T) == 8) dep_add(acc, v.v[2]);
+}
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -194,6 +206,12 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// a consumer thread's release of a ring slot: every consumer thread arrives
+// (the empty barriers count threads), at an address that depends on the
+// thread's own loads from the slot (acc, see dep_add; zero is 0 at run time)
+__device__ __forceinline__ void release_slot(uint64_t* bar, uint32_t acc, uint32_t zero) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar) + (acc & zero)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -234,7 +252,7 @@ template <class T>
 __global__ void __launch_bounds__(K<T>::kBoundThreads, 1)
 stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant__ CUtensorMap tm_up,
                  const __grid_constant__ CUtensorMap tm_m, T* __restrict__ uprev, int nx, int ny,
-                 int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs<T> cf)
+                 int z0, int z1, int chunk, int ntx, long tiles, int zv0, Coeffs<T> cf, uint32_t zero)
 {
     constexpr int TY = K<T>::TY, NU = K<T>::NU, NR = K<T>::NR, SW = K<T>::SW;
     constexpr int kUStage = K<T>::kUStage, kRStage = K<T>::kRStage, kConsumerWarps = K<T>::kConsumerWarps;
@@ -255,8 +273,8 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
     const long items = tiles * ((z1 - z0 + chunk - 1) / chunk);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NU; s++) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], kConsumerWarps); }
-        for (int s = 0; s < NR; s++) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], kConsumerWarps); }
+        for (int s = 0; s < NU; s++) { mbar_init(&ufull[s], 1); mbar_init(&uempty[s], 32 * kConsumerWarps); }
+        for (int s = 0; s < NR; s++) { mbar_init(&rfull[s], 1); mbar_init(&rempty[s], 32 * kConsumerWarps); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
@@ -312,10 +330,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             mbar_wait(&ufull[g % NU], (g / NU) & 1);
             return uring + (g % NU) * kUStage;
         };
-        auto release_u = [&](int p) {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&uempty[uslot(p)]);
-        };
+        auto release_u = [&](int p, uint32_t acc) { release_slot(&uempty[uslot(p)], acc, zero); };
 
         V4<T> q[9];
         // centres of planes zb-4 .. zb+3; a plane outside [zb, ze) is released as soon
@@ -325,7 +340,11 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
         for (int i = 0; i < 8; i++) {
             const int p = pfirst + i;
             q[i] = ld4(wait_u(p) + cidx);
-            if (p < zb || p >= ze) { consumed(q[i]); release_u(p); }
+            if (p < zb || p >= ze) {
+                uint32_t acc = 0;
+                dep_add4(acc, q[i]);
+                release_u(p, acc);
+            }
         }
 
         for (int z = zb; z < ze; z++) {
@@ -347,12 +366,27 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             const V4<T> uc = q[4];
             T ax[4][4];
             x_pairs(crow, uc, ax);
+            // the release depends on every load from slot z through the pair sums:
+            // ay[d][0] reads both y loads of distance d and ax[3][0] = xl + xr both x
+            // loads; fp64 loads each 4-cell vector in two halves, 64 apart, so also
+            // ay[d][2], and its x pairs come from four loads per half (ax[3] and ax[1])
+            uint32_t acc = 0;
 #pragma unroll
-            for (int d = 0; d < 4; d++)
+            for (int d = 0; d < 4; d++) dep_add(acc, ay[d][0]);
+            dep_add(acc, ax[3][0]);
+            if (sizeof(T) == 8) {
 #pragma unroll
-                for (int o = 0; o < 4; o++) { consumed(ax[d][o]); consumed(ay[d][o]); }
-            release_u(z);
-            if (z + 4 >= ze) { consumed(q[8]); release_u(z + 4); }
+                for (int d = 0; d < 4; d++) dep_add(acc, ay[d][2]);
+                dep_add(acc, ax[1][0]);
+                dep_add(acc, ax[3][2]);
+                dep_add(acc, ax[1][2]);
+            }
+            release_u(z, acc);
+            if (z + 4 >= ze) {
+                uint32_t acc8 = 0;
+                dep_add4(acc8, q[8]);
+                release_u(z + 4, acc8);
+            }
 
             T Lv[4];
 #pragma unroll
@@ -377,12 +411,13 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
             const V4<T> mv = ld4(rt + TX * TY + ridx);
             T res[4];
 #pragma unroll
-            for (int o = 0; o < 4; o++) {
-                res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
-                consumed(res[o]);
+            for (int o = 0; o < 4; o++) res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
+            {
+                uint32_t accr = 0;
+                dep_add4(accr, upv);
+                dep_add4(accr, mv);
+                release_slot(&rempty[g % NR], accr, zero);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&rempty[g % NR]);
             if (active) st4(uprev + (size_t)z * plane + col, res, gx, nx);
             // shift the queue (an unroll by 9 to rotate by renaming measured slower:
             // 9x the code, instruction-cache and register pressure)
@@ -462,7 +497,7 @@ cudaError_t launch_stencil_step_t(const T* u, T* uprev, const T* m, int nx, int 
     const long items = tiles * ((nzu + chunk - 1) / chunk);
     const int grid = (int)std::min<long>(kStencilCTAs, items);
     stencil25_kernel<T><<<grid, KT::kThreads, KT::kSmemBytes, s>>>(mu, mup, mm, uprev, nx, ny, z0, z1, chunk, ntx,
-                                                                   tiles, zv0, cf);
+                                                                   tiles, zv0, cf, 0u);
     note_launches(1);
     return cudaGetLastError();
 }
