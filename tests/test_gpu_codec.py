@@ -72,3 +72,20 @@ def test_round_trip_error_small_at_rate_24():
     f = synth.dense(64, 64, 64, seed=3)
     g = gpu_decode(gpu_encode(f, 24), f.shape, 24)
     assert np.abs(g - f).max() <= 1e-5 * np.abs(f).max()
+
+
+@pytest.mark.parametrize("seed", [21, 22])
+def test_random_shapes_and_rates_bit_exact(seed):
+    """Seeded random shapes (multiples of 4, ragged CTA counts) and rates 1..64:
+    streams and decoded fields bit-exact against the oracle."""
+    rng = np.random.default_rng(seed)
+    for case in range(12):
+        nx, ny, nz = (4 * int(rng.integers(1, 24)) for _ in range(3))
+        rate = int(rng.integers(1, 65))
+        f = synth.dense(nx, ny, nz, seed=300 + case) * np.float32(10.0 ** int(rng.integers(-30, 30)))
+        f = f.astype(np.float32)
+        want = oracle.zfp_encode(f, rate)
+        got = gpu_encode(f, rate)
+        assert np.array_equal(got, want), (nx, ny, nz, rate)
+        back = gpu_decode(got, f.shape, rate)
+        assert np.array_equal(bits(back), bits(oracle.zfp_decode(want, f.shape, rate))), (nx, ny, nz, rate)
