@@ -143,11 +143,11 @@ CASES64 = [
 ]
 
 
-def _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident=0, serpentine=0):
+def _run64_gpu(u, up, m, T, P, rates, store, calls, m_resident=0, serpentine=0, **kw):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
-                                precision=64, m_resident=m_resident, serpentine=serpentine)
+                                precision=64, m_resident=m_resident, serpentine=serpentine, **kw)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -239,3 +239,25 @@ def test_stencil_ring_release_stress(dtype):
             fn(du, dup, dm, nx, ny, nz, c, 0, nz, 0, nz, torch.cuda.current_stream())
             torch.cuda.synchronize()
             assert np.array_equal(dup.cpu().numpy(), want), (nx, ny, nz)
+
+
+def test_random_configurations64_bit_exact():
+    """48 seeded random configurations in the paper's precision (fp64, rates
+    raw / 1..64, every orchestration option) against the fp64 oracle."""
+    rng = np.random.default_rng(64)
+    for case in range(48):
+        T = int(rng.integers(1, 4))
+        P = int(rng.choice([q for q in (8, 12, 16, 20, 24) if q >= 8 * T]))
+        nz = P * int(rng.integers(1, 4))
+        nx, ny = 4 * int(rng.integers(2, 10)), 4 * int(rng.integers(1, 7))
+        rates = tuple(int(rng.choice([0, 1, 7, 16, 24, 32, 41, 64])) for _ in range(3))
+        store = int(rng.integers(0, 2))
+        kw = dict(slots=int(rng.integers(2, 4)), slab_sets=int(rng.choice([0, 3])))
+        serp, mres = int(rng.integers(0, 2)), int(rng.integers(0, 2))
+        calls = [int(x) for x in rng.integers(1, 3 * T + 2, size=int(rng.integers(1, 3)))]
+        u, up, m = _state64(nx, ny, nz, 500 + case)
+        gu, gup, _ = _run64_gpu(u, up, m, T, P, rates, store, calls, mres, serp, **kw)
+        ou, oup = _run64_oracle(u, up, m, T, rates, calls)
+        assert np.array_equal(b64(gu), b64(ou)) and np.array_equal(b64(gup), b64(oup)), \
+            (nx, ny, nz, T, P, rates, store, serp, mres, kw, calls)
+
