@@ -364,3 +364,39 @@ def test_random_configurations_bit_exact(seed):
         ou, oup = _run_oracle(u, up, m, T, rates, calls)
         cfg = (nx, ny, nz, T, P, rates, store, opts, calls)
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), cfg
+
+
+def test_random_partitioned_configurations_bit_exact():
+    """24 seeded random z-partitioned runs (in-process local group of 2-4 ranks,
+    compressed halos) with every orchestration option: equal to the oracle,
+    i.e. to world 1, bit for bit."""
+    z = Z()
+    rng = np.random.default_rng(4242)
+    for case in range(24):
+        world = int(rng.choice([2, 3, 4]))
+        T = int(rng.integers(1, 3))
+        P = int(rng.choice([q for q in (8, 12, 16) if q >= 8 * T]))
+        S = P * int(rng.integers(1, 3))
+        nz = S * world
+        nx, ny = 4 * int(rng.integers(2, 9)), 4 * int(rng.integers(1, 6))
+        rates = tuple(int(rng.choice([0, 3, 12, 16, 33])) for _ in range(3))
+        opts = dict(store=int(rng.integers(0, 2)), slots=int(rng.integers(2, 4)),
+                    slab_sets=int(rng.choice([0, 3])), serpentine=int(rng.integers(0, 2)),
+                    m_resident=int(rng.integers(0, 2)))
+        n = int(rng.integers(1, 3 * T + 2))
+        u, up, m = _fields(nx, ny, nz, 700 + case)
+        cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), **opts)
+        ctxs = z.oocz_create_local_group(cfg, world)
+        try:
+            for r, c in enumerate(ctxs):
+                for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                    z.oocz_set_field(c, f, a[r * S:(r + 1) * S])
+            z.oocz_step_local_group(ctxs, n)
+            gu = np.concatenate([z.oocz_get_field(c, z.OOCZ_U, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+            gup = np.concatenate([z.oocz_get_field(c, z.OOCZ_UPREV, np.empty((S, ny, nx), np.float32)) for c in ctxs])
+        finally:
+            for c in ctxs:
+                z.oocz_destroy(c)
+        ou, oup = _run_oracle(u, up, m, T, rates, [n])
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), \
+            (world, nx, ny, nz, T, P, rates, opts, n)
