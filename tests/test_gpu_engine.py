@@ -400,3 +400,20 @@ def test_random_partitioned_configurations_bit_exact():
         ou, oup = _run_oracle(u, up, m, T, rates, [n])
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), \
             (world, nx, ny, nz, T, P, rates, opts, n)
+
+
+@pytest.mark.parametrize("serpentine,m_resident", [(0, 0), (1, 1)])
+@pytest.mark.parametrize("rates", [(0, 0, 0), (16, 0, 16), (16, 16, 16)])
+def test_paper_decomposition_bit_exact(rates, serpentine, m_resident):
+    """The paper's own z decomposition (tests/golden/: 1152 interior planes,
+    8 divisions, T = 12) with a small x/y extent."""
+    from golden_io import keyvals
+    s, t = keyvals("paper_sec5_schedule.txt"), keyvals("paper_table1.txt")
+    nz, T = t["interior"], s["temporal_blocking"]
+    P = nz // s["divisions"]
+    nx, ny = 32, 24
+    u, up, m = _fields(nx, ny, nz, 77)
+    gu, gup, st, _ = _run_gpu(u, up, m, T, P, rates, 0, [2 * T], serpentine=serpentine, m_resident=m_resident)
+    ou, oup = _run_oracle(u, up, m, T, rates, [2 * T])
+    assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+    assert st["sweeps"] == 2

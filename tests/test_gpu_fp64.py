@@ -261,3 +261,20 @@ def test_random_configurations64_bit_exact():
         assert np.array_equal(b64(gu), b64(ou)) and np.array_equal(b64(gup), b64(oup)), \
             (nx, ny, nz, T, P, rates, store, serp, mres, kw, calls)
 
+
+
+@pytest.mark.parametrize("rates", [(32, 0, 0), (0, 0, 32), (24, 0, 24)])
+def test_paper_codes_in_paper_decomposition64(rates):
+    """The paper's four codes (uncompressed; one read-write
+    dataset at 32/64; the read-only dataset at 32/64; one read-write and the
+    read-only dataset at 24/64) in fp64, on the paper's z decomposition
+    (tests/golden/: 1152 planes, 8 divisions, T = 12) with a small x/y extent."""
+    from golden_io import keyvals
+    s, t = keyvals("paper_sec5_schedule.txt"), keyvals("paper_table1.txt")
+    nz, T = t["interior"], s["temporal_blocking"]
+    P = nz // s["divisions"]
+    nx, ny = 16, 12
+    u, up, m = _state64(nx, ny, nz, 5)
+    gu, gup, st = _run64_gpu(u, up, m, T, P, rates, 0, [2 * T])
+    ou, oup = _run64_oracle(u, up, m, T, rates, [2 * T])
+    assert np.array_equal(b64(gu), b64(ou)) and np.array_equal(b64(gup), b64(oup))
