@@ -79,10 +79,13 @@ typedef struct {
                               device: its compressed rows never cross the host link in between
                               (1/D of the traffic per sweep saved).  Orchestration beyond the
                               paper (R22).  Results identical.  */
-    int32_t  slab_sets;    /* device slab sets the blocks rotate through: 0 (= 2), 2, 3 or 4.
+    int32_t  slab_sets;    /* device slab sets the blocks rotate through: 0 (= 2), 1, 2, 3 or 4.
                               Each set is (P + 8T) planes per streamed field.  With more sets
                               block i+1 decodes and block i-1 encodes while block i runs its
-                              stencil (the encode has its own stream).  Results identical. */
+                              stencil (the encode has its own stream); with 1 those run one
+                              after another (least HBM: a compressed store that nearly fills
+                              the GPU, e.g. C3 with store = OOCZ_STORE_DEVICE).  Results
+                              identical.  Out of range: OOCZ_EINVAL. */
 } oocz_config;
 
 typedef struct {

@@ -18,7 +18,9 @@
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
 //    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
 //    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
-//    bound) run while block i's stencil (HBM bound) does.
+//    bound) run while block i's stencil (HBM bound) does.  One set serialises
+//    decode -> stencil -> encode on the device (the copies still overlap) and
+//    is for grids whose compressed store nearly fills HBM.
 //
 // Device-side data layout (per rank):
 //   slab[s][f]: `slab_sets` sets (blocks rotate through them; default 2) of
@@ -352,8 +354,8 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->store != OOCZ_STORE_HOST && cfg->store != OOCZ_STORE_DEVICE)
         BAD(OOCZ_EINVAL, "store (%d) unknown", cfg->store);
     if (cfg->store == OOCZ_STORE_HOST && cfg->slots < 2) BAD(OOCZ_EINVAL, "slots (%d) < 2", cfg->slots);
-    if (cfg->slab_sets != 0 && (cfg->slab_sets < 2 || cfg->slab_sets > 4))
-        BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 2, 3, 4}", cfg->slab_sets);
+    if (cfg->slab_sets < 0 || cfg->slab_sets > 4)
+        BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 1, 2, 3, 4}", cfg->slab_sets);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)

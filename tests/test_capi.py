@@ -53,7 +53,8 @@ def test_cfl_limit_default_coefficients(z):
     (dict(precision=64, block_planes=32), 1, 0, ""),
     (dict(slab_sets=3, block_planes=32), 1, 0, ""),
     (dict(slab_sets=5, block_planes=32), 1, -1, "slab_sets (5)"),
-    (dict(slab_sets=1, block_planes=32), 1, -1, "slab_sets (1)"),
+    (dict(slab_sets=1, block_planes=32), 1, 0, ""),
+    (dict(slab_sets=-1, block_planes=32), 1, -1, "slab_sets (-1)"),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)

@@ -252,7 +252,7 @@ def test_random_configurations64_bit_exact():
         nx, ny = 4 * int(rng.integers(2, 10)), 4 * int(rng.integers(1, 7))
         rates = tuple(int(rng.choice([0, 1, 7, 16, 24, 32, 41, 64])) for _ in range(3))
         store = int(rng.integers(0, 2))
-        kw = dict(slots=int(rng.integers(2, 4)), slab_sets=int(rng.choice([0, 3])))
+        kw = dict(slots=int(rng.integers(2, 4)), slab_sets=int(rng.choice([0, 1, 3])))
         serp, mres = int(rng.integers(0, 2)), int(rng.integers(0, 2))
         calls = [int(x) for x in rng.integers(1, 3 * T + 2, size=int(rng.integers(1, 3)))]
         u, up, m = _state64(nx, ny, nz, 500 + case)

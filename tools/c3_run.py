@@ -120,13 +120,18 @@ def main():
     for spec in args.schedules.split(","):
         # "name[:P]": paper_faithful, serpentine, or serpentine_mres (serpentine sweeps + m
         # decoded once into HBM: 98 GiB at C3, so it needs a smaller P to fit)
-        parts = spec.split(":")                  # name[:P[:slots]]
+        # "hbm[:P[:slots[:sets]]]": the whole compressed store in HBM (154.6 GB at
+        # rate 16) beside one slab set -- the 309 GB state stepped without the host link
+        parts = spec.split(":")                  # name[:P[:slots[:sets]]]
         sched = parts[0]
         Pk = int(parts[1]) if len(parts) > 1 else P
         slots = int(parts[2]) if len(parts) > 2 else 2
-        cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=Pk, rate=[rate] * 3, store=Z.OOCZ_STORE_HOST,
+        hbm = sched == "hbm"
+        sets = int(parts[3]) if len(parts) > 3 else (1 if hbm else 0)
+        cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=Pk, rate=[rate] * 3,
+                                    store=Z.OOCZ_STORE_DEVICE if hbm else Z.OOCZ_STORE_HOST,
                                     serpentine=int(sched.startswith("serpentine")),
-                                    m_resident=int(sched.endswith("mres")), slots=slots)
+                                    m_resident=int(sched.endswith("mres")), slots=slots, slab_sets=sets)
         t0 = time.time()
         ctx = Z.oocz_create(cfg)
         t_create = time.time() - t0
@@ -149,7 +154,8 @@ def main():
             h2d = st["h2d_bytes"] - s0["h2d_bytes"]
             d2h = st["d2h_bytes"] - s0["d2h_bytes"]
             cups = nx * ny * nz * T * args.sweeps / dev_s
-            run = {"P": Pk, "slots": slots, "cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
+            run = {"P": Pk, "slots": slots, "slab_sets": sets, "store": "device" if hbm else "host",
+                   "cell_updates_per_s": round(cups, 1), "s_per_sweep": round(dev_s / args.sweeps, 3),
                    "h2d_bytes_per_sweep": h2d // args.sweeps, "d2h_bytes_per_sweep": d2h // args.sweeps,
                    "h2d_GBps": round(h2d / dev_s / 1e9, 2), "d2h_GBps": round(d2h / dev_s / 1e9, 2),
                    "device_bytes": st["device_bytes_used"], "pinned_host_bytes": st["host_bytes_pinned"],
