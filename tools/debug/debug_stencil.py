@@ -1,6 +1,6 @@
 import os, sys
 import numpy as np, torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 from paper_2109_05410_b200 import oocz as Z
 n, planes = 64, 40
 u = torch.rand(planes, n, n, device="cuda"); up = u.clone(); m = torch.full_like(u, 0.1)

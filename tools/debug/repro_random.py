@@ -1,5 +1,5 @@
 import sys, os
-sys.path.insert(0, '/root/repo/tests'); sys.path.insert(0, '/root/repo')
+_R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))); sys.path.insert(0, os.path.join(_R, 'tests')); sys.path.insert(0, _R)
 os.chdir('/root/repo')
 import numpy as np
 import test_gpu_engine as E

@@ -3,7 +3,7 @@ kernel on another stream, against the oracle."""
 import os
 import sys
 import torch
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 import oracle  # noqa: E402
 from paper_2109_05410_b200 import oocz as Z  # noqa: E402
