@@ -2,9 +2,12 @@
 every function include/oocz.h declares, and its host-only calls (config
 validation, sizes, CFL bound) follow the contract."""
 import ctypes as C
+import os
 from fractions import Fraction
 
 import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -72,3 +75,29 @@ def test_default_config(z):
     import oracle
     assert list(cfg.c) == list(oracle.default_coeffs())
     assert cfg.precision == 32 and list(cfg.c64) == list(oracle.C64)
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No fallback: without the CUDA library the binding refuses to import."""
+    import subprocess
+    import sys
+    env = dict(os.environ, OOCZ_LIB=str(tmp_path / "absent.so"))
+    r = subprocess.run([sys.executable, "-c", "import paper_2109_05410_b200.oocz"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=120)
+    assert r.returncode != 0 and "not built" in r.stderr
+
+
+def test_product_never_touches_the_oracle():
+    """The package (the product path) imports nothing from oracle/ (test
+    infrastructure only) and links nothing from it."""
+    import glob
+    import re
+    pkg = os.path.join(ROOT, "paper_2109_05410_b200")
+    files = glob.glob(os.path.join(pkg, "*.py")) + glob.glob(os.path.join(pkg, "csrc", "*"))
+    assert files
+    for f in files:
+        if f.endswith(".so") or f.endswith(".o"):
+            continue
+        src = open(f, errors="replace").read()
+        assert not re.search(r"^\s*(import|from)\s+oracle", src, re.M), f
+        assert "liboracle" not in src and "oracle.h" not in src, f
