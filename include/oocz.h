@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OOCZ_ABI_VERSION 3
+#define OOCZ_ABI_VERSION 4
 
 typedef enum {
     OOCZ_OK = 0,
@@ -86,6 +86,12 @@ typedef struct {
                               after another (least HBM: a compressed store that nearly fills
                               the GPU, e.g. C3 with store = OOCZ_STORE_DEVICE).  Results
                               identical.  Out of range: OOCZ_EINVAL. */
+    int32_t  graphs;       /* 1: replay each oocz_step's sweeps as a captured CUDA graph (built
+                              on the first call with that nsteps, cached per context, chunks of
+                              at most 16 sweeps).  Takes effect with store = OOCZ_STORE_DEVICE,
+                              world = 1, profile = 0 and serpentine = 0; otherwise ignored.  For
+                              launch-bound small grids.  Results identical.  0 or 1, else
+                              OOCZ_EINVAL. */
 } oocz_config;
 
 typedef struct {

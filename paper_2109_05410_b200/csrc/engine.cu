@@ -39,6 +39,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -182,6 +183,11 @@ struct oocz_ctx {
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr, ev_join_h2d = nullptr, ev_join_comp = nullptr;
     std::vector<oocz_event> events;
     oocz_stats stats{};
+    // CUDA graphs (cfg.graphs): one executable graph per chunk length in steps
+    struct Graph { cudaGraphExec_t exec; uint64_t launches; int sweeps; };
+    std::map<int64_t, Graph> graph_cache;
+    bool capturing = false;                 // inside a capture: slab sets by block index
+    cudaEvent_t ev_g_fork = nullptr, ev_g_join[4] = {};
 };
 
 namespace {
@@ -356,6 +362,7 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->store == OOCZ_STORE_HOST && cfg->slots < 2) BAD(OOCZ_EINVAL, "slots (%d) < 2", cfg->slots);
     if (cfg->slab_sets < 0 || cfg->slab_sets > 4)
         BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 1, 2, 3, 4}", cfg->slab_sets);
+    if (cfg->graphs != 0 && cfg->graphs != 1) BAD(OOCZ_EINVAL, "graphs (%d) must be 0 or 1", cfg->graphs);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
@@ -520,6 +527,8 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_enc, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_dec, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&ctx->ev_g_fork, cudaEventDisableTiming));
+    for (auto& e : ctx->ev_g_join) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
     const int nslots = host ? cfg->slots : 1;
     auto mk = [&](std::vector<cudaEvent_t>& v, int n) -> cudaError_t {
@@ -640,6 +649,10 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     }
     if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->ev_join_dec) cudaEventDestroy(ctx->ev_join_dec);
+    for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.exec);
+    if (ctx->ev_g_fork) cudaEventDestroy(ctx->ev_g_fork);
+    for (auto e : ctx->ev_g_join)
+        if (e) cudaEventDestroy(e);
     if (ctx->s_d2h) cudaStreamDestroy(ctx->s_d2h);
     delete ctx;
 }
@@ -937,8 +950,10 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
     // slab set: blocks rotate through nsets; with serpentine sweeps by block
-    // index, so a turnaround block finds its own slab (and its decoded m) again
-    const int set = ctx->cfg.serpentine ? i % ctx->nsets : (int)(ctx->seq % ctx->nsets);
+    // index, so a turnaround block finds its own slab (and its decoded m) again;
+    // in a graph capture by block
+    // index too (a captured graph must not depend on the call's block count)
+    const int set = ctx->cfg.serpentine || ctx->capturing ? i % ctx->nsets : (int)(ctx->seq % ctx->nsets);
     // m_resident: m is read in place from the decoded copy, never streamed
     const int nf = ctx->m_full ? 2 : 3;
     uint8_t* slab[3] = {ctx->slab[set][0], ctx->slab[set][1],
@@ -1202,6 +1217,91 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
     return OOCZ_OK;
 }
 
+// ---- CUDA graphs (cfg.graphs).  A chunk of up to kGraphSweeps sweeps is
+// captured once per length in steps and replayed on the decode stream.  The
+// capture forks every stream from the decode stream, re-records every event the
+// blocks wait on at the fork (so the graph depends on nothing outside itself)
+// and joins all streams back at the end; consecutive replays are ordered by the
+// decode stream, so sweep k+1 of the next chunk starts after the whole chunk.
+// The enqueued work is exactly the eager path's (enqueue_block), slab sets
+// chosen by block index.
+static constexpr int kGraphSweeps = 16;
+
+static bool graph_eligible(const oocz_ctx* c)
+{
+    return c->cfg.graphs && c->cfg.store == OOCZ_STORE_DEVICE && c->world == 1 && !c->halo && !c->cfg.profile &&
+           !c->cfg.serpentine;
+}
+
+static oocz_status capture_chunk(oocz_ctx* ctx, int64_t nsteps, int* sweeps)
+{
+    cudaStream_t o = ctx->s_dec;
+    cudaStream_t others[4] = {ctx->s_h2d, ctx->s_comp, ctx->s_enc, ctx->s_d2h};
+    CK(cudaEventRecord(ctx->ev_g_fork, o));
+    for (cudaStream_t s : others) CK(cudaStreamWaitEvent(s, ctx->ev_g_fork, 0));
+    for (int k = 0; k < ctx->nsets; k++) {
+        CK(cudaEventRecord(ctx->ev_decoded[k], o));
+        CK(cudaEventRecord(ctx->ev_slab_free[k], o));
+        CK(cudaEventRecord(ctx->ev_stepped[k], o));
+    }
+    for (int i = 0; i < ctx->D; i++) {
+        CK(cudaEventRecord(ctx->ev_encoded[i], o));
+        CK(cudaEventRecord(ctx->ev_written[i], o));
+    }
+    int64_t done = 0;
+    int sweep = 0;
+    while (done < nsteps) {
+        const int ts = (int)std::min<int64_t>(ctx->T, nsteps - done);
+        for (int i = 0; i < ctx->D; i++) {
+            oocz_status st = enqueue_block(ctx, sweep, i, ts, 1, false, false);
+            if (st != OOCZ_OK) return st;
+        }
+        done += ts;
+        sweep++;
+    }
+    for (int k = 0; k < 4; k++) {
+        CK(cudaEventRecord(ctx->ev_g_join[k], others[k]));
+        CK(cudaStreamWaitEvent(o, ctx->ev_g_join[k], 0));
+    }
+    *sweeps = sweep;
+    return OOCZ_OK;
+}
+
+static oocz_status run_graph_chunk(oocz_ctx* ctx, int64_t nsteps)
+{
+    auto it = ctx->graph_cache.find(nsteps);
+    if (it == ctx->graph_cache.end()) {
+        cudaStream_t o = ctx->s_dec;
+        const long long seq0 = ctx->seq;
+        const uint64_t l0 = g_launches.load();
+        CK(cudaStreamBeginCapture(o, cudaStreamCaptureModeRelaxed));
+        ctx->capturing = true;
+        int sweeps = 0;
+        oocz_status st = capture_chunk(ctx, nsteps, &sweeps);
+        ctx->capturing = false;
+        cudaGraph_t g = nullptr;
+        const cudaError_t e = cudaStreamEndCapture(o, &g);
+        ctx->seq = seq0;
+        const uint64_t launches = g_launches.load() - l0;
+        g_launches.fetch_sub(launches);          // captured, not launched: counted per replay
+        if (st != OOCZ_OK) {
+            if (g) cudaGraphDestroy(g);
+            return st;
+        }
+        if (e != cudaSuccess) return fail(ctx, OOCZ_ECUDA, "graph capture: %s", cudaGetErrorString(e));
+        cudaGraphExec_t x = nullptr;
+        const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
+        cudaGraphDestroy(g);
+        if (ei != cudaSuccess) return fail(ctx, OOCZ_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei));
+        it = ctx->graph_cache.emplace(nsteps, oocz_ctx::Graph{x, launches, sweeps}).first;
+    }
+    CK(cudaGraphLaunch(it->second.exec, ctx->s_dec));
+    note_launches(it->second.launches);
+    ctx->seq += (long long)it->second.sweeps * ctx->D;
+    ctx->stats.sweeps += (uint64_t)it->second.sweeps;
+    return OOCZ_OK;
+}
+
 // Enqueue all sweeps of every context in lockstep (one context unless this is
 // an in-process local group), then wait.
 static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
@@ -1217,6 +1317,15 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
     const int T = ctxs[0]->T;
     int64_t done = 0;
     int sweep = 0;
+    if (n == 1 && graph_eligible(ctxs[0])) {
+        const int64_t chunk = (int64_t)kGraphSweeps * T;
+        while (done < nsteps) {
+            const int64_t k = std::min<int64_t>(chunk, nsteps - done);
+            oocz_status st = run_graph_chunk(ctxs[0], k);
+            if (st != OOCZ_OK) return st;
+            done += k;
+        }
+    }
     while (done < nsteps) {
         const int ts = (int)std::min<int64_t>(T, nsteps - done);
         for (int r = 0; r < n; r++) {

@@ -417,3 +417,48 @@ def test_paper_decomposition_bit_exact(rates, serpentine, m_resident):
     ou, oup = _run_oracle(u, up, m, T, rates, [2 * T])
     assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
     assert st["sweeps"] == 2
+
+
+@pytest.mark.parametrize("slab_sets", [1, 2, 3])
+@pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES + [
+    (64, 64, 64, 2, 32, (16, 16, 16), [10, 10, 3, 10]),     # cached graphs reused, a partial sweep
+    (32, 32, 128, 1, 8, (12, 0, 8), [40]),                  # 40 sweeps: three chunks of <= 16
+])
+def test_graphs_bit_exact(nx, ny, nz, T, P, rates, calls, slab_sets):
+    """cfg.graphs = 1 (store in HBM): the captured-and-replayed sweeps give the
+    eager path's bits, call after call, and count the same kernel launches."""
+    u, up, m = _fields(nx, ny, nz, 11)
+    z = Z()
+    launches = []
+    outs = []
+    for graphs in (0, 1):
+        cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=1,
+                                    slab_sets=slab_sets, graphs=graphs)
+        with z.Stepper(cfg) as s:
+            s.set(u, up, m)
+            l0 = z.oocz_kernel_launch_count()
+            for n in calls:
+                s.step(n)
+            launches.append(z.oocz_kernel_launch_count() - l0)
+            st = s.stats()
+            outs.append((s.get(z.OOCZ_U), s.get(z.OOCZ_UPREV), st["sweeps"]))
+    ou, oup = _run_oracle(u, up, m, T, rates, calls)
+    for gu, gup, _ in outs:
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup))
+    assert outs[0][2] == outs[1][2] and launches[0] == launches[1]
+
+
+def test_graphs_ignored_where_not_eligible():
+    """Host store (or serpentine / profile): graphs = 1 falls back to the eager
+    path, same bits."""
+    nx, ny, nz, T, P, rates = 32, 24, 64, 2, 16, (16, 16, 16)
+    u, up, m = _fields(nx, ny, nz, 12)
+    z = Z()
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=0, graphs=1,
+                                serpentine=1, slots=3)
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        s.step(7)
+        gu = s.get(z.OOCZ_U)
+    ou, _ = _run_oracle(u, up, m, T, rates, [7])
+    assert np.array_equal(bits(gu), bits(ou))
