@@ -156,6 +156,7 @@ struct oocz_ctx {
     int nsets = 2;                          // slab sets in rotation (cfg.slab_sets, default 2)
     uint8_t* slab[kMaxSets][3] = {};
     uint8_t* ccopy[3] = {nullptr, nullptr, nullptr};
+    uint8_t* pcopy[2] = {nullptr, nullptr};  // parallelogram strip of u, u- (ascending sweeps)
     uint8_t* m_full = nullptr;              // m_resident: decoded m, planes [-h, S + h)
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
@@ -438,6 +439,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     // slab sets (m is not streamed into them when it is resident) + the C_i copy
     const int slab_fields = cfg->m_resident ? 2 : 3;    // also the streamed fields
     size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb + slab_fields * (size_t)(2 * h) * pb;
+    if (!cfg->serpentine) need += 2 * (size_t)h * pb;   // pcopy
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
     if (host) {
@@ -476,6 +478,8 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         }
         if (f < slab_fields) CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
     }
+    if (!cfg->serpentine)
+        for (auto& q : ctx->pcopy) CKC(cudaMalloc(&q, (size_t)h * pb));
     CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
     if (cfg->m_resident) {
         CKC(cudaMalloc(&ctx->m_full, (size_t)(S + 2 * h) * pb));
@@ -624,6 +628,7 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
     for (int f = 0; f < 3; f++) {
         for (int k = 0; k < oocz_ctx::kMaxSets; k++) cudaFree(ctx->slab[k][f]);
         cudaFree(ctx->ccopy[f]);
+        if (f < 2) cudaFree(ctx->pcopy[f]);
         if (ctx->cfg.store == OOCZ_STORE_HOST) cudaFreeHost(ctx->store[f]);
         else cudaFree(ctx->store[f]);
     }
@@ -1030,12 +1035,29 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     // ---- (a4) slab assembly on the decode stream, once this slab set is free
     CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
     const bool has_c = !turn && (dir > 0 ? i > 0 : i < D - 1);   // the shared region kept by the previous block
+    // Parallelogram tiling (sweeps without serpentine, reading R26): block i > 0
+    // updates [iP + 4(ts-s), (i+1)P + 4(ts-s)) in step s instead of the cone
+    // [iP - h + 4s, (i+1)P + h - 4s).  The planes below that it reads come at their
+    // last two time levels from block i-1 (pcopy, slab [h-4, h-4+4ts)), so of the
+    // time-t C_{i-1} only slab [h+4ts-4, 2h) of u, u- is needed.
+#ifdef OOCZ_CONE_ONLY             // A/B: the trapezoid cone everywhere
+    const bool para = false;
+#else
+    const bool para = !ctx->cfg.serpentine;
+#endif
+    const int c0 = para ? h + 4 * ts - 4 : 0;                     // first C plane needed (u, u-)
+    auto c_first = [&](int f) { return f == OOCZ_M ? 0 : c0; };
     if (has_c) {
         // ascending: C_{i-1} -> slab [0, 2h); descending: C_i -> slab [P, P+2h)
         const size_t dst = dir > 0 ? 0 : (size_t)P * pb;
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
-        for (int f = 0; f < nf; f++)
-            CK(cudaMemcpyAsync(slab[f] + dst, ctx->ccopy[f], (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
+        uint64_t cb = 0;
+        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(2 * h - c_first(f)) * pb;
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
+        for (int f = 0; f < nf; f++) {
+            const size_t o = (size_t)c_first(f) * pb;
+            CK(cudaMemcpyAsync(slab[f] + dst + o, ctx->ccopy[f] + o, (size_t)(2 * h - c_first(f)) * pb,
+                               cudaMemcpyDeviceToDevice, sd));
+        }
         prof_end(ctx, sd);
     }
     if (ctx->halo) {  // neighbour-rank halos received at the sweep start
@@ -1066,9 +1088,14 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     // ascending C_i = slab [P, P+2h), descending C_{i-1} = slab [0, 2h)
     if (dir > 0 ? i < D - 1 : i > 0) {
         const size_t off = dir > 0 ? (size_t)P * pb : 0;
-        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, nf * 2 * (uint64_t)(2 * h) * pb);
-        for (int f = 0; f < nf; f++)
-            CK(cudaMemcpyAsync(ctx->ccopy[f], slab[f] + off, (size_t)(2 * h) * pb, cudaMemcpyDeviceToDevice, sd));
+        uint64_t cb = 0;
+        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(2 * h - c_first(f)) * pb;
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
+        for (int f = 0; f < nf; f++) {
+            const size_t o = (size_t)c_first(f) * pb;
+            CK(cudaMemcpyAsync(ctx->ccopy[f] + o, slab[f] + off + o, (size_t)(2 * h - c_first(f)) * pb,
+                               cudaMemcpyDeviceToDevice, sd));
+        }
         prof_end(ctx, sd);
     }
     CK(cudaEventRecord(ctx->ev_decoded[set], sd));
@@ -1077,9 +1104,16 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     CK(cudaStreamWaitEvent(sc, ctx->ev_decoded[set], 0));
     uint8_t* cu = slab[OOCZ_U];
     uint8_t* cp = slab[OOCZ_UPREV];
+    const size_t strip = (size_t)(4 * ts) * pb;
+    if (para && i > 0) {          // block i-1's strip [iP-4, iP+4ts-4), both leapfrog buffers
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 4 * (uint64_t)strip);
+        CK(cudaMemcpyAsync(cu + (size_t)(h - 4) * pb, ctx->pcopy[0], strip, cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(cp + (size_t)(h - 4) * pb, ctx->pcopy[1], strip, cudaMemcpyDeviceToDevice, sc));
+        prof_end(ctx, sc);
+    }
     for (int s = 1; s <= ts; s++) {
-        const int z0 = std::max(4 * s, g.vlo);
-        const int z1 = std::min(ctx->L - 4 * s, g.vhi);
+        const int z0 = !para ? std::max(4 * s, g.vlo) : i == 0 ? std::max(4 * s, g.vlo) : h + 4 * (ts - s);
+        const int z1 = std::min(para ? P + h + 4 * (ts - s) : ctx->L - 4 * s, g.vhi);
         // algorithmic bytes: read u, u-, m and write u+ once per updated cell
         prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 4ull * (uint64_t)std::max(z1 - z0, 0) * pb);
         CK(stencil_step(ctx, cu, cp, slab[OOCZ_M], z0, z1, g.vlo, g.vhi, sc));
@@ -1087,8 +1121,17 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         std::swap(cu, cp);
     }
 
+    if (para && i < D - 1) {      // the strip [(i+1)P-4, (i+1)P+4ts-4) for block i+1
+        prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 4 * (uint64_t)strip);
+        CK(cudaMemcpyAsync(ctx->pcopy[0], slab[OOCZ_U] + (size_t)(P + h - 4) * pb, strip, cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(ctx->pcopy[1], slab[OOCZ_UPREV] + (size_t)(P + h - 4) * pb, strip,
+                           cudaMemcpyDeviceToDevice, sc));
+        prof_end(ctx, sc);
+    }
+
     // ---- (a6) encode own planes [iP, (i+1)P) = slab [h, P + h) of u, u-, on
-    // the encode stream: the next block's stencil need not wait for it
+    // the encode stream: the next block's stencil need not wait for it (the
+    // slab is free once the strip above is copied out)
     CK(cudaEventRecord(ctx->ev_stepped[set], sc));
     CK(cudaStreamWaitEvent(se, ctx->ev_stepped[set], 0));
     const uint8_t* own[2] = {cu + (size_t)h * pb, cp + (size_t)h * pb};
