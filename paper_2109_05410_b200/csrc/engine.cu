@@ -157,6 +157,8 @@ struct oocz_ctx {
     uint8_t* slab[kMaxSets][3] = {};
     uint8_t* ccopy[3] = {nullptr, nullptr, nullptr};
     uint8_t* pcopy[2] = {nullptr, nullptr};  // parallelogram strip of u, u- (ascending sweeps)
+    bool para = false;                      // parallelogram tiles (reading R26)
+    int cbase[3] = {0, 0, 0};               // first C plane ccopy[f] holds (h for u, u- with para)
     uint8_t* m_full = nullptr;              // m_resident: decoded m, planes [-h, S + h)
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
@@ -438,8 +440,16 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     const size_t pb = ctx->pb;
     // slab sets (m is not streamed into them when it is resident) + the C_i copy
     const int slab_fields = cfg->m_resident ? 2 : 3;    // also the streamed fields
-    size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb + slab_fields * (size_t)(2 * h) * pb;
-    if (!cfg->serpentine) need += 2 * (size_t)h * pb;   // pcopy
+#ifdef OOCZ_CONE_ONLY             // A/B: the trapezoid cone everywhere
+    ctx->para = false;
+#else
+    ctx->para = !cfg->serpentine;
+#endif
+    // with parallelogram tiles only C planes [h + 4ts - 4, 2h) of u, u- are kept
+    for (int f = 0; f < 2; f++) ctx->cbase[f] = ctx->para ? h : 0;
+    size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb;
+    for (int f = 0; f < slab_fields; f++) need += (size_t)(2 * h - ctx->cbase[f]) * pb;
+    if (ctx->para) need += 2 * (size_t)h * pb;   // pcopy
     const bool host = cfg->store == OOCZ_STORE_HOST;
     const int rd_max_planes = std::min(P + h, S);
     if (host) {
@@ -476,9 +486,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             CKC(cudaMalloc(&ctx->slab[k][f], (size_t)ctx->L * pb));
             CKC(cudaMemset(ctx->slab[k][f], 0, (size_t)ctx->L * pb));
         }
-        if (f < slab_fields) CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h) * pb));
+        if (f < slab_fields) CKC(cudaMalloc(&ctx->ccopy[f], (size_t)(2 * h - ctx->cbase[f]) * pb));
     }
-    if (!cfg->serpentine)
+    if (ctx->para)
         for (auto& q : ctx->pcopy) CKC(cudaMalloc(&q, (size_t)h * pb));
     CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
     if (cfg->m_resident) {
@@ -1040,11 +1050,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     // [iP - h + 4s, (i+1)P + h - 4s).  The planes below that it reads come at their
     // last two time levels from block i-1 (pcopy, slab [h-4, h-4+4ts)), so of the
     // time-t C_{i-1} only slab [h+4ts-4, 2h) of u, u- is needed.
-#ifdef OOCZ_CONE_ONLY             // A/B: the trapezoid cone everywhere
-    const bool para = false;
-#else
-    const bool para = !ctx->cfg.serpentine;
-#endif
+    const bool para = ctx->para;
     const int c0 = para ? h + 4 * ts - 4 : 0;                     // first C plane needed (u, u-)
     auto c_first = [&](int f) { return f == OOCZ_M ? 0 : c0; };
     if (has_c) {
@@ -1055,8 +1061,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
         for (int f = 0; f < nf; f++) {
             const size_t o = (size_t)c_first(f) * pb;
-            CK(cudaMemcpyAsync(slab[f] + dst + o, ctx->ccopy[f] + o, (size_t)(2 * h - c_first(f)) * pb,
-                               cudaMemcpyDeviceToDevice, sd));
+            CK(cudaMemcpyAsync(slab[f] + dst + o, ctx->ccopy[f] + o - (size_t)ctx->cbase[f] * pb,
+                               (size_t)(2 * h - c_first(f)) * pb, cudaMemcpyDeviceToDevice, sd));
         }
         prof_end(ctx, sd);
     }
@@ -1093,8 +1099,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
         for (int f = 0; f < nf; f++) {
             const size_t o = (size_t)c_first(f) * pb;
-            CK(cudaMemcpyAsync(ctx->ccopy[f] + o, slab[f] + off + o, (size_t)(2 * h - c_first(f)) * pb,
-                               cudaMemcpyDeviceToDevice, sd));
+            CK(cudaMemcpyAsync(ctx->ccopy[f] + o - (size_t)ctx->cbase[f] * pb, slab[f] + off + o,
+                               (size_t)(2 * h - c_first(f)) * pb, cudaMemcpyDeviceToDevice, sd));
         }
         prof_end(ctx, sd);
     }
