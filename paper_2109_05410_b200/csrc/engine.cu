@@ -15,6 +15,11 @@
 //    are exactly "the i-th remainder and the (i-1)-th common region" halves it
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
+//  * temporal blocking (beyond the paper, reading R26): ascending sweeps use
+//    parallelogram tiles -- block i > 0 updates [iP + 4(ts-s), (i+1)P + 4(ts-s))
+//    in step s and takes the strip [iP-4, iP+4ts-4) at its last two time levels
+//    from block i-1 -- so every cell is updated once per step; serpentine
+//    sweeps keep the paper's trapezoid cone [iP-h+4s, (i+1)P+h-4s);
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
 //    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
 //    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
@@ -26,7 +31,9 @@
 //   slab[s][f]: `slab_sets` sets (blocks rotate through them; default 2) of
 //               (P + 2h) planes of nx*ny fp32,
 //               slab plane 0 = rank plane iP - h
-//   ccopy[f]  : 2h planes, time-t copy of C_i (u, u-, m)
+//   ccopy[f]  : 2h planes, time-t copy of C_i (u, u-, m); with parallelogram
+//               tiles only its upper h planes for u, u-
+//   pcopy[2]  : h planes of u, u-: the parallelogram strip for block i+1
 //   in[slot]  : H2D staging of one read unit (3 fields), `slots` deep
 //   out[slot] : D2H staging of one write unit (2 read-write fields)
 //   store[f]  : pinned host (OOCZ_STORE_HOST) or device (OOCZ_STORE_DEVICE)
