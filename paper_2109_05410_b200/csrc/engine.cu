@@ -15,11 +15,11 @@
 //    are exactly "the i-th remainder and the (i-1)-th common region" halves it
 //    owns (reading R13);
 //  * the time-t copy of C_i is kept on the GPU for block i+1 (reading R14);
-//  * temporal blocking (beyond the paper, reading R26): ascending sweeps use
-//    parallelogram tiles -- block i > 0 updates [iP + 4(ts-s), (i+1)P + 4(ts-s))
+//  * temporal blocking (beyond the paper, reading R26): parallelogram tiles --
+//    in an ascending sweep block i > 0 updates [iP + 4(ts-s), (i+1)P + 4(ts-s))
 //    in step s and takes the strip [iP-4, iP+4ts-4) at its last two time levels
-//    from block i-1 -- so every cell is updated once per step; serpentine
-//    sweeps keep the paper's trapezoid cone [iP-h+4s, (i+1)P+h-4s);
+//    from block i-1 (descending sweeps mirror it) -- so every cell is updated
+//    once per step instead of the paper's trapezoid cone [iP-h+4s, (i+1)P+h-4s);
 //  * copies, codec and stencil overlap on CUDA streams (Fig. 5): h2d, decode,
 //    compute (stencil), encode, d2h.  Blocks rotate through `slab_sets` slab
 //    sets, so the decode of block i+1 and the encode of block i-1 (integer-ALU
@@ -163,7 +163,7 @@ struct oocz_ctx {
     int nsets = 2;                          // slab sets in rotation (cfg.slab_sets, default 2)
     uint8_t* slab[kMaxSets][3] = {};
     uint8_t* ccopy[3] = {nullptr, nullptr, nullptr};
-    uint8_t* pcopy[2] = {nullptr, nullptr};  // parallelogram strip of u, u- (ascending sweeps)
+    uint8_t* pcopy[2] = {nullptr, nullptr};  // parallelogram strip of u, u- for the next block
     bool para = false;                      // parallelogram tiles (reading R26)
     int cbase[3] = {0, 0, 0};               // first C plane ccopy[f] holds (h for u, u- with para)
     uint8_t* m_full = nullptr;              // m_resident: decoded m, planes [-h, S + h)
@@ -450,10 +450,11 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
 #ifdef OOCZ_CONE_ONLY             // A/B: the trapezoid cone everywhere
     ctx->para = false;
 #else
-    ctx->para = !cfg->serpentine;
+    ctx->para = true;
 #endif
-    // with parallelogram tiles only C planes [h + 4ts - 4, 2h) of u, u- are kept
-    for (int f = 0; f < 2; f++) ctx->cbase[f] = ctx->para ? h : 0;
+    // with parallelogram tiles and ascending sweeps only, only C planes
+    // [h + 4ts - 4, 2h) of u, u- are kept (descending sweeps need [0, h - 4ts + 4))
+    for (int f = 0; f < 2; f++) ctx->cbase[f] = ctx->para && !cfg->serpentine ? h : 0;
     size_t need = (size_t)ctx->nsets * slab_fields * (size_t)ctx->L * pb;
     for (int f = 0; f < slab_fields; f++) need += (size_t)(2 * h - ctx->cbase[f]) * pb;
     if (ctx->para) need += 2 * (size_t)h * pb;   // pcopy
@@ -1052,24 +1053,31 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     // ---- (a4) slab assembly on the decode stream, once this slab set is free
     CK(cudaStreamWaitEvent(sd, ctx->ev_slab_free[set], 0));
     const bool has_c = !turn && (dir > 0 ? i > 0 : i < D - 1);   // the shared region kept by the previous block
-    // Parallelogram tiling (sweeps without serpentine, reading R26): block i > 0
-    // updates [iP + 4(ts-s), (i+1)P + 4(ts-s)) in step s instead of the cone
-    // [iP - h + 4s, (i+1)P + h - 4s).  The planes below that it reads come at their
-    // last two time levels from block i-1 (pcopy, slab [h-4, h-4+4ts)), so of the
-    // time-t C_{i-1} only slab [h+4ts-4, 2h) of u, u- is needed.
+    // Parallelogram tiling (reading R26).  Ascending: a block with a block before
+    // it in the sweep updates [iP + 4(ts-s), (i+1)P + 4(ts-s)) in step s instead
+    // of the cone [iP - h + 4s, (i+1)P + h - 4s); the planes below that it reads
+    // come at their last two time levels from block i-1 (pcopy -> slab
+    // [h-4, h+4ts-4)), so of the time-t C_{i-1} only slab [h+4ts-4, 2h) of u, u-
+    // is needed.  Descending sweeps mirror it: [iP - 4(ts-s), (i+1)P - 4(ts-s)),
+    // the strip from block i+1 at slab [P+h-4ts+4, P+h+4), and C_i's slab
+    // [P, P+h-4ts+4).  The first block of a sweep keeps the cone on that side.
     const bool para = ctx->para;
-    const int c0 = para ? h + 4 * ts - 4 : 0;                     // first C plane needed (u, u-)
-    auto c_first = [&](int f) { return f == OOCZ_M ? 0 : c0; };
+    const bool has_next = dir > 0 ? i < D - 1 : i > 0;
+    // the planes [cr0, cr1) of the 2h-plane C region that are needed (u, u-)
+    const int cr0 = para && dir > 0 ? h + 4 * ts - 4 : 0;
+    const int cr1 = para && dir < 0 ? h - 4 * ts + 4 : 2 * h;
+    auto c_lo = [&](int f) { return f == OOCZ_M ? 0 : cr0; };
+    auto c_hi = [&](int f) { return f == OOCZ_M ? 2 * h : cr1; };
     if (has_c) {
         // ascending: C_{i-1} -> slab [0, 2h); descending: C_i -> slab [P, P+2h)
         const size_t dst = dir > 0 ? 0 : (size_t)P * pb;
         uint64_t cb = 0;
-        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(2 * h - c_first(f)) * pb;
+        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(c_hi(f) - c_lo(f)) * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
         for (int f = 0; f < nf; f++) {
-            const size_t o = (size_t)c_first(f) * pb;
+            const size_t o = (size_t)c_lo(f) * pb;
             CK(cudaMemcpyAsync(slab[f] + dst + o, ctx->ccopy[f] + o - (size_t)ctx->cbase[f] * pb,
-                               (size_t)(2 * h - c_first(f)) * pb, cudaMemcpyDeviceToDevice, sd));
+                               (size_t)(c_hi(f) - c_lo(f)) * pb, cudaMemcpyDeviceToDevice, sd));
         }
         prof_end(ctx, sd);
     }
@@ -1099,15 +1107,15 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     if (host && turn) CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[i]], sd));   // the kept slot is read
     // keep the time-t shared region for the next block (reading R14):
     // ascending C_i = slab [P, P+2h), descending C_{i-1} = slab [0, 2h)
-    if (dir > 0 ? i < D - 1 : i > 0) {
+    if (has_next) {
         const size_t off = dir > 0 ? (size_t)P * pb : 0;
         uint64_t cb = 0;
-        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(2 * h - c_first(f)) * pb;
+        for (int f = 0; f < nf; f++) cb += 2 * (uint64_t)(c_hi(f) - c_lo(f)) * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 4, sd, cb);
         for (int f = 0; f < nf; f++) {
-            const size_t o = (size_t)c_first(f) * pb;
+            const size_t o = (size_t)c_lo(f) * pb;
             CK(cudaMemcpyAsync(ctx->ccopy[f] + o - (size_t)ctx->cbase[f] * pb, slab[f] + off + o,
-                               (size_t)(2 * h - c_first(f)) * pb, cudaMemcpyDeviceToDevice, sd));
+                               (size_t)(c_hi(f) - c_lo(f)) * pb, cudaMemcpyDeviceToDevice, sd));
         }
         prof_end(ctx, sd);
     }
@@ -1118,15 +1126,23 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     uint8_t* cu = slab[OOCZ_U];
     uint8_t* cp = slab[OOCZ_UPREV];
     const size_t strip = (size_t)(4 * ts) * pb;
-    if (para && i > 0) {          // block i-1's strip [iP-4, iP+4ts-4), both leapfrog buffers
+    if (para && has_c) {          // the previous block's strip, both leapfrog buffers
+        const size_t at = (size_t)(dir > 0 ? h - 4 : P + h - 4 * ts + 4) * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 4 * (uint64_t)strip);
-        CK(cudaMemcpyAsync(cu + (size_t)(h - 4) * pb, ctx->pcopy[0], strip, cudaMemcpyDeviceToDevice, sc));
-        CK(cudaMemcpyAsync(cp + (size_t)(h - 4) * pb, ctx->pcopy[1], strip, cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(cu + at, ctx->pcopy[0], strip, cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(cp + at, ctx->pcopy[1], strip, cudaMemcpyDeviceToDevice, sc));
         prof_end(ctx, sc);
     }
     for (int s = 1; s <= ts; s++) {
-        const int z0 = !para ? std::max(4 * s, g.vlo) : i == 0 ? std::max(4 * s, g.vlo) : h + 4 * (ts - s);
-        const int z1 = std::min(para ? P + h + 4 * (ts - s) : ctx->L - 4 * s, g.vhi);
+        const int cone0 = std::max(4 * s, g.vlo), cone1 = std::min(ctx->L - 4 * s, g.vhi);
+        int z0 = cone0, z1 = cone1;
+        if (para && dir > 0) {
+            if (has_c) z0 = h + 4 * (ts - s);
+            z1 = std::min(P + h + 4 * (ts - s), g.vhi);
+        } else if (para) {
+            z0 = std::max(h - 4 * (ts - s), g.vlo);
+            if (has_c) z1 = P + h - 4 * (ts - s);
+        }
         // algorithmic bytes: read u, u-, m and write u+ once per updated cell
         prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 4ull * (uint64_t)std::max(z1 - z0, 0) * pb);
         CK(stencil_step(ctx, cu, cp, slab[OOCZ_M], z0, z1, g.vlo, g.vhi, sc));
@@ -1134,11 +1150,12 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         std::swap(cu, cp);
     }
 
-    if (para && i < D - 1) {      // the strip [(i+1)P-4, (i+1)P+4ts-4) for block i+1
+    if (para && has_next) {       // the strip for the next block: ascending rank planes
+        // [(i+1)P-4, (i+1)P+4ts-4), descending [iP-4ts+4, iP+4)
+        const size_t from = (size_t)(dir > 0 ? P + h - 4 : h - 4 * ts + 4) * pb;
         prof_begin(ctx, sweep, i, OOCZ_ST_COPY, 1, sc, 4 * (uint64_t)strip);
-        CK(cudaMemcpyAsync(ctx->pcopy[0], slab[OOCZ_U] + (size_t)(P + h - 4) * pb, strip, cudaMemcpyDeviceToDevice, sc));
-        CK(cudaMemcpyAsync(ctx->pcopy[1], slab[OOCZ_UPREV] + (size_t)(P + h - 4) * pb, strip,
-                           cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(ctx->pcopy[0], slab[OOCZ_U] + from, strip, cudaMemcpyDeviceToDevice, sc));
+        CK(cudaMemcpyAsync(ctx->pcopy[1], slab[OOCZ_UPREV] + from, strip, cudaMemcpyDeviceToDevice, sc));
         prof_end(ctx, sc);
     }
 

@@ -467,10 +467,11 @@ def test_graphs_ignored_where_not_eligible():
 @pytest.mark.parametrize("nx,ny,nz,T,P,calls", [(32, 24, 96, 3, 24, [7]), (24, 16, 64, 2, 16, [4, 3]),
                                                 (16, 16, 128, 4, 32, [8])])
 def test_parallelogram_updates_every_cell_once_per_step(nx, ny, nz, T, P, calls):
-    """Reading R26: without serpentine sweeps every block updates exactly P planes
-    per step (parallelogram tiling), so one step of the whole grid costs the
-    stencil 16 B per cell and no more; serpentine sweeps keep the trapezoid cone
-    (P + 2h - 8s planes).  Both are bit-exact against the oracle."""
+    """Reading R26: every block updates exactly P planes per step (parallelogram
+    tiles, mirrored in the descending sweeps of serpentine runs), so one step of
+    the whole grid costs the stencil 16 B per cell and no more, where the paper's
+    trapezoid cone costs (P + 2h - 8s) planes per block.  Bit-exact against the
+    oracle either way."""
     u, up, m = _fields(nx, ny, nz, 13)
     rates = (16, 16, 16)
     ou, oup = _run_oracle(u, up, m, T, rates, calls)
@@ -482,5 +483,5 @@ def test_parallelogram_updates_every_cell_once_per_step(nx, ny, nz, T, P, calls)
         # events of the last call only
         stencil_bytes[serp] = sum(e["bytes"] for e in evs if e["stage"] == 2)
     last = calls[-1]
-    assert stencil_bytes[0] == 4 * nz * pb * last          # read u, u-, m, write u+ once per cell and step
-    assert stencil_bytes[1] > stencil_bytes[0]
+    for serp in (0, 1):                                     # read u, u-, m, write u+ once per cell and step
+        assert stencil_bytes[serp] == 4 * nz * pb * last
