@@ -225,15 +225,32 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
             q[perm[i + 32]] = (int32_t)((hi[i] ^ zb::kNBMask) - zb::kNBMask);
         }
         zb::inv_xform(q);
+        // dequantise: one branch per block (not per value, which the compiler
+        // if-converts into both paths); emax >= -96 is the FMUL path of
+        // zb::dequantize, the rest its fp64 path
+        const int em = emax[s];
+        if (em >= -96) {
+            const float sc = __int_as_float((em - 30 + 127) << 23);
 #pragma unroll
-        for (int k = 0; k < 4; k++)
+            for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const int l = 16 * k + 4 * j;
-                *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
-                    make_float4(zb::dequantize(q[l], emax[s]), zb::dequantize(q[l + 1], emax[s]),
-                                zb::dequantize(q[l + 2], emax[s]), zb::dequantize(q[l + 3], emax[s]));
-            }
+                for (int j = 0; j < 4; j++) {
+                    const int l = 16 * k + 4 * j;
+                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
+                        make_float4(__fmul_rn(__int2float_rn(q[l]), sc), __fmul_rn(__int2float_rn(q[l + 1]), sc),
+                                    __fmul_rn(__int2float_rn(q[l + 2]), sc), __fmul_rn(__int2float_rn(q[l + 3]), sc));
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int l = 16 * k + 4 * j;
+                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
+                        make_float4(zb::dequantize(q[l], em), zb::dequantize(q[l + 1], em),
+                                    zb::dequantize(q[l + 2], em), zb::dequantize(q[l + 3], em));
+                }
+        }
     }
 }
 
@@ -372,15 +389,30 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
             q[perm[i + 32]] = (int64_t)((u1 ^ zb::kNBMask64) - zb::kNBMask64);
         }
         zb::inv_xform(q);
+        // one branch per block: emax >= -960 is zb::dequantize64's one-DMUL path
+        if (emax >= -960) {
+            const double sc = __longlong_as_double((long long)(emax - 62 + 1023) << 52);
 #pragma unroll
-        for (int k = 0; k < 4; k++)
+            for (int k = 0; k < 4; k++)
 #pragma unroll
-            for (int j = 0; j < 4; j++) {
-                const int l = 16 * k + 4 * j;
-                double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
-                row[0] = make_double2(zb::dequantize64(q[l], emax), zb::dequantize64(q[l + 1], emax));
-                row[1] = make_double2(zb::dequantize64(q[l + 2], emax), zb::dequantize64(q[l + 3], emax));
-            }
+                for (int j = 0; j < 4; j++) {
+                    const int l = 16 * k + 4 * j;
+                    double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
+                    row[0] = make_double2(__dmul_rn(__ll2double_rn(q[l]), sc), __dmul_rn(__ll2double_rn(q[l + 1]), sc));
+                    row[1] = make_double2(__dmul_rn(__ll2double_rn(q[l + 2]), sc),
+                                          __dmul_rn(__ll2double_rn(q[l + 3]), sc));
+                }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; k++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    const int l = 16 * k + 4 * j;
+                    double2* row = reinterpret_cast<double2*>(base + ((size_t)k * ny + j) * nx);
+                    row[0] = make_double2(zb::dequantize64(q[l], emax), zb::dequantize64(q[l + 1], emax));
+                    row[1] = make_double2(zb::dequantize64(q[l + 2], emax), zb::dequantize64(q[l + 3], emax));
+                }
+        }
     }
 }
 
