@@ -272,7 +272,7 @@ def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7
     av, bv = a64[zs, ys, xs], b64[zs, ys, xs]
     keep = np.abs(bv) >= 1e-30
     mean_pw = float(np.mean(np.abs(av - bv)[keep] / np.abs(bv)[keep])) if keep.any() else 0.0
-    sig = np.abs(bv) >= 1e-6 * np.abs(b64).max()     # points the wave has reached
+    sig = keep & (np.abs(bv) >= 1e-6 * np.abs(b64).max())     # points the wave has reached
     mean_sig = float(np.mean(np.abs(av - bv)[sig] / np.abs(bv)[sig])) if sig.any() else 0.0
     return {"normwise_max": normwise, "mean_pointwise": mean_pw, "points": int(keep.sum()),
             "skipped": int((~keep).sum()), "mean_pointwise_significant": mean_sig,
