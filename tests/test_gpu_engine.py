@@ -366,12 +366,12 @@ def test_random_configurations_bit_exact(seed):
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), cfg
 
 
-def test_random_partitioned_configurations_bit_exact():
+def test_random_partitioned_configurations_bit_exact(seed=4242):
     """24 seeded random z-partitioned runs (in-process local group of 2-4 ranks,
     compressed halos) with every orchestration option: equal to the oracle,
     i.e. to world 1, bit for bit."""
     z = Z()
-    rng = np.random.default_rng(4242)
+    rng = np.random.default_rng(seed)
     for case in range(24):
         world = int(rng.choice([2, 3, 4]))
         T = int(rng.integers(1, 3))

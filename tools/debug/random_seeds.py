@@ -12,4 +12,6 @@ seeds = [int(s) for s in (sys.argv[1] if len(sys.argv) > 1 else "11,12,13,14").s
 for sd in seeds:
     t = time.time()
     E.test_random_configurations_bit_exact(sd)
+    if os.environ.get("PARTITIONED", "0") == "1":
+        E.test_random_partitioned_configurations_bit_exact(sd)
     print("seed", sd, "ok", round(time.time() - t, 1), "s", flush=True)
