@@ -241,10 +241,10 @@ def test_stencil_ring_release_stress(dtype):
             assert np.array_equal(dup.cpu().numpy(), want), (nx, ny, nz)
 
 
-def test_random_configurations64_bit_exact():
+def test_random_configurations64_bit_exact(seed=64):
     """48 seeded random configurations in the paper's precision (fp64, rates
     raw / 1..64, every orchestration option) against the fp64 oracle."""
-    rng = np.random.default_rng(64)
+    rng = np.random.default_rng(seed)
     for case in range(48):
         T = int(rng.integers(1, 4))
         P = int(rng.choice([q for q in (8, 12, 16, 20, 24) if q >= 8 * T]))
