@@ -1,27 +1,43 @@
 #!/usr/bin/env python3
 """Benchmark of the out-of-core compressed stencil stepper (arXiv 2109.05410).
 
-One bench "step" = one sweep = T = 4 leapfrog steps over the whole grid through
-the whole hot path (per z-block H2D/decode ->
-4 cone-limited 25-point steps -> encode/D2H, region sharing, 3 streams).
+One bench "step" = one sweep = T = 4 leapfrog steps over the whole grid
+through the whole hot path (per z-block H2D / decode
+-> 4 temporally blocked 25-point steps -> encode / D2H, region sharing,
+separate copy / codec / stencil streams).
 
-Workload (BASELINE.json configs[1]): 512^3 fp32, DENSE(seed 1) wavefield,
-u- = u, LAYERED m; P = 128 (4 z-blocks), T = 4, ZFP fixed rate 16 on all three
-fields, and the same with compression off ("raw") for the paper's speedup
-question.  Metric: cell-updates/s = nx*ny*nz*T*K / time of K sweeps.
+Headline workload (BASELINE.json configs[2]): a 4096 x 4096 x
+1536 fp32 wavefield, previous wavefield and velocity model -- 309 GB of state,
+more than the GPU's HBM and the host's RAM -- DENSE(seed 2) u, u- = u, LAYERED
+m, streamed OUT OF CORE on one B200 at ZFP fixed rate 16 on all three fields
+(a 154.6 GB pinned compressed store), T = 4.  Inputs are generated on the GPU
+in plane chunks (synth.dense_torch / layered_torch, bit-identical to synth)
+and compressed with oocz_set_field_planes; no full-size array ever exists.
 
-  value : compressed store resident in HBM (inputs already on the device):
-          decode -> stencil -> encode per block, device-timed (CUDA events on
-          the library's own streams), max over ranks.
-  e2e   : the paper's out-of-core path through the public C ABI with the
-          store in pinned HOST memory: every sweep moves the whole compressed
-          state H2D and the read-write fields D2H inside the timed region.
+  value : cell-updates/s = nx*ny*nz*T*K / device time of K sweeps, the store
+          in pinned HOST memory: every sweep moves the compressed state over
+          the host link (PCIe) inside the timed region.  Device-timed with CUDA
+          events on the library's own streams (first enqueue -> join), max over
+          ranks.  Schedule: the library's fastest orchestration of the same
+          computation (serpentine sweeps + m decoded once into HBM + 3 staging
+          slots, R22/R23; bit-identical results, tests).
+  e2e   : the same K sweeps timed by the host wall clock around oocz_step
+          (the public C ABI call), max over ranks.
+  c3_paper_faithful : the paper's schedule (ascending sweeps, m streamed, P=192).
+  zfp_vs_raw : the paper's question at the largest C3-shaped grid whose RAW
+          store fits this host (4096 x 4096 x 768: 154.6 GB raw = the C3 rate-16
+          store), both schedules, plus the error of the compressed run.
+  c3_hbm_resident : the compressed C3 store held in HBM instead (no host link).
+  c2 : the 512^3 configuration (configs[1]) -- HBM-resident and out-of-core,
+          rates 8/16/24, the paper's codes 2-4 in fp32 and fp64, T = 8 / 12.
 
-Multi-GPU (torchrun, N > 1): the grid is z-partitioned, one 512^3 slab per
-rank (weak scaling), radius-4 halos exchanged in compressed form with NCCL.
+Multi-GPU (torchrun, N > 1; configs[3]): the same C3 grid
+z-partitioned over N ranks (strong scaling), each rank streaming its own slab
+out of core from its own pinned store, radius-4 halos exchanged in compressed
+form with NCCL.
 
---impl reference: the CPU oracle (oracle/, test infrastructure) timed on
-the host cores on a bounded sample of the same workload.
+--impl reference: the CPU oracle (oracle/, test infrastructure) timed on the
+host cores on a bounded sample of the same workload.
 """
 from __future__ import annotations
 
@@ -40,10 +56,21 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "cell-updates/s out-of-core, ZFP vs raw, at 1/2/4/8 B200; max rel. error"
-NX = NY = NZ = 512
 T = 4
-P = 128
 RATE = 16
+# C3 (configs[2])
+C3N, C3Z, C3SEED = 4096, 1536, 2
+# C2 (configs[1])
+NX = NY = NZ = 512
+P = 128
+
+
+_T0 = time.perf_counter()
+
+
+def log(msg: str) -> None:
+    """Progress on stderr (the JSON line is the only stdout)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
 
 
 def peaks():
@@ -56,15 +83,16 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks and throttle reasons sampled during the timed regions."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
 
     def __init__(self, index: int):
         self.index = index
         self.samples = []
+        self.active = False
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
@@ -74,7 +102,7 @@ class ClockSampler:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                                       "--format=csv,noheader,nounits"], capture_output=True, text=True,
                                      timeout=5).stdout.strip()
-                if out:
+                if out and self.active:
                     self.samples.append([x.strip() for x in out.split(",")])
             except Exception:
                 pass
@@ -96,56 +124,33 @@ class ClockSampler:
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({names[i] for s in self.samples for i in range(4) if s[2 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(self.samples),
+                "note": "sampled only while timed sweeps run (out-of-core sweeps leave the SMs partly idle)"}
 
 
-# ---------------------------------------------------------------- GPU arm
-def make_fields(rank: int, S: int):
-    from paper_2109_05410_b200 import synth
-    z0 = rank * S
-    u = synth.dense(NX, NY, NZ, seed=1, z0=z0 % NZ, z1=z0 % NZ + S) if S <= NZ else None
-    m = synth.layered(NX, NY, NZ, z0=z0 % NZ, z1=z0 % NZ + S)
-    return u, u, m
-
-
-def run_mode(Z, store, rates, fields, rank, world, nccl_id, device, steps, warmup, dist, profile, m_resident=0,
-             tb=T, precision=32, serpentine=0, slots=2, slab_sets=0, graphs=0):
-    """Returns (device seconds for `steps` sweeps (max over ranks), stats, events, launches)."""
-    import torch
-    cfg = Z.oocz_default_config(NX, NY, NZ * world, tb=tb, block_planes=P, rate=list(rates), store=store,
-                                m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=slots, profile=profile, slab_sets=slab_sets, graphs=graphs)
-    if callable(nccl_id):   # a fresh NCCL unique id per communicator (an id bootstraps one init only)
-        nccl_id = nccl_id()
-    ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
+def host_info() -> dict:
+    """lscpu model, sockets, physical cores, and host RAM (for the oracle and the store)."""
+    info = {"logical_cpus": os.cpu_count()}
     try:
-        for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
-            Z.oocz_set_field(ctx, f, a.astype(np.float64) if precision == 64 else a)
-        Z.oocz_step(ctx, warmup * tb)
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        st0 = Z.oocz_get_stats(ctx)
-        l0 = Z.oocz_kernel_launch_count()
-        Z.oocz_step(ctx, steps * tb)
-        launches = Z.oocz_kernel_launch_count() - l0
-        torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        st = Z.oocz_get_stats(ctx)
-        for k in ("sweeps", "h2d_bytes", "d2h_bytes", "halo_bytes"):   # the timed call only
-            st[k] -= st0[k]
-        dev_s = st["last_step_device_ms"] / 1e3
-        if dist:
-            from paper_2109_05410_b200 import dist as D
-            dev_s = D.max_over_ranks(dist, dev_s, device="cuda")
-        evs = Z.oocz_get_events(ctx) if profile else []
-        # per-sweep bytes of the timed call only
-        st_all = st
-        return dev_s, st_all, evs, launches, ctx
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {ln.split(":", 1)[0].strip(): ln.split(":", 1)[1].strip() for ln in out.splitlines() if ":" in ln}
+        info["model"] = kv.get("Model name")
+        sockets = int(kv.get("Socket(s)", "1") or 1)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        info["sockets"] = sockets
+        info["physical_cores"] = sockets * cps if cps else None
+        info["threads_per_core"] = int(kv.get("Thread(s) per core", "1") or 1)
+        info["hypervisor"] = kv.get("Hypervisor vendor")
     except Exception:
-        Z.oocz_destroy(ctx)
-        raise
+        pass
+    try:
+        with open("/proc/meminfo") as fh:
+            mi = {ln.split(":")[0]: int(ln.split()[1]) * 1024 for ln in fh}
+        info["mem_total_bytes"] = mi.get("MemTotal")
+        info["mem_available_bytes"] = mi.get("MemAvailable")
+    except Exception:
+        pass
+    return info
 
 
 def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
@@ -199,10 +204,363 @@ def lanes_summary(evs) -> dict:
     return out
 
 
+TRAFFIC_JSON = {"stencil": "r01_stencil_instep_traffic.json"}
+ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
+
+
+def kernel_table(evs) -> dict:
+    from paper_2109_05410_b200.oocz import STAGES
+    per = {}
+    for e in evs:
+        name = STAGES[e["stage"]]
+        if name not in ("stencil", "decode", "encode"):
+            continue
+        d = per.setdefault(name, [0.0, 0, 0])
+        d[0] += e["end_ms"] - e["start_ms"]
+        d[1] += e["bytes"]
+        d[2] += 1
+    return per
+
+
+def roofline(evs, peak_gbs, peak_src):
+    """Dominant kernel of the timed region from its per-launch CUDA events
+    (recorded on the stream each kernel is launched on): achieved =
+    algorithmic bytes of all its launches / their summed duration."""
+    per = kernel_table(evs)
+    if not per:
+        return None, {}
+    dom = max(per, key=lambda k: per[k][0])
+    ms, nbytes, n = per[dom]
+    achieved = nbytes / (ms / 1e3) / 1e9
+    table = {k: {"ms": round(v[0], 4), "launches": v[2], "GB/s": round(v[1] / (v[0] / 1e3) / 1e9, 1),
+                 "avg_launch_ms": round(v[0] / v[2], 4)}
+             for k, v in per.items()}
+    kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
+    traffic, tsrc = None, None
+    try:   # DRAM bytes per launch from a committed ncu capture of the same kind of launch
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON[dom])) as fh:
+            tj = json.load(fh)
+        traffic = int(tj["traffic_over_algorithmic"] * nbytes / n)
+        tsrc = (f"profiles/{TRAFFIC_JSON[dom]}: ncu dram read+write / algorithmic = "
+                f"{tj['traffic_over_algorithmic']}, x this run's algorithmic bytes per launch")
+    except Exception:
+        pass
+    return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": peak_gbs,
+            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
+            "traffic": traffic, "traffic_source": tsrc, "avg_launch_ms": round(ms / n, 4),
+            "launches": n, "algorithmic_bytes_per_launch": int(nbytes / n),
+            "algorithmic_bytes": "stencil: 16 B per updated cell (read u, u-, m; write u+); decode / encode: "
+                                 "compressed bytes + 4 B per value (DESIGN.md section 6)"}, table
+
+
+def codec_alu_roofline(table) -> dict | None:
+    """The codec kernels are bound by the integer ALU pipe,
+    not by HBM: their fraction is the ALU pipe's share of its peak issue rate
+    (148 SMs x 4 sub-partitions x one warp-instruction per 2 cycles at 1965 MHz),
+    measured by ncu (sm__inst_executed_pipe_alu) on the committed capture."""
+    for cand in ("r02_ncu_kernels.json", "r01_ncu_kernels.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", cand)) as fh:
+                kj = json.load(fh)
+            break
+        except Exception:
+            kj = None
+    if kj is None:
+        return None
+    out = {}
+    for name, stage in (("zfp_decode_kernel", "decode"), ("zfp_encode_kernel", "encode")):
+        ks = [k for k in kj["kernels"] if k["kernel"].endswith(name)]
+        if not ks:
+            continue
+        k = ks[0]
+        frac = k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"] / 100.0
+        out[name] = {"bound": "alu", "achieved": round(frac * ALU_PEAK, 1), "peak": round(ALU_PEAK, 1),
+                     "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
+                     "issue_active": round(k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100, 4),
+                     "isolated_us": k["gpu__time_duration.sum"],
+                     "in_step_avg_ms": table[stage]["avg_launch_ms"] if stage in table else None,
+                     "source": f"profiles/{cand} (ncu --set full, one C2 slab, rate 16)"}
+    return out or None
+
+
+def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7) -> dict:
+    """Compressed run `a` vs the uncompressed run `b` after the same steps
+    (R18/R19): normwise max|a-b|/max|b| over the given
+    planes, the paper's mean point-wise |a-b|/|b| over `per_plane` seeded points
+    per plane (|b| < 1e-30 skipped), and the same over the points the wave has
+    reached (|b| >= 1e-6 max|b|)."""
+    from paper_2109_05410_b200 import synth
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    normwise = float(np.abs(a64 - b64).max() / max(np.abs(b64).max(), 1e-300))
+    l2 = float(np.sqrt(np.sum((a64 - b64) ** 2)) / max(np.sqrt(np.sum(b64 ** 2)), 1e-300))
+    nz, ny, nx = b.shape
+    r = synth.uniforms(seed, 2 * per_plane * nz).reshape(nz, per_plane, 2)
+    ys = (r[..., 0] * ny).astype(np.int64)
+    xs = (r[..., 1] * nx).astype(np.int64)
+    zs = np.repeat(np.arange(nz), per_plane).reshape(nz, per_plane)
+    av, bv = a64[zs, ys, xs], b64[zs, ys, xs]
+    keep = np.abs(bv) >= 1e-30
+    mean_pw = float(np.mean(np.abs(av - bv)[keep] / np.abs(bv)[keep])) if keep.any() else 0.0
+    sig = keep & (np.abs(bv) >= 1e-6 * np.abs(b64).max())
+    mean_sig = float(np.mean(np.abs(av - bv)[sig] / np.abs(bv)[sig])) if sig.any() else 0.0
+    return {"normwise_max": normwise, "l2": l2, "mean_pointwise": mean_pw, "points": int(keep.sum()),
+            "skipped": int((~keep).sum()), "mean_pointwise_significant": mean_sig,
+            "significant_points": int(sig.sum()), "vs": "same build, compression off (raw)"}
+
+
+# ---------------------------------------------------------------- C3 / C4: out of core at scale
+def set_fields_gpu(Z, ctx, nx, ny, nz, z_lo, S, seed, chunk=16):
+    """Set this rank's slab [z_lo, z_lo + S) of DENSE(seed) (u and u-) and LAYERED
+    (m), generated on the GPU chunk by chunk; returns seconds."""
+    import torch
+    from paper_2109_05410_b200 import synth
+    t0 = time.perf_counter()
+    for z0 in range(0, S, chunk):
+        z1 = min(z0 + chunk, S)
+        d = synth.dense_torch(nx, ny, nz, seed, z_lo + z0, z_lo + z1)
+        Z.oocz_set_field_planes(ctx, Z.OOCZ_U, z0, d)
+        Z.oocz_set_field_planes(ctx, Z.OOCZ_UPREV, z0, d)
+        del d
+        Z.oocz_set_field_planes(ctx, Z.OOCZ_M, z0, synth.layered_torch(nx, ny, nz, z_lo + z0, z_lo + z1))
+    torch.cuda.synchronize()
+    return time.perf_counter() - t0
+
+
+def pick_P(S: int, prefer: int) -> int:
+    for p in (prefer, 96, 64, 48, 32):
+        if p <= S and S % p == 0 and p >= 8 * T:
+            return p
+    return S
+
+
+def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device, steps, warmup, dist,
+           profile=0, sample_planes=None):
+    """One out-of-core (or HBM-resident) run on the C3-shaped grid: create (with
+    the shared pinned arena), set fields on the GPU, W warm-up sweeps, K timed
+    sweeps; device time (library events) and host wall time of the timed call,
+    max over ranks."""
+    import torch
+    S = nz // world
+    store = opt.get("store", 0)
+    cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=opt["P"], rate=list(rates), store=store,
+                                m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
+                                slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile)
+    if callable(nccl_id):
+        nccl_id = nccl_id()
+    torch.cuda.empty_cache()             # the generator's chunks: HBM for the context (C3 fills it)
+    log(f"{label}: grid {nx}x{ny}x{nz} rates {list(rates)} {opt} W={warmup} K={steps}")
+    t0 = time.perf_counter()
+    if store == 0:
+        ctx = Z.oocz_create_ex(cfg, rank, world, nccl_id, device, arena[0], arena[1])
+    else:
+        ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
+    t_create = time.perf_counter() - t0
+    try:
+        # a compressed store in HBM leaves little room for the generator's fp64 chunks
+        t_set = set_fields_gpu(Z, ctx, nx, ny, nz, rank * S, S, C3SEED, chunk=16 if store == 0 else 4)
+        Z.oocz_step(ctx, warmup * T)
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        st0 = Z.oocz_get_stats(ctx)
+        l0 = Z.oocz_kernel_launch_count()
+        h0 = time.perf_counter()
+        Z.oocz_step(ctx, steps * T)          # returns when every stream is done
+        host_s = time.perf_counter() - h0
+        launches = Z.oocz_kernel_launch_count() - l0
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        st = Z.oocz_get_stats(ctx)
+        dev_s = st["last_step_device_ms"] / 1e3
+        if dist:
+            from paper_2109_05410_b200 import dist as D
+            dev_s = D.max_over_ranks(dist, dev_s, device="cuda")
+            host_s = D.max_over_ranks(dist, host_s, device="cuda")
+        sweeps = st["sweeps"] - st0["sweeps"]
+        h2d = (st["h2d_bytes"] - st0["h2d_bytes"]) / max(sweeps, 1)
+        d2h = (st["d2h_bytes"] - st0["d2h_bytes"]) / max(sweeps, 1)
+        cells = nx * ny * nz * T * steps
+        res = {"label": label, "grid": [nx, ny, nz], "rates": list(rates), "P": opt["P"], "D": S // opt["P"],
+               "schedule": {k: v for k, v in opt.items() if k != "P"},
+               "cups": cells / dev_s, "e2e_cups": cells / host_s, "device_s": dev_s, "host_s": host_s,
+               "sweeps": steps, "warmup": warmup, "launches": launches,
+               "h2d_per_sweep": h2d, "d2h_per_sweep": d2h, "halo_per_sweep": (st["halo_bytes"] - st0["halo_bytes"]) / max(sweeps, 1),
+               "h2d_GBps": h2d * steps / dev_s / 1e9, "d2h_GBps": d2h * steps / dev_s / 1e9,
+               "device_bytes": st["device_bytes_used"], "create_s": round(t_create, 2), "set_fields_s": round(t_set, 2),
+               "evs": Z.oocz_get_events(ctx) if profile else []}
+        if sample_planes is not None:    # planes of u for the compressed-vs-raw error
+            res["u_planes"] = np.concatenate([Z.oocz_get_field_planes(ctx, Z.OOCZ_U, z0, np.empty((4, ny, nx), np.float32))
+                                              for z0 in sample_planes])
+        log(f"{label}: {res['cups'] / 1e9:.1f} G cell-updates/s (host {res['e2e_cups'] / 1e9:.1f} G), "
+            f"create {t_create:.1f} s, set {t_set:.1f} s")
+        return res
+    finally:
+        Z.oocz_destroy(ctx)
+
+
+def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link, clk, info):
+    import torch
+    nx = ny = C3N
+    nz = C3Z
+    S = nz // world
+    # the pinned host store is allocated ONCE (pinning runs at ~2 GB/s) and reused by every
+    # out-of-core run below: the largest is the rate-16 C3 store (= the raw 4096^2 x 768 one)
+    cfg16 = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=pick_P(S, 64), rate=[RATE] * 3)
+    need = Z.oocz_host_store_bytes(cfg16, world)
+    raw_nz = nz // 2                                     # raw 4 B/value = 2 x rate 16
+    t0 = time.perf_counter()
+    log(f"pinning a {need / 1e9:.1f} GB host arena")
+    arena_p = Z.oocz_host_alloc(need)
+    arena = (arena_p, need)
+    t_arena = time.perf_counter() - t0
+    out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
+    try:
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=3)
+        PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2)
+        clk.active = True
+        out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id, local,
+                                 args.steps, args.warmup, dist, profile=1)
+        clk.active = False
+        if world == 1 and not args.quick:
+            sw, wu = args.sec_steps, 1
+            clk.active = True
+            out["pf"] = run_c3(Z, "c3_zfp_host_pf", nx, ny, nz, (RATE,) * 3, PF, arena, rank, world, nccl_id, local,
+                               sw, wu, dist)
+            # ZFP vs raw on the largest C3-shaped grid whose raw store fits this host
+            planes = [0, raw_nz // 4, raw_nz // 2, 3 * raw_nz // 4 - 4, raw_nz - 4]
+            HSr = dict(HS, P=pick_P(raw_nz, 64))
+            PFr = dict(PF, P=pick_P(raw_nz, 96))
+            for key, rates, opt in (("half_zfp_hs", (RATE,) * 3, HSr), ("half_raw_hs", (0, 0, 0), HSr),
+                                    ("half_zfp_pf", (RATE,) * 3, PFr), ("half_raw_pf", (0, 0, 0), PFr)):
+                out[key] = run_c3(Z, key, nx, ny, raw_nz, rates, opt, arena, rank, world, nccl_id, local, sw, wu,
+                                  dist, sample_planes=planes)
+            clk.active = False
+    finally:
+        Z.oocz_host_free(arena_p)
+    if world == 1 and not args.quick:
+        # the compressed C3 store held in HBM (154.6 GB) beside one slab set: no host link
+        clk.active = True
+        try:
+            out["hbm"] = run_c3(Z, "c3_zfp_dev", nx, ny, nz, (RATE,) * 3, dict(P=96, store=1, slab_sets=1), None,
+                                rank, world, nccl_id, local, args.sec_steps, 1, dist)
+        except Exception as e:            # a secondary number: report, do not lose the headline
+            out["hbm_error"] = f"{type(e).__name__}: {e}"[:300]
+        clk.active = False
+    torch.cuda.empty_cache()
+    return out
+
+
+def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
+    h = c3["headline"]
+    roof, table = roofline(h["evs"], peak_gbs, peak_src)
+    busier = max(h["h2d_per_sweep"], h["d2h_per_sweep"])
+    link_peak = link["concurrent_per_direction_GBps"]
+    rep = {
+        "value": round(h["cups"], 1),
+        "ms_per_step": round(h["device_s"] * 1e3 / args.steps, 3),
+        "e2e": {"value": round(h["e2e_cups"], 1), "unit": "cell-updates/s",
+                "h2d_bytes_per_step": int(h["h2d_per_sweep"]), "d2h_bytes_per_step": int(h["d2h_per_sweep"]),
+                "path": "host wall clock around oocz_step (the public C ABI) over the K timed sweeps; the "
+                        "compressed store is in pinned host memory, so each sweep's H2D of the state and D2H "
+                        "of the updated read-write fields are inside the call",
+                "ms_per_step": round(h["host_s"] * 1e3 / args.steps, 3)},
+        "roofline": roof,
+        "roofline_host_link": {
+            "bound": "host-link", "achieved": round(busier * args.steps / h["device_s"] / 1e9, 2),
+            "peak": link_peak, "unit": "GB/s",
+            "frac": round(busier * args.steps / h["device_s"] / 1e9 / link_peak, 4),
+            "h2d_GBps": round(h["h2d_GBps"], 2), "d2h_GBps": round(h["d2h_GBps"], 2),
+            "peak_source": "measured in this run: pinned H2D and D2H at once on two streams (host_link_probe)",
+            "what": "the out-of-core roofline (SURVEY 8(d)): bytes the busier direction must move per sweep / "
+                    "time, over the measured concurrent per-direction bandwidth",
+            "host_link_probe": link},
+        "kernels_in_step": table,
+        "codec_alu_roofline": codec_alu_roofline(table),
+        "lanes": lanes_summary(h["evs"]),
+        "gpu_launches": int(h["launches"]),
+        "headline_run": {k: (round(v, 4) if isinstance(v, float) else v) for k, v in h.items()
+                         if k not in ("evs", "u_planes")},
+    }
+    if "pf" in c3:
+        pf = c3["pf"]
+        rep["c3_paper_faithful"] = {
+            "value": round(pf["cups"], 1), "e2e": round(pf["e2e_cups"], 1), "P": pf["P"], "D": pf["D"],
+            "h2d_bytes_per_step": int(pf["h2d_per_sweep"]), "d2h_bytes_per_step": int(pf["d2h_per_sweep"]),
+            "h2d_GBps": round(pf["h2d_GBps"], 2), "d2h_GBps": round(pf["d2h_GBps"], 2),
+            "sweeps": pf["sweeps"],
+            "schedule": "the paper's: ascending sweeps, m streamed and decoded every sweep, 2 staging slots",
+            "headline_over_paper_faithful": round(h["cups"] / pf["cups"], 3)}
+    if "half_raw_pf" in c3:
+        zr = {"grid": c3["half_raw_pf"]["grid"],
+              "why": "the full C3 raw store (3 x 103.1 GB = 309.2 GB) cannot exist on this host "
+                     f"(RAM {info.get('mem_total_bytes', 0) / 1e9:.1f} GB); 4096 x 4096 x 768 is the largest C3-shaped "
+                     "grid whose raw store (154.6 GB) fits, the same bytes as the C3 rate-16 store",
+              "c3_raw_store_bytes": 3 * C3N * C3N * C3Z * 4, "host_mem_bytes": info.get("mem_total_bytes")}
+        for sched, zk, rk in (("headline_schedule", "half_zfp_hs", "half_raw_hs"),
+                              ("paper_faithful", "half_zfp_pf", "half_raw_pf")):
+            z, r = c3[zk], c3[rk]
+            err = rel_errors(z["u_planes"], r["u_planes"])
+            err["planes"] = "u after the same steps, 5 block-rows spread over z (100 seeded points per plane)"
+            zr[sched] = {"zfp": round(z["cups"], 1), "raw": round(r["cups"], 1),
+                         "speedup": round(z["cups"] / r["cups"], 3),
+                         "zfp_e2e": round(z["e2e_cups"], 1), "raw_e2e": round(r["e2e_cups"], 1),
+                         "zfp_h2d_bytes_per_step": int(z["h2d_per_sweep"]),
+                         "raw_h2d_bytes_per_step": int(r["h2d_per_sweep"]),
+                         "zfp_h2d_GBps": round(z["h2d_GBps"], 2), "raw_h2d_GBps": round(r["h2d_GBps"], 2),
+                         "P": z["P"], "steps": (z["sweeps"] + z["warmup"]) * T, "max_rel_error": err}
+        zr["paper_context"] = "1.20x (fp64, mode 4, V100-PCIe 3.0, PAPER.md:227)"
+        rep["zfp_vs_raw"] = zr
+    if "hbm_error" in c3:
+        rep["c3_hbm_resident"] = {"error": c3["hbm_error"]}
+    if "hbm" in c3:
+        d = c3["hbm"]
+        rep["c3_hbm_resident"] = {"value": round(d["cups"], 1), "P": d["P"], "slab_sets": 1,
+                                  "device_bytes": d["device_bytes"], "sweeps": d["sweeps"],
+                                  "what": "the same C3 problem with the 154.6 GB compressed store held in HBM "
+                                          "(store = device): decode -> stencil -> encode per block, no host link"}
+    return rep
+
+
+# ---------------------------------------------------------------- C2 (configs[1]): 512^3
+def make_fields_c2():
+    from paper_2109_05410_b200 import synth
+    u = synth.dense(NX, NY, NZ, seed=1)
+    m = synth.layered(NX, NY, NZ)
+    return u, u, m
+
+
+def run_mode_c2(Z, store, rates, fields, device, steps, warmup, profile, m_resident=0, tb=T, precision=32,
+                serpentine=0, slots=2, slab_sets=0):
+    """Returns (device seconds for `steps` sweeps, stats, events, launches, ctx)."""
+    import torch
+    cfg = Z.oocz_default_config(NX, NY, NZ, tb=tb, block_planes=P, rate=list(rates), store=store,
+                                m_resident=m_resident, precision=precision, serpentine=serpentine,
+                                slots=slots, profile=profile, slab_sets=slab_sets)
+    ctx = Z.oocz_create(cfg, 0, 1, None, device)
+    try:
+        for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
+            Z.oocz_set_field(ctx, f, a.astype(np.float64) if precision == 64 else a)
+        Z.oocz_step(ctx, warmup * tb)
+        torch.cuda.synchronize()
+        st0 = Z.oocz_get_stats(ctx)
+        l0 = Z.oocz_kernel_launch_count()
+        Z.oocz_step(ctx, steps * tb)
+        launches = Z.oocz_kernel_launch_count() - l0
+        st = Z.oocz_get_stats(ctx)
+        for k in ("sweeps", "h2d_bytes", "d2h_bytes", "halo_bytes"):
+            st[k] -= st0[k]
+        evs = Z.oocz_get_events(ctx) if profile else []
+        return st["last_step_device_ms"] / 1e3, st, evs, launches, ctx
+    except Exception:
+        Z.oocz_destroy(ctx)
+        raise
+
+
 def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
     """Each hot kernel alone on one block's slab (P + 2h planes of the C2 data),
     CUDA events on the launching stream, L2 flushed between launches; achieved =
-    algorithmic bytes / median duration (DESIGN.md "Roofline")."""
+    algorithmic bytes / median duration (DESIGN.md section 6)."""
     import torch
     planes = P + 8 * T
     u = torch.from_numpy(np.ascontiguousarray(fields[0][:planes])).cuda()
@@ -237,7 +595,6 @@ def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
         t = med(fn)
         res[name] = {"ms": round(t * 1e3, 4), "achieved_GBps": round(nbytes / t / 1e9, 1),
                      "frac": round(nbytes / t / 1e9 / peak_gbs, 4), "algorithmic_bytes": int(nbytes)}
-    # fp64 twins (the paper's precision) at its 2:1 rate 32/64
     u64, m64 = u.double(), m.double()
     up64, out64 = u64.clone(), torch.empty_like(u64)
     r64 = 32
@@ -256,96 +613,113 @@ def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
     return res
 
 
-def rel_errors(a: np.ndarray, b: np.ndarray, per_plane: int = 100, seed: int = 7) -> dict:
-    """Compressed run `a` vs the uncompressed run `b` after the same steps
-    (R18/R19): normwise max|a-b|/max|b| over the whole
-    field, and the paper's mean point-wise |a-b|/|b| over `per_plane` seeded
-    points per plane (|b| < 1e-30 skipped)."""
-    from paper_2109_05410_b200 import synth
-    a64, b64 = a.astype(np.float64), b.astype(np.float64)
-    normwise = float(np.abs(a64 - b64).max() / max(np.abs(b64).max(), 1e-300))
-    nz, ny, nx = b.shape
-    r = synth.uniforms(seed, 2 * per_plane * nz).reshape(nz, per_plane, 2)
-    ys = (r[..., 0] * ny).astype(np.int64)
-    xs = (r[..., 1] * nx).astype(np.int64)
-    zs = np.repeat(np.arange(nz), per_plane).reshape(nz, per_plane)
-    av, bv = a64[zs, ys, xs], b64[zs, ys, xs]
-    keep = np.abs(bv) >= 1e-30
-    mean_pw = float(np.mean(np.abs(av - bv)[keep] / np.abs(bv)[keep])) if keep.any() else 0.0
-    sig = keep & (np.abs(bv) >= 1e-6 * np.abs(b64).max())     # points the wave has reached
-    mean_sig = float(np.mean(np.abs(av - bv)[sig] / np.abs(bv)[sig])) if sig.any() else 0.0
-    return {"normwise_max": normwise, "mean_pointwise": mean_pw, "points": int(keep.sum()),
-            "skipped": int((~keep).sum()), "mean_pointwise_significant": mean_sig,
-            "significant_points": int(sig.sum()), "vs": "same build, compression off (raw)"}
-
-
-def roofline(evs, peak_gbs, peak_src):
-    """Dominant kernel of the timed region from the per-launch CUDA events."""
-    from paper_2109_05410_b200.oocz import STAGES
-    per = {}
-    for e in evs:
-        name = STAGES[e["stage"]]
-        if name not in ("stencil", "decode", "encode"):
-            continue
-        d = per.setdefault(name, [0.0, 0, 0])
-        d[0] += e["end_ms"] - e["start_ms"]
-        d[1] += e["bytes"]
-        d[2] += 1
-    if not per:
-        return None, {}
-    dom = max(per, key=lambda k: per[k][0])
-    ms, nbytes, n = per[dom]
-    achieved = nbytes / (ms / 1e3) / 1e9
-    table = {k: {"ms": round(v[0], 4), "launches": v[2], "GB/s": round(v[1] / (v[0] / 1e3) / 1e9, 1)}
-             for k, v in per.items()}
-    kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
-    traffic, tsrc = None, None
-    try:   # DRAM bytes per launch from a committed ncu capture of the same in-step launches
-        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)) as fh:
-            tj = json.load(fh)
-        if dom == "stencil":
-            traffic = int(tj["traffic_over_algorithmic"] * nbytes / n)
-            tsrc = (f"profiles/{TRAFFIC_JSON}: ncu dram read+write / algorithmic = "
-                    f"{tj['traffic_over_algorithmic']} on the same launches, x this run's algorithmic bytes per launch")
-    except Exception:
-        pass
-    return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": peak_gbs,
-            "peak_source": peak_src, "unit": "GB/s", "frac": round(achieved / peak_gbs, 4),
-            "traffic": traffic, "traffic_source": tsrc, "avg_launch_ms": round(ms / n, 4),
-            "algorithmic_bytes_per_launch": int(nbytes / n)}, table
-
-
-TRAFFIC_JSON = "r01_stencil_instep_traffic.json"
-ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
-
-
-def codec_alu_roofline(table) -> dict | None:
-    """The codec kernels are bound by the integer ALU pipe (IADD3/LOP3/SHF/PRMT,
-    DESIGN.md "Roofline"), not by HBM: their fraction is the ALU pipe's share of
-    its peak issue rate (148 SMs x 4 sub-partitions x one warp-instruction per
-    2 cycles at 1965 MHz = 581.6 G warp-instructions/s), measured by ncu
-    (sm__inst_executed_pipe_alu) on the committed capture of the same kernels."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01_ncu_kernels.json")) as fh:
-            kj = json.load(fh)
-    except Exception:
-        return None
+def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
+    fields = make_fields_c2()
+    steps, warmup = args.c2_steps, 3
+    cells = NX * NY * NZ * T * steps
+    OD = dict(m_resident=1)
+    OH = dict(serpentine=1, m_resident=1, slots=3)
+    PF = dict(serpentine=0, m_resident=0)
+    modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
+             ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
+    if not args.quick:
+        modes += [(f"r{r}_{k}", st, (r,) * 3, o) for r in (8, 24) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
+        modes += [("pf_zfp_dev", 1, (RATE,) * 3, PF), ("pf_zfp_host", 0, (RATE,) * 3, PF),
+                  ("pf_raw_dev", 1, (0, 0, 0), PF), ("pf_raw_host", 0, (0, 0, 0), PF)]
+        # the paper's codes 2-4 as fp32 rate vectors, out of core,
+        # paper-faithful schedule: one read-write field (u-, reading R7/R25) at 16/32,
+        # the read-only m at 16/32, one read-write field + m at 12/32 (the paper's 24/64)
+        modes += [("pm2_host", 0, (0, 16, 0), PF), ("pm3_host", 0, (0, 0, 16), PF),
+                  ("pm4_host", 0, (0, 12, 12), PF)]
+        modes += [(f"t{t}_{k}", st, (RATE,) * 3, dict(o, tb=t)) for t in (8, 12)
+                  for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
+        F = dict(PF, precision=64)
+        modes += [("f64raw_host", 0, (0, 0, 0), F), ("f64pm2_host", 0, (0, 32, 0), F),
+                  ("f64pm3_host", 0, (0, 0, 32), F), ("f64pm4_host", 0, (0, 24, 24), F),
+                  ("f64all_host", 0, (32, 32, 32), F), ("f64all_dev", 1, (32, 32, 32), F),
+                  ("f64raw_dev", 1, (0, 0, 0), F),
+                  ("f64allo_host", 0, (32, 32, 32), dict(OH, precision=64)),
+                  ("f64allo_dev", 1, (32, 32, 32), dict(OD, precision=64))]
     out = {}
-    for name, stage in (("zfp_decode_kernel", "decode"), ("zfp_encode_kernel", "encode")):
-        ks = [k for k in kj["kernels"] if k["kernel"].endswith(name)]
-        if not ks:
-            continue
-        k = ks[0]
-        frac = k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"] / 100.0
-        out[name] = {"bound": "alu", "achieved": round(frac * ALU_PEAK, 1), "peak": round(ALU_PEAK, 1),
-                     "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
-                     "issue_active": round(k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100, 4),
-                     "isolated_us": k["gpu__time_duration.sum"],
-                     "in_step_avg_ms": round(table[stage]["ms"] / table[stage]["launches"], 4) if stage in table else None,
-                     "source": "profiles/r01_ncu_kernels.json (ncu --set full, one C2 slab, rate 16)"}
-    return out or None
+    for label, store, rates, opt in modes:
+        log(f"c2 {label}")
+        tb = opt.get("tb", T)
+        prec = opt.get("precision", 32)
+        clk.active = True
+        dev_s, st, evs, launches, ctx = run_mode_c2(Z, store, rates, fields, device, steps, warmup,
+                                                    profile=int(label == "zfp_dev"),
+                                                    m_resident=opt.get("m_resident", 0), tb=tb, precision=prec,
+                                                    serpentine=opt.get("serpentine", 0), slots=opt.get("slots", 2),
+                                                    slab_sets=opt.get("slab_sets", 0))
+        clk.active = False
+        sw = max(st["sweeps"], 1)
+        out[label] = {"s": dev_s, "cups": cells // T * tb / dev_s, "launches": launches, "evs": evs,
+                      "h2d_per_sweep": st["h2d_bytes"] / sw, "d2h_per_sweep": st["d2h_bytes"] / sw}
+        if store == 1 or "pm" in label or label.startswith("f64") or label.endswith("raw_host"):
+            out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX),
+                                                                       np.float64 if prec == 64 else np.float32))
+        Z.oocz_destroy(ctx)
+    roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
+    err = rel_errors(out["zfp_dev"]["u"], out["raw_dev"]["u"])
+    err["steps"] = (warmup + steps) * T
+    v, e = out["zfp_dev"], out["zfp_host"]
+    rep = {"workload": f"C2: {NX}^3 fp32, DENSE(1) + LAYERED, P={P} ({NZ // P} z-blocks), T={T}",
+           "steps": steps, "warmup": warmup,
+           "value_hbm_resident": round(v["cups"], 1),
+           "e2e_out_of_core": round(e["cups"], 1),
+           "e2e_host_link_frac": round(max(e["h2d_per_sweep"], e["d2h_per_sweep"]) / (e["s"] / steps) / 1e9 /
+                                       link["concurrent_per_direction_GBps"], 4),
+           "e2e_h2d_bytes_per_step": int(e["h2d_per_sweep"]), "e2e_d2h_bytes_per_step": int(e["d2h_per_sweep"]),
+           "raw": {"value_hbm_resident": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1)},
+           "speedup_zfp_vs_raw": {"hbm_resident": round(v["cups"] / out["raw_dev"]["cups"], 3),
+                                  "out_of_core": round(e["cups"] / out["raw_host"]["cups"], 3)},
+           "max_rel_error": err,
+           "roofline_in_step": roof, "kernels_in_step": table, "lanes": lanes_summary(v["evs"]),
+           "schedule": "HBM-resident: m_resident=1; out of core: serpentine=1, m_resident=1, slots=3"}
+    if "pf_raw_host" in out:
+        rep["paper_faithful"] = {"value_hbm_resident": round(out["pf_zfp_dev"]["cups"], 1),
+                                 "e2e_out_of_core": round(out["pf_zfp_host"]["cups"], 1),
+                                 "raw_e2e": round(out["pf_raw_host"]["cups"], 1),
+                                 "speedup_out_of_core": round(out["pf_zfp_host"]["cups"] / out["pf_raw_host"]["cups"], 3)}
+        ref = out["pf_raw_host"]
+        pm = {"what": "PAPER.md:212-215 codes as rate vectors (u, u-, m); out of core; speedup vs code 1 "
+                      "(the paper: 1.16x / 1.18x / 1.20x, fp64, V100-PCIe); the one read-write dataset is u- "
+                      "(reading R25)", "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1)}}
+        for key, lab, rates in (("2_rw_16", "pm2_host", [0, 16, 0]), ("3_ro_16", "pm3_host", [0, 0, 16]),
+                                ("4_rw_ro_12", "pm4_host", [0, 12, 12])):
+            er = rel_errors(out[lab]["u"], ref["u"])
+            pm[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
+                       "speedup": round(out[lab]["cups"] / ref["cups"], 3),
+                       "normwise_max_rel_error": er["normwise_max"], "mean_pointwise_rel_error": er["mean_pointwise"]}
+        rep["paper_modes"] = pm
+        ref = out["f64raw_host"]
+        pf64 = {"what": "the paper's precision and rates (fp64; PAPER.md:208, :212-215): codes 1-4 out of core and "
+                        "every field at 32/64; speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, V100-PCIe)",
+                "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1),
+                               "value": round(out["f64raw_dev"]["cups"], 1)}}
+        for key, lab, rates in (("2_rw_32", "f64pm2_host", [0, 32, 0]), ("3_ro_32", "f64pm3_host", [0, 0, 32]),
+                                ("4_rw_ro_24", "f64pm4_host", [0, 24, 24]), ("all_32", "f64all_host", [32, 32, 32])):
+            er = rel_errors(out[lab]["u"], ref["u"])
+            pf64[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
+                         "speedup": round(out[lab]["cups"] / ref["cups"], 3),
+                         "normwise_max_rel_error": er["normwise_max"], "mean_pointwise_rel_error": er["mean_pointwise"]}
+        pf64["all_32"]["value"] = round(out["f64all_dev"]["cups"], 1)
+        pf64["all_32_orchestrated"] = {"e2e": round(out["f64allo_host"]["cups"], 1),
+                                       "value": round(out["f64allo_dev"]["cups"], 1)}
+        rep["paper_precision_fp64"] = pf64
+        rep["other_rates"] = {}
+        for r in (8, 24):
+            er = rel_errors(out[f"r{r}_dev"]["u"], out["raw_dev"]["u"])
+            rep["other_rates"][str(r)] = {"value_hbm_resident": round(out[f"r{r}_dev"]["cups"], 1),
+                                          "e2e": round(out[f"r{r}_host"]["cups"], 1),
+                                          "normwise_max_rel_error": er["normwise_max"]}
+        rep["temporal_blocking"] = {f"T={t}": {"value_hbm_resident": round(out[f"t{t}_dev"]["cups"], 1),
+                                               "e2e": round(out[f"t{t}_host"]["cups"], 1)} for t in (8, 12)}
+        rep["roofline_isolated"] = isolated_kernels(Z, fields, peak_gbs)
+    return rep
 
 
+# ---------------------------------------------------------------- GPU arm
 def gpu_arm(args):
     import torch
     rank = int(os.environ.get("RANK", "0"))
@@ -360,256 +734,116 @@ def gpu_arm(args):
     from paper_2109_05410_b200 import oocz as Z
     from paper_2109_05410_b200 import dist as D
     nccl_id = (lambda: D.share_nccl_id(dist, rank, Z.oocz_get_nccl_id, device="cuda")) if world > 1 else None
-    fields = make_fields(rank, NZ)
-    cells = NX * NY * NZ * world * T * args.steps
     peak_gbs, peak_src = peaks()
+    info = host_info()
     link = host_link_probe()
-    out = {}
     with ClockSampler(local) as clk:
-        # (label, store, rates, options).  The headline runs the library's fastest
-        # orchestration of the SAME computation (bit-identical results, tests):
-        # serpentine sweeps + m resident in HBM (readings R22/R23);
-        # "pf_*" are the paper-faithful schedule (ascending sweeps, m streamed).
-        # Each path runs its fastest schedule of the same computation: with the store
-        # in HBM m resident (serpentine sweeps save host-link bytes only, and the
-        # block at each turn serialises decode after its own encode); out of core
-        # serpentine + m resident + 3 staging slots.
-        OD = dict(m_resident=1)
-        OH = dict(serpentine=1, m_resident=1, slots=3)
-        PF = dict(serpentine=0, m_resident=0)
-        modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
-                 ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
-        # the single-GPU analyses (other rates, schedules, paper modes, fp64, T) run at
-        # N = 1; a multi-GPU run measures the headline paths only (each extra mode is
-        # another NCCL communicator and pinned store per rank)
-        if not args.quick and world == 1:   # configs[1]: rates 8/16/24
-            modes += [(f"r{r}_{k}", st, (r,) * 3, o) for r in (8, 24) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
-            # the paper-faithful schedule, and each orchestration alone
-            modes += [("pf_zfp_dev", 1, (RATE,) * 3, PF), ("pf_zfp_host", 0, (RATE,) * 3, PF),
-                      ("pf_raw_dev", 1, (0, 0, 0), PF), ("pf_raw_host", 0, (0, 0, 0), PF),
-                      ("mres_host", 0, (RATE,) * 3, dict(m_resident=1)),
-                      ("serp_dev", 1, (RATE,) * 3, dict(serpentine=1)), ("serp_host", 0, (RATE,) * 3, dict(serpentine=1)),
-                      ("sm_dev", 1, (RATE,) * 3, dict(serpentine=1, m_resident=1)),
-                      # two staging slots: the block after each turn re-reads its own rows
-                      ("sm2_host", 0, (RATE,) * 3, dict(serpentine=1, m_resident=1, slots=2))]
-            # the paper's codes 2-4 as fp32 rate vectors, out of core,
-            # paper-faithful schedule: one read-write field (u-, reading R7) at 16/32, the
-            # read-only m at 16/32, one read-write field + m at 12/32 (the paper's 24/64)
-            modes += [("pm2_host", 0, (0, 16, 0), PF), ("pm3_host", 0, (0, 0, 16), PF),
-                      ("pm4_host", 0, (0, 12, 12), PF)]
-            # temporal-blocking depth: T = 8 and the paper's T = 12
-            # (PAPER.md:217), same P = 128: host bytes per step fall as 1/T, redundant
-            # stencil work grows as 4(T-1)/P
-            modes += [(f"t{t}_{k}", st, (RATE,) * 3, dict(o, tb=t)) for t in (8, 12) for k, st, o in (("dev", 1, OD), ("host", 0, OH))]
-            # the paper's own precision (fp64) and rates 32/64, 24/64
-            # (PAPER.md:213-215): codes 1-4 out of core (paper-faithful schedule), plus all
-            # fields at 32/64 (paper-faithful and orchestrated)
-            F = dict(PF, precision=64)
-            modes += [("f64raw_host", 0, (0, 0, 0), F), ("f64pm2_host", 0, (0, 32, 0), F),
-                      ("f64pm3_host", 0, (0, 0, 32), F), ("f64pm4_host", 0, (0, 24, 24), F),
-                      ("f64all_host", 0, (32, 32, 32), F), ("f64all_dev", 1, (32, 32, 32), F),
-                      ("f64raw_dev", 1, (0, 0, 0), F),
-                      ("f64allo_host", 0, (32, 32, 32), dict(OH, precision=64)),
-                      ("f64allo_dev", 1, (32, 32, 32), dict(OD, precision=64))]
-        for label, store, rates, opt in modes:
-            tb = opt.get("tb", T)
-            prec = opt.get("precision", 32)
-            dev_s, st, evs, launches, ctx = run_mode(Z, store, rates, fields, rank, world, nccl_id, local,
-                                                     args.steps, args.warmup, dist,
-                                                     profile=int(label in ("zfp_dev", "zfp_host")),
-                                                     m_resident=opt.get("m_resident", 0), tb=tb,
-                                                     precision=prec, serpentine=opt.get("serpentine", 0),
-                                                     slots=opt.get("slots", 2),
-                                                     slab_sets=opt.get("slab_sets", 0))
-            sweeps_total = st["sweeps"]
-            cells_mode = cells // T * tb
-            out[label] = {"s": dev_s, "cups": cells_mode / dev_s, "launches": launches, "evs": evs,
-                          "h2d_per_sweep": st["h2d_bytes"] / max(sweeps_total, 1),
-                          "d2h_per_sweep": st["d2h_bytes"] / max(sweeps_total, 1),
-                          "halo_per_sweep": st["halo_bytes"] / max(sweeps_total, 1)}
-            if store == 1 or "pm" in label or label.startswith("f64") or label.endswith("raw_host"):
-                # final u^t, for the compressed-vs-raw error (same step count)
-                out[label]["u"] = Z.oocz_get_field(ctx, Z.OOCZ_U, np.empty((NZ, NY, NX),
-                                                                           np.float64 if prec == 64 else np.float32))
-            Z.oocz_destroy(ctx)
+        c3 = c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link, clk, info)
+        c2 = c2_arm(args, Z, local, peak_gbs, peak_src, link, clk) if world == 1 and not args.no_c2 else None
     clocks = clk.summary()
     if rank != 0:
         if dist:
             dist.destroy_process_group()
         return
-    roof, table = roofline(out["zfp_dev"]["evs"], peak_gbs, peak_src)
-    err = rel_errors(out["zfp_dev"]["u"], out["raw_dev"]["u"])
-    err["steps"] = (args.warmup + args.steps) * T
-    paper_modes = None
-    if "pm2_host" in out:
-        ref = out["pf_raw_host"]
-        paper_modes = {"what": "PAPER.md:212-215 codes as rate vectors (u, u-, m); out of core; "
-                               "speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, fp64, V100-PCIe)",
-                       "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1)}}
-        for key, lab, rates in (("2_rw_16", "pm2_host", [0, 16, 0]), ("3_ro_16", "pm3_host", [0, 0, 16]),
-                                ("4_rw_ro_12", "pm4_host", [0, 12, 12])):
-            er = rel_errors(out[lab]["u"], ref["u"])
-            paper_modes[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
-                                "speedup": round(out[lab]["cups"] / ref["cups"], 3),
-                                "normwise_max_rel_error": er["normwise_max"],
-                                "mean_pointwise_rel_error": er["mean_pointwise"]}
-    paper_fp64 = None
-    if "f64raw_host" in out:
-        ref = out["f64raw_host"]
-        paper_fp64 = {"what": "the paper's precision and rates (fp64; PAPER.md:208, :212-215): codes 1-4 out of core "
-                              "and every field at 32/64; speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, "
-                              "V100-PCIe)",
-                      "1_original": {"rates": [0, 0, 0], "e2e": round(ref["cups"], 1),
-                                     "value": round(out["f64raw_dev"]["cups"], 1)}}
-        for key, lab, rates in (("2_rw_32", "f64pm2_host", [0, 32, 0]), ("3_ro_32", "f64pm3_host", [0, 0, 32]),
-                                ("4_rw_ro_24", "f64pm4_host", [0, 24, 24]), ("all_32", "f64all_host", [32, 32, 32])):
-            er = rel_errors(out[lab]["u"], ref["u"])
-            paper_fp64[key] = {"rates": rates, "e2e": round(out[lab]["cups"], 1),
-                               "speedup": round(out[lab]["cups"] / ref["cups"], 3),
-                               "e2e_h2d_bytes_per_step": int(out[lab]["h2d_per_sweep"]),
-                               "normwise_max_rel_error": er["normwise_max"],
-                               "mean_pointwise_rel_error": er["mean_pointwise"]}
-        paper_fp64["all_32"]["value"] = round(out["f64all_dev"]["cups"], 1)
-        paper_fp64["all_32_orchestrated"] = {"rates": [32, 32, 32], "e2e": round(out["f64allo_host"]["cups"], 1),
-                                             "value": round(out["f64allo_dev"]["cups"], 1),
-                                             "speedup": round(out["f64allo_host"]["cups"] / ref["cups"], 3),
-                                             "schedule": "value: m resident; e2e: serpentine + m resident, 3 slots"}
-    orch = None
-    if "mres_host" in out:
-        orch = {"what": "SURVEY 8(f) row 2, beyond the paper, same bits: the paper-faithful schedule (ascending "
-                        "sweeps, m streamed), m decoded once and kept in HBM (m_resident=1, R23), serpentine "
-                        "sweeps (serpentine=1, R22), both (2 staging slots); the headline value runs m_resident, "
-                        "the headline e2e serpentine + m_resident with 3 staging slots"}
-        for key, dlab, hlab in (("paper_faithful", "pf_zfp_dev", "pf_zfp_host"),
-                                ("m_resident", "zfp_dev", "mres_host"), ("serpentine", "serp_dev", "serp_host"),
-                                ("serpentine+m_resident", "sm_dev", "sm2_host")):
-            dv, hs = out[dlab], out[hlab]
-            orch[key] = {"value": round(dv["cups"], 1), "e2e": round(hs["cups"], 1),
-                         "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
-                         "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
-                         "e2e_host_link_GBps": round(hs["h2d_per_sweep"] / (hs["s"] / args.steps) / 1e9, 2)}
-        if "zfp_host" in out:
-            hs = out["zfp_host"]
-            orch["serpentine+m_resident, 3 staging slots"] = {
-                "e2e": round(hs["cups"], 1), "e2e_h2d_bytes_per_step": int(hs["h2d_per_sweep"]),
-                "e2e_d2h_bytes_per_step": int(hs["d2h_per_sweep"]),
-                "e2e_d2h_GBps": round(hs["d2h_per_sweep"] / (hs["s"] / args.steps) / 1e9, 2)}
-    per_rate = {}
-    for r in (8, 24):
-        if f"r{r}_dev" in out:
-            er = rel_errors(out[f"r{r}_dev"]["u"], out["raw_dev"]["u"])
-            per_rate[str(r)] = {"value": round(out[f"r{r}_dev"]["cups"], 1),
-                                "e2e": round(out[f"r{r}_host"]["cups"], 1),
-                                "e2e_h2d_bytes_per_step": int(out[f"r{r}_host"]["h2d_per_sweep"]),
-                                "normwise_max_rel_error": er["normwise_max"],
-                                "mean_pointwise_rel_error": er["mean_pointwise"]}
-    iso = isolated_kernels(Z, fields, peak_gbs)
-    v, e = out["zfp_dev"], out["zfp_host"]
+    rep = c3_report(c3, args, world, link, peak_gbs, peak_src, info)
+    h = c3["headline"]
     line = {
         "metric": METRIC,
-        "value": round(v["cups"], 1),
+        "value": rep["value"],
         "unit": "cell-updates/s",
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": round(v["s"] * 1e3 / args.steps, 4),
+        "ms_per_step": rep["ms_per_step"],
         "higher_is_better": True,
-        "scaling": "weak",
+        "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f32",
-        "data": "synthetic (DENSE seed 1 wavefield, u- = u, LAYERED m; SURVEY 8(d))",
-        "config": {"workload": f"C2: {NX}^3 fp32 per GPU, 25-point leapfrog, P={P} ({NZ // P} z-blocks), "
-                               f"T={T}, ZFP rate {RATE} on u, u-, m; compressed store resident in HBM; "
-                               f"m decoded once (same bits as the paper's schedule)",
-                   "schedule": "value: m_resident=1; e2e: serpentine=1, m_resident=1, slots=3 (each path's "
-                               "fastest schedule, all bit-identical; the paper-faithful schedule and each "
-                               "orchestration alone: orchestrated.*)",
-                   "grid": [NX, NY, NZ * world], "tb": T, "block_planes": P, "rate": RATE,
+        "data": "synthetic, generated on the GPU (DENSE seed 2 wavefield, u- = u, LAYERED m; SURVEY 8(d))",
+        "config": {"workload": f"C3{' (C4: z-split over %d GPUs)' % world if world > 1 else ''}: "
+                               f"{C3N}x{C3N}x{C3Z} fp32 u, u-, m (309.2 GB raw) out of core, ZFP rate {RATE} on all "
+                               f"three fields (154.6 GB pinned host store), T={T}, P={h['P']} ({h['D']} z-blocks"
+                               f"{' per GPU' if world > 1 else ''})",
+                   "grid": [C3N, C3N, C3Z], "tb": T, "block_planes": h["P"], "rate": RATE,
+                   "schedule": "serpentine sweeps + m decoded once into HBM + 3 staging slots (the library's fastest "
+                               "schedule of the same computation, bit-identical to the paper's; the paper's own: "
+                               "c3_paper_faithful)",
                    "step": "one sweep = T leapfrog steps over the whole grid",
-                   "l2": "inputs larger than L2 (compressed store 768 MiB + 480 MiB slab per GPU)",
+                   "l2": "inputs larger than L2 (the state is 154.6 GB; each sweep streams all of it)",
                    "parallelism": f"z-slabs x{world}, NCCL compressed halos" if world > 1 else "single GPU"},
-        "e2e": {"value": round(e["cups"], 1), "unit": "cell-updates/s",
-                "h2d_bytes_per_step": int(e["h2d_per_sweep"]), "d2h_bytes_per_step": int(e["d2h_per_sweep"]),
-                "path": "oocz_step with the store in pinned host memory (the paper's out-of-core path)",
-                "host_link_GBps": {"h2d": round(e["h2d_per_sweep"] / (e["s"] / args.steps) / 1e9, 2),
-                                   "d2h": round(e["d2h_per_sweep"] / (e["s"] / args.steps) / 1e9, 2)},
-                # the out-of-core roofline: bytes the method must move per sweep in the
-                # busier direction (region sharing: every stored byte once H2D, the
-                # read-write ones once D2H; less with serpentine / m resident) over the
-                # measured concurrent pinned bandwidth per direction
-                "roofline": {"bound": "host-link",
-                             "achieved": round(max(e["h2d_per_sweep"], e["d2h_per_sweep"]) /
-                                               (e["s"] / args.steps) / 1e9, 2),
-                             "peak": link["concurrent_per_direction_GBps"], "unit": "GB/s",
-                             "frac": round(max(e["h2d_per_sweep"], e["d2h_per_sweep"]) / (e["s"] / args.steps) /
-                                           1e9 / link["concurrent_per_direction_GBps"], 4),
-                             "peak_source": "measured in this run (bench.host_link_probe)"},
-                "host_link_probe": link,
-                "lanes": lanes_summary(e["evs"])},
-        "raw": {"value": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1),
-                "e2e_h2d_bytes_per_step": int(out["raw_host"]["h2d_per_sweep"]),
-                "schedule": "the headline's (value: m resident; e2e: serpentine + m resident, 3 slots)"},
-        "speedup_zfp_vs_raw": {"value": round(v["cups"] / out["raw_dev"]["cups"], 3),
-                               "e2e": round(e["cups"] / out["raw_host"]["cups"], 3),
-                               "paper_context": "1.20x (fp64, V100-PCIe, PAPER.md:227)",
-                               **({"paper_faithful_e2e": round(out["pf_zfp_host"]["cups"] / out["pf_raw_host"]["cups"], 3)}
-                                  if "pf_raw_host" in out else {})},
-        "max_rel_error": err,
-        "gpu_launches": int(v["launches"]),
-        "roofline": roof,
-        "roofline_codec": codec_alu_roofline(table),
-        "kernels_in_step": table,
-        "lanes": lanes_summary(v["evs"]),
-        "roofline_isolated": iso,
-        "other_rates": per_rate,
-        "orchestrated": orch,
-        "paper_modes": paper_modes,
-        "paper_precision_fp64": paper_fp64,
-        "temporal_blocking": {f"T={t}": {"value": round(out[f"t{t}_dev"]["cups"], 1),
-                                         "e2e": round(out[f"t{t}_host"]["cups"], 1),
-                                         "e2e_h2d_bytes_per_step": int(out[f"t{t}_host"]["h2d_per_sweep"]),
-                                         "step": f"one sweep = {t} leapfrog steps"}
-                              for t in (8, 12) if f"t{t}_dev" in out} or None,
+        "e2e": rep["e2e"],
+        "roofline": rep["roofline"],
+        "roofline_host_link": rep["roofline_host_link"],
+        "gpu_launches": rep["gpu_launches"],
+        "kernels_in_step": rep["kernels_in_step"],
+        "roofline_codec": rep["codec_alu_roofline"],
+        "lanes": rep["lanes"],
+        "zfp_vs_raw": rep.get("zfp_vs_raw"),
+        "c3_paper_faithful": rep.get("c3_paper_faithful"),
+        "c3_hbm_resident": rep.get("c3_hbm_resident"),
+        "c3_arena": c3["arena"],
+        "headline_run": rep["headline_run"],
+        "c2": c2,
+        "host": info,
         "clocks": clocks,
     }
     if world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds)
+        log("cpu baseline")
+        line["cpu_baseline"] = cpu_baseline(seconds=args.cpu_seconds, info=info)
     print(json.dumps(line))
     if dist:
         dist.destroy_process_group()
 
 
 # ---------------------------------------------------------------- CPU oracle arm
-def _oracle_sweep_sample(planes: int):
-    """One sweep (T steps + round trips) of the oracle on a 512 x 512 x `planes`
-    sample of the workload; returns (cells*T, seconds)."""
+def _oracle_sweep_sample(planes: int, nx: int = C3N, ny: int = 64, z0: int = 0):
+    """One sweep (T steps + rate-16 round trips) of the oracle on an nx x ny x
+    `planes` box of the C3 workload (DENSE(2), LAYERED); returns (cells*T, s)."""
     import oracle
     from paper_2109_05410_b200 import synth
-    u = synth.dense(NX, NY, NZ, seed=1, z0=0, z1=planes)
-    m = synth.layered(NX, NY, NZ, z0=0, z1=planes)
+    u = synth.dense(nx, ny, C3Z, seed=C3SEED, z0=z0, z1=z0 + planes, y0=0, y1=ny, x0=0, x1=nx)
+    m = synth.layered(nx, ny, C3Z, z0=z0, z1=z0 + planes, y0=0, y1=ny, x0=0, x1=nx)
     t0 = time.perf_counter()
     oracle.advance(u, u, m, T, (RATE,) * 3, T)
     dt = time.perf_counter() - t0
-    return NX * NY * planes * T, dt
+    return nx * ny * planes * T, dt
 
 
-def cpu_baseline(seconds: float = 15.0):
-    """The oracle, as it stands, on the host cores: whole sweeps of the C2 grid
-    (or a slab of it) until about `seconds` of CPU work have been timed."""
+def _oracle_worker(args):
+    planes, seconds, z0 = args
+    n_tot, s_tot, k = 0, 0.0, 0
+    while s_tot < seconds and k < 16:
+        n, dt = _oracle_sweep_sample(planes, z0=z0)
+        n_tot += n
+        s_tot += dt
+        k += 1
+    return n_tot, s_tot, k
+
+
+def cpu_baseline(seconds: float = 15.0, info: dict | None = None):
+    """The oracle, as it stands (single-threaded C), on the host: whole sweeps of
+    4096 x 64 x 64 boxes of the C3 workload, (1) on one core and (2) as one
+    independent process per logical CPU (boxes at different z), each for about
+    `seconds`; cell-updates/s summed over the processes."""
+    import multiprocessing as mp
     import oracle
     oracle.build()
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    n, dt = _oracle_sweep_sample(64)                  # calibrate
-    planes = int(max(16, min(NZ, (seconds * n / dt) / (NX * NY * T))) // 4 * 4)
-    tot_n, tot_s, sweeps = 0, 0.0, 0
-    while tot_s < seconds and sweeps < 8:
-        n, dt = _oracle_sweep_sample(planes)
-        tot_n += n
-        tot_s += dt
-        sweeps += 1
-    return {"value": round(tot_n / tot_s, 1), "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
-            "sample": f"{sweeps} sweep(s) (T={T} steps + rate-{RATE} round trips each) of a {NX}x{NY}x{planes} "
-                      f"slab of the C2 workload, {tot_s:.1f} s of oracle time"}
+    info = info or host_info()
+    planes = 64
+    n1, s1, k1 = _oracle_worker((planes, seconds / 2, 0))
+    ncpu = os.cpu_count() or 1
+    # spawn, not fork: the parent holds CUDA and driver threads
+    with mp.get_context("spawn").Pool(ncpu) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_oracle_worker, [(planes, seconds / 2, (4 * i * planes) % (C3Z - planes)) for i in range(ncpu)])
+        wall = time.perf_counter() - t0
+    n_all = sum(r[0] for r in res)
+    return {"value": round(n_all / wall, 1), "unit": "cell-updates/s", "cores": ncpu, "kind": "oracle",
+            "sample": f"{ncpu} processes x {min(r[2] for r in res)}-{max(r[2] for r in res)} sweeps (T={T} steps + "
+                      f"rate-{RATE} round trips each) of 4096x64x{planes} boxes of the C3 workload, {wall:.1f} s "
+                      f"wall; the oracle itself is single-threaded C, run unchanged",
+            "single_thread": {"value": round(n1 / s1, 1), "sweeps": k1, "seconds": round(s1, 1)},
+            "host": {k: info.get(k) for k in ("model", "sockets", "physical_cores", "logical_cpus", "hypervisor")}}
 
 
 def reference_arm(args):
@@ -618,8 +852,8 @@ def reference_arm(args):
         return
     import oracle
     oracle.build()
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    planes = 32
+    info = host_info()
+    planes = 16
     for _ in range(args.warmup):
         _oracle_sweep_sample(planes)
     tot_n, tot_s = 0, 0.0
@@ -628,16 +862,17 @@ def reference_arm(args):
         tot_n += n
         tot_s += dt
     v = tot_n / tot_s
-    sample = (f"each step: one sweep (T={T} steps + rate-{RATE} round trips) of a {NX}x{NY}x{planes} "
-              f"slab of the C2 workload")
+    sample = (f"each step: one sweep (T={T} steps + rate-{RATE} round trips) of a 4096x64x{planes} box of the C3 "
+              f"workload (DENSE(2) + LAYERED), single-threaded oracle")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "cell-updates/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(tot_s * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": round(tot_s * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": f"C2 sample: {NX}x{NY}x{planes} of the {NX}^3 grid, T={T}, rate {RATE}"},
-        "cpu_baseline": {"value": round(v, 1), "unit": "cell-updates/s", "cores": cores, "kind": "oracle",
-                         "sample": sample},
+        "config": {"workload": f"C3 sample: 4096x64x{planes} boxes of the {C3N}x{C3N}x{C3Z} grid, T={T}, rate {RATE}"},
+        "cpu_baseline": {"value": round(v, 1), "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+                         "sample": sample, "host": {k: info.get(k) for k in ("model", "sockets", "physical_cores",
+                                                                             "logical_cpus")}},
         "e2e": {"value": round(v, 1), "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
 
@@ -645,12 +880,15 @@ def reference_arm(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=10, help="timed sweeps of the C3 headline")
     ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--sec-steps", type=int, default=3, help="timed sweeps of each secondary C3 run")
+    ap.add_argument("--c2-steps", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--quick", action="store_true", help="rate 16 and raw only")
+    ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="the C3 headline and C2 rate 16 / raw only")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)

@@ -148,10 +148,34 @@ oocz_status oocz_get_nccl_id(uint8_t id[128]);
 oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world,
                         const uint8_t* nccl_id /* NULL if world == 1 */,
                         int32_t device, oocz_ctx** out);
+/* Caller-owned host store (one pinned arena reused by several contexts in turn,
+ * e.g. the benchmark's schedules over one 155 GB store: pinning takes ~0.45 s
+ * per GiB, the allocation, not the stepping, would dominate).
+ *  - oocz_host_store_bytes: arena bytes a host-store context for (cfg, world)
+ *    needs on each rank (the three field stores, each rounded up to 4 KiB);
+ *    0 if nz is not divisible by world.
+ *  - oocz_host_alloc / oocz_host_free: pinned, portable host memory
+ *    (cudaHostAlloc); OOCZ_ECUDA if the allocation fails (oocz_last_error(NULL)).
+ *  - oocz_create_ex: oocz_create, but with store = OOCZ_STORE_HOST the stores
+ *    are carved from `host_arena` (pinned host memory of arena_bytes >=
+ *    oocz_host_store_bytes, else OOCZ_EINVAL / OOCZ_ECAPACITY), which the
+ *    caller owns and frees after oocz_destroy.  host_arena == NULL: the
+ *    context allocates its own (= oocz_create).  A non-NULL arena with
+ *    store = OOCZ_STORE_DEVICE is OOCZ_EINVAL.  One arena serves one live
+ *    context at a time. */
+size_t      oocz_host_store_bytes(const oocz_config* cfg, int32_t world);
+oocz_status oocz_host_alloc(size_t bytes, void** out);
+void        oocz_host_free(void* p);
+oocz_status oocz_create_ex(const oocz_config* cfg, int32_t rank, int32_t world,
+                           const uint8_t* nccl_id, int32_t device,
+                           void* host_arena, size_t arena_bytes, oocz_ctx** out);
 /* Copy this rank's slab (count = nx*ny*nz/world values: float for precision 32,
  * double for precision 64) of field f into the
  * store, compressing it on the GPU (the initial round trip).
- * Rejects NaN/Inf (OOCZ_ENONFINITE) and, for OOCZ_M, m < 0 or m > m_max (OOCZ_ECFL). */
+ * Rejects NaN/Inf (OOCZ_ENONFINITE) and, for OOCZ_M, m < 0 or m > m_max (OOCZ_ECFL),
+ * checked on the input AND on its fixed-rate round trip RT(m) (what the stencil
+ * reads).  Validation runs before anything is written: a rejected call leaves
+ * the previous field (store, set state) unchanged. */
 oocz_status oocz_set_field(oocz_ctx* ctx, int32_t field, const void* src, size_t count);
 oocz_status oocz_set_field_device(oocz_ctx* ctx, int32_t field, const void* d_src, size_t count);
 /* Advance n steps: floor(n/T) sweeps of T steps, then one sweep of n mod T.
@@ -171,7 +195,7 @@ oocz_status oocz_get_field(oocz_ctx* ctx, int32_t field, void* dst, size_t count
  * else host memory (pageable or pinned).  A field counts as set once every
  * block-row has been set (oocz_step needs all three; get_* needs the field);
  * set_field_planes applies the same checks as set_field to its planes (NaN /
- * Inf, m range) and, on failure, leaves those rows unset.  A device source is
+ * Inf, m range) and, on failure, leaves the context unchanged.  A device source is
  * read after a device-wide synchronisation (it may be produced on any stream);
  * the calls return once dst is written. */
 oocz_status oocz_set_field_planes(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes,

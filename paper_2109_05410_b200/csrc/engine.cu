@@ -170,10 +170,11 @@ struct oocz_ctx {
     std::vector<uint8_t*> in_slot, out_slot;
     size_t in_off[3] = {0, 0, 0}, out_off[2] = {0, 0};
     size_t in_slot_bytes = 0, out_slot_bytes = 0;
-    unsigned int* d_flags = nullptr;        // [0] scan flags, [1] fp32 max bits, [2..3] fp64 max bits
+    unsigned int* d_flags = nullptr;        // two scan records (input, RT(m)): [0] flags, [1] fp32 max bits, [2..3] fp64 max bits
     // store
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
     size_t store_bytes[3] = {0, 0, 0};
+    bool store_external = false;            // host store carved from a caller-owned arena (oocz_create_ex)
     // streams / events
     cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_enc = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_decoded[kMaxSets] = {}, ev_slab_free[kMaxSets] = {}, ev_stepped[kMaxSets] = {};
@@ -389,8 +390,12 @@ extern "C" oocz_status oocz_get_nccl_id(uint8_t id[128])
     return halo_get_unique_id(id) ? OOCZ_OK : OOCZ_ENCCL;
 }
 
+// bytes of one field's store, rounded up so that stores carved from one arena stay 4 KiB aligned
+static size_t arena_field_bytes(size_t b) { return (b + 4095) / 4096 * 4096; }
+
 static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
-                               int32_t device, HaloComm* preset_halo, oocz_ctx** out)
+                               int32_t device, HaloComm* preset_halo, uint8_t* arena, size_t arena_bytes,
+                               oocz_ctx** out)
 {
     if (!out) return OOCZ_EINVAL;
     *out = nullptr;
@@ -498,7 +503,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     }
     if (ctx->para)
         for (auto& q : ctx->pcopy) CKC(cudaMalloc(&q, (size_t)h * pb));
-    CKC(cudaMalloc(&ctx->d_flags, 4 * sizeof(unsigned int)));
+    CKC(cudaMalloc(&ctx->d_flags, 8 * sizeof(unsigned int)));
     if (cfg->m_resident) {
         CKC(cudaMalloc(&ctx->m_full, (size_t)(S + 2 * h) * pb));
         CKC(cudaMemset(ctx->m_full, 0, (size_t)(S + 2 * h) * pb));
@@ -512,9 +517,29 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             ctx->in_slot.push_back(a);
             ctx->out_slot.push_back(b);
         }
-        for (int f = 0; f < 3; f++) {
-            CKC(cudaHostAlloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1), cudaHostAllocDefault));
-            ctx->stats.host_bytes_pinned += ctx->store_bytes[f];
+        if (arena) {
+            size_t want = 0;
+            for (int f = 0; f < 3; f++) want += arena_field_bytes(ctx->store_bytes[f]);
+            cudaPointerAttributes pa{};
+            CKC(cudaPointerGetAttributes(&pa, arena));
+            if (pa.type != cudaMemoryTypeHost) {
+                fprintf(stderr, "oocz_create_ex: the arena is not pinned host memory\n");
+                return cleanup_fail(OOCZ_EINVAL);
+            }
+            if (arena_bytes < want) {
+                fprintf(stderr, "oocz_create_ex: arena %zu B < %zu B needed\n", arena_bytes, want);
+                return cleanup_fail(OOCZ_ECAPACITY);
+            }
+            ctx->store_external = true;
+            for (int f = 0; f < 3; f++) {
+                ctx->store[f] = arena;
+                arena += arena_field_bytes(ctx->store_bytes[f]);
+            }
+        } else {
+            for (int f = 0; f < 3; f++) {
+                CKC(cudaHostAlloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1), cudaHostAllocDefault));
+                ctx->stats.host_bytes_pinned += ctx->store_bytes[f];
+            }
         }
     } else {
         for (int f = 0; f < 3; f++) CKC(cudaMalloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1)));
@@ -593,7 +618,42 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
 extern "C" oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
                                    int32_t device, oocz_ctx** out)
 {
-    return create_impl(cfg, rank, world, nccl_id, device, nullptr, out);
+    return create_impl(cfg, rank, world, nccl_id, device, nullptr, nullptr, 0, out);
+}
+
+extern "C" oocz_status oocz_create_ex(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
+                                      int32_t device, void* host_arena, size_t arena_bytes, oocz_ctx** out)
+{
+    if (host_arena && cfg && cfg->store != OOCZ_STORE_HOST) return OOCZ_EINVAL;
+    return create_impl(cfg, rank, world, nccl_id, device, nullptr, static_cast<uint8_t*>(host_arena), arena_bytes,
+                       out);
+}
+
+extern "C" size_t oocz_host_store_bytes(const oocz_config* cfg, int32_t world)
+{
+    if (!cfg || world < 1 || cfg->nz % world) return 0;
+    size_t t = 0;
+    for (int f = 0; f < 3; f++)
+        t += arena_field_bytes((size_t)(cfg->nz / world / 4) *
+                               row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], esz_of(cfg)));
+    return t;
+}
+
+extern "C" oocz_status oocz_host_alloc(size_t bytes, void** out)
+{
+    if (!out) return OOCZ_EINVAL;
+    *out = nullptr;
+    const cudaError_t e = cudaHostAlloc(out, std::max<size_t>(bytes, 1), cudaHostAllocPortable);
+    if (e != cudaSuccess) {
+        *out = nullptr;
+        return stateless_status(e, "cudaHostAlloc");
+    }
+    return OOCZ_OK;
+}
+
+extern "C" void oocz_host_free(void* p)
+{
+    if (p) cudaFreeHost(p);
 }
 
 extern "C" oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t world, int32_t device,
@@ -622,7 +682,7 @@ extern "C" oocz_status oocz_create_local_group(const oocz_config* cfg, int32_t w
     std::vector<HaloComm*> halos(world, nullptr);
     for (int r = 0; r < world && hs; r++) halos[r] = hs[r];
     for (int r = 0; r < world; r++) {
-        st = create_impl(cfg, r, world, nullptr, device, halos[r], &outs[r]);
+        st = create_impl(cfg, r, world, nullptr, device, halos[r], nullptr, 0, &outs[r]);
         if (st != OOCZ_OK) {
             for (int k = 0; k < r; k++) { oocz_destroy(outs[k]); outs[k] = nullptr; }
             for (int k = r; k < world; k++) if (halos[k]) halo_destroy(halos[k]);
@@ -647,7 +707,9 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         for (int k = 0; k < oocz_ctx::kMaxSets; k++) cudaFree(ctx->slab[k][f]);
         cudaFree(ctx->ccopy[f]);
         if (f < 2) cudaFree(ctx->pcopy[f]);
-        if (ctx->cfg.store == OOCZ_STORE_HOST) cudaFreeHost(ctx->store[f]);
+        if (ctx->cfg.store == OOCZ_STORE_HOST) {
+            if (!ctx->store_external) cudaFreeHost(ctx->store[f]);
+        }
         else cudaFree(ctx->store[f]);
     }
     for (auto p : ctx->in_slot) cudaFree(p);
@@ -708,9 +770,39 @@ extern "C" oocz_status oocz_get_events(const oocz_ctx* ctx, oocz_event* evs, siz
 }
 
 // ------------------------------------------------------------------ set / get
+// Max |value| (as a double) and flags from one scan record of d_flags:
+// rec[0] bit 0 non-finite, bit 1 negative; rec[1] fp32 max bits; rec[2..3] fp64 max bits.
+static double scan_max(const oocz_ctx* ctx, const unsigned int* rec)
+{
+    if (ctx->esz == 8) {
+        double mx;
+        std::memcpy(&mx, &rec[2], sizeof mx);
+        return mx;
+    }
+    float m32;
+    std::memcpy(&m32, &rec[1], sizeof m32);
+    return m32;
+}
+
+static cudaError_t scan_planes(oocz_ctx* ctx, const uint8_t* buf, size_t n, unsigned int* rec, cudaStream_t s)
+{
+    if (ctx->esz == 8)
+        return launch_scan_field(reinterpret_cast<const double*>(buf), n, rec,
+                                 reinterpret_cast<unsigned long long*>(rec + 2), s);
+    return launch_scan_field(reinterpret_cast<const float*>(buf), n, rec, s);
+}
+
 // Compress planes [z0, z0 + nplanes) (rank-local, 4-aligned) of field f from src
 // into the store (the initial round trip).  The field counts as set
 // once every 4-plane row has been set; then its halos are (re)published.
+//
+// Two passes, so that a rejected call changes nothing ("a failed
+// validation leaves the state unchanged"):
+//   1. validate: every chunk is scanned for NaN / Inf and, for m, sign and the
+//      CFL bound -- both on the input and on its fixed-rate round trip RT(m),
+//      which is what the stencil will read (encode into scratch, decode, scan);
+//      nothing is written to the store, rows_set or m_full;
+//   2. write: encode into the store (and decode RT(m) into m_full if resident).
 static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int32_t nplanes, const void* src_v,
                                    bool on_device)
 {
@@ -725,27 +817,60 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     // a device source may still be being written on a stream of the caller's
     // (the copies below run on the library's own non-blocking stream)
     if (on_device) CK(cudaDeviceSynchronize());
-    // rows of this range count as unset until the call succeeds
-    for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 0;
-    ctx->field_set[field] = false;
-    std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     cudaStream_t s = ctx->s_comp;
-    const int chunk = ctx->P;                       // planes per pass, <= slab capacity
     const double mmax = ctx->esz == 8 ? cfl_limit(ctx->cfg.c64) : cfl_limit(ctx->cfg.c);
     const uint8_t* src = static_cast<const uint8_t*>(src_v);
     const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
-    CK(cudaMemsetAsync(ctx->d_flags, 0, 4 * sizeof(unsigned int), s));
+    const cudaMemcpyKind in_kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    const int rate = ctx->cfg.rate[field];
+    const bool check_rt = field == OOCZ_M && rate > 0;
+    // ---- pass 1: validate (scratch only: slab set 0, which holds nothing between steps)
+    {
+        // the encoded chunk goes to slab[0][1]: half a block of planes fits even at
+        // rate 64 in fp32 (8 B per value <= 4 B x (P + 2h) / (P / 2) planes)
+        const int chunk = check_rt ? std::max(4, ctx->P / 2 / 4 * 4) : ctx->P;
+        CK(cudaMemsetAsync(ctx->d_flags, 0, 8 * sizeof(unsigned int), s));
+        for (int z = z0; z < z0 + nplanes; z += chunk) {
+            const int np = std::min(chunk, z0 + nplanes - z);
+            const size_t n = (size_t)np * ctx->plane_elems;
+            uint8_t* buf = ctx->slab[0][0];
+            CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb, in_kind, s));
+            CK(scan_planes(ctx, buf, n, ctx->d_flags, s));
+            if (check_rt) {       // RT(m): encode -> decode over the raw chunk -> scan
+                uint8_t* enc = ctx->slab[0][1];
+                CK(encode_or_copy(ctx, field, buf, np, enc, s));
+                CK(decode_or_copy(ctx, field, enc, np, buf, s));
+                CK(scan_planes(ctx, buf, n, ctx->d_flags + 4, s));
+            }
+        }
+        unsigned int flags[8] = {};
+        CK(cudaMemcpyAsync(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (flags[0] & 1u) return fail(ctx, OOCZ_ENONFINITE, "field %d contains NaN or Inf", field);
+        if (field == OOCZ_M) {
+            if (flags[0] & 2u) return fail(ctx, OOCZ_ECFL, "m has negative values");
+            const double mx = scan_max(ctx, flags);
+            if (mx > mmax) return fail(ctx, OOCZ_ECFL, "max m (%.9g) > m_max(c) (%.9g)", mx, mmax);
+            if (check_rt) {
+                if (flags[4] & 1u)
+                    return fail(ctx, OOCZ_ENONFINITE, "m at rate %d decodes to NaN or Inf", rate);
+                if (flags[4] & 2u)
+                    return fail(ctx, OOCZ_ECFL, "m at rate %d decodes to negative values", rate);
+                const double mrt = scan_max(ctx, flags + 4);
+                if (mrt > mmax)
+                    return fail(ctx, OOCZ_ECFL, "max m decoded at rate %d (%.9g) > m_max(c) (%.9g)", rate, mrt, mmax);
+            }
+        }
+    }
+    // ---- pass 2: write.  Rows of this range count as unset until it succeeds.
+    for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 0;
+    ctx->field_set[field] = false;
+    std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
+    const int chunk = ctx->P;                       // planes per pass, <= slab capacity
     for (int z = z0; z < z0 + nplanes; z += chunk) {
         const int np = std::min(chunk, z0 + nplanes - z);
-        const size_t n = (size_t)np * ctx->plane_elems;
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
-        CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb,
-                           on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, s));
-        if (ctx->esz == 8)
-            CK(launch_scan_field(reinterpret_cast<const double*>(buf), n, ctx->d_flags,
-                                 reinterpret_cast<unsigned long long*>(ctx->d_flags + 2), s));
-        else
-            CK(launch_scan_field(reinterpret_cast<const float*>(buf), n, ctx->d_flags, s));
+        CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb, in_kind, s));
         const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         const uint8_t* coded;
@@ -761,23 +886,7 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
         if (field == OOCZ_M && ctx->m_full)         // m_resident: keep the decoded RT(m)
             CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->pb, s));
     }
-    unsigned int flags[4] = {0, 0, 0, 0};
-    CK(cudaMemcpyAsync(flags, ctx->d_flags, sizeof flags, cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (flags[0] & 1u) return fail(ctx, OOCZ_ENONFINITE, "field %d contains NaN or Inf", field);
-    if (field == OOCZ_M) {
-        double mx;
-        if (ctx->esz == 8) {
-            std::memcpy(&mx, &flags[2], sizeof mx);
-        } else {
-            float m32;
-            std::memcpy(&m32, &flags[1], sizeof m32);
-            mx = m32;
-        }
-        if (flags[0] & 2u) return fail(ctx, OOCZ_ECFL, "m has negative values");
-        if ((double)mx > mmax)
-            return fail(ctx, OOCZ_ECFL, "max m (%.9g) > m_max(c) (%.9g)", (double)mx, mmax);
-    }
     for (int r = z0 / 4; r < (z0 + nplanes) / 4; r++) ctx->rows_set[field][r] = 1;
     ctx->field_set[field] = std::all_of(ctx->rows_set[field].begin(), ctx->rows_set[field].end(),
                                         [](uint8_t v) { return v != 0; });

@@ -70,6 +70,11 @@ _SIGS = {
     "oocz_validate": (C.c_int, [C.POINTER(oocz_config), _i32, C.c_char_p, C.c_size_t]),
     "oocz_get_nccl_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "oocz_create": (C.c_int, [C.POINTER(oocz_config), _i32, _i32, C.POINTER(C.c_uint8), _i32, C.POINTER(_ctx_p)]),
+    "oocz_create_ex": (C.c_int, [C.POINTER(oocz_config), _i32, _i32, C.POINTER(C.c_uint8), _i32, _vp, C.c_size_t,
+                                 C.POINTER(_ctx_p)]),
+    "oocz_host_store_bytes": (C.c_size_t, [C.POINTER(oocz_config), _i32]),
+    "oocz_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(_vp)]),
+    "oocz_host_free": (None, [_vp]),
     "oocz_set_field": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_set_field_device": (C.c_int, [_ctx_p, _i32, _vp, C.c_size_t]),
     "oocz_step": (C.c_int, [_ctx_p, C.c_int64]),
@@ -225,6 +230,30 @@ def oocz_create(cfg: oocz_config, rank: int = 0, world: int = 1, nccl_id: bytes 
         idp = (C.c_uint8 * 128)(*nccl_id)
     _check(_lib.oocz_create(C.byref(cfg), rank, world, idp, device, C.byref(out)))
     return out.value
+
+
+def oocz_create_ex(cfg: oocz_config, rank: int = 0, world: int = 1, nccl_id: bytes | None = None,
+                   device: int = 0, host_arena: int | None = None, arena_bytes: int = 0) -> int:
+    out = _ctx_p()
+    idp = None
+    if nccl_id is not None:
+        idp = (C.c_uint8 * 128)(*nccl_id)
+    _check(_lib.oocz_create_ex(C.byref(cfg), rank, world, idp, device, host_arena, arena_bytes, C.byref(out)))
+    return out.value
+
+
+def oocz_host_store_bytes(cfg: oocz_config, world: int = 1) -> int:
+    return int(_lib.oocz_host_store_bytes(C.byref(cfg), world))
+
+
+def oocz_host_alloc(nbytes: int) -> int:
+    out = _vp()
+    _check(_lib.oocz_host_alloc(nbytes, C.byref(out)))
+    return out.value
+
+
+def oocz_host_free(p: int | None) -> None:
+    _lib.oocz_host_free(p)
 
 
 def oocz_create_local_group(cfg: oocz_config, world: int, device: int = 0) -> list[int]:

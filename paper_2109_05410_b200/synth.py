@@ -63,11 +63,17 @@ def dense_params(seed: int):
     return p
 
 
-def dense(nx: int, ny: int, nz: int, seed: int, z0: int = 0, z1: int | None = None) -> np.ndarray:
+def dense(nx: int, ny: int, nz: int, seed: int, z0: int = 0, z1: int | None = None,
+          y0: int = 0, y1: int | None = None, x0: int = 0, x1: int | None = None) -> np.ndarray:
+    """Box [z0, z1) x [y0, y1) x [x0, x1) of DENSE(seed) as fp32: the same
+    elementwise fp64 operations on sub-ranges of the index vectors, so a box
+    holds exactly the values of the whole field there."""
     z1 = nz if z1 is None else z1
-    out = np.zeros((z1 - z0, ny, nx), np.float64)
-    i = np.arange(nx, dtype=np.float64)
-    j = np.arange(ny, dtype=np.float64)
+    y1 = ny if y1 is None else y1
+    x1 = nx if x1 is None else x1
+    out = np.zeros((z1 - z0, y1 - y0, x1 - x0), np.float64)
+    i = np.arange(x0, x1, dtype=np.float64)
+    j = np.arange(y0, y1, dtype=np.float64)
     k = np.arange(z0, z1, dtype=np.float64)
     for lam, ph, a in dense_params(seed):
         sx = np.sin(2 * np.pi * i / lam[0] + ph[0])
@@ -77,15 +83,55 @@ def dense(nx: int, ny: int, nz: int, seed: int, z0: int = 0, z1: int | None = No
     return out.astype(np.float32)
 
 
-def layered(nx: int, ny: int, nz: int, z0: int = 0, z1: int | None = None) -> np.ndarray:
+def layered(nx: int, ny: int, nz: int, z0: int = 0, z1: int | None = None,
+            y0: int = 0, y1: int | None = None, x0: int = 0, x1: int | None = None) -> np.ndarray:
     z1 = nz if z1 is None else z1
-    i = np.arange(nx, dtype=np.float64)
-    j = np.arange(ny, dtype=np.float64)
+    y1 = ny if y1 is None else y1
+    x1 = nx if x1 is None else x1
+    i = np.arange(x0, x1, dtype=np.float64)
+    j = np.arange(y0, y1, dtype=np.float64)
     k = np.arange(z0, z1)
     vel = np.array([1500.0, 2500.0, 3500.0, 4500.0])[np.minimum((4 * k) // max(nz, 1), 3)]
     lat = 1.0 + 0.05 * np.sin(2 * np.pi * j / 97.0)[:, None] * np.sin(2 * np.pi * i / 89.0)[None, :]
     m = (vel[:, None, None] * lat[None, :, :] * 0.4 / 4500.0) ** 2
     return m.astype(np.float32)
+
+
+# ---- the same generators evaluated on the GPU, plane chunk by plane chunk, for
+# grids that never exist whole in host memory (C3: 3 x 103 GB).  The sin tables
+# are numpy's (fp64); the products and sums are the same fp64 operations in the
+# same order, so the values are bit-identical to dense() / layered() (checked
+# by tests/test_synth_gpu.py and on every run of the C3-scale parity test).
+
+def dense_torch(nx: int, ny: int, nz: int, seed: int, z0: int, z1: int, device="cuda"):
+    """Planes [z0, z1) of DENSE(seed) as an fp32 torch tensor on `device`."""
+    import torch
+    i = np.arange(nx, dtype=np.float64)
+    j = np.arange(ny, dtype=np.float64)
+    k = np.arange(z0, z1, dtype=np.float64)
+    out = torch.zeros((z1 - z0, ny, nx), dtype=torch.float64, device=device)
+    for lam, ph, a in dense_params(seed):
+        sx = torch.from_numpy(np.sin(2 * np.pi * i / lam[0] + ph[0])).to(device)
+        sy = torch.from_numpy(np.sin(2 * np.pi * j / lam[1] + ph[1])).to(device)
+        asz = torch.from_numpy(a * np.sin(2 * np.pi * k / lam[2] + ph[2])).to(device)   # a * sz, as numpy
+        out += asz[:, None, None] * (sy[:, None] * sx[None, :])[None, :, :]
+    return out.to(torch.float32)
+
+
+def layered_torch(nx: int, ny: int, nz: int, z0: int, z1: int, device="cuda", _lat={}):
+    """Planes [z0, z1) of LAYERED as an fp32 torch tensor on `device`."""
+    import torch
+    key = (nx, ny, str(device))
+    if key not in _lat:
+        i = np.arange(nx, dtype=np.float64)
+        j = np.arange(ny, dtype=np.float64)
+        lat = 1.0 + 0.05 * np.sin(2 * np.pi * j / 97.0)[:, None] * np.sin(2 * np.pi * i / 89.0)[None, :]
+        _lat.clear()
+        _lat[key] = torch.from_numpy(lat).to(device)
+    k = np.arange(z0, z1)
+    vel = torch.from_numpy(np.array([1500.0, 2500.0, 3500.0, 4500.0])[np.minimum((4 * k) // max(nz, 1), 3)]).to(device)
+    t = vel[:, None, None] * _lat[key][None, :, :] * 0.4 / 4500.0
+    return (t * t).to(torch.float32)
 
 
 def random_blocks(nblocks: int, seed: int) -> np.ndarray:

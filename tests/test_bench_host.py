@@ -55,7 +55,8 @@ def test_rel_errors_metrics():
 
 
 def test_codec_alu_roofline_from_committed_capture():
-    table = {"decode": {"ms": 2.0, "launches": 8}, "encode": {"ms": 1.0, "launches": 8}}
+    table = {"decode": {"ms": 2.0, "launches": 8, "avg_launch_ms": 0.25},
+             "encode": {"ms": 1.0, "launches": 8, "avg_launch_ms": 0.125}}
     r = bench.codec_alu_roofline(table)
     assert r is not None
     for k in ("zfp_decode_kernel", "zfp_encode_kernel"):
@@ -63,3 +64,11 @@ def test_codec_alu_roofline_from_committed_capture():
         assert r[k]["peak"] == pytest.approx(148 * 4 * 0.5 * 1.965, rel=1e-3)
         assert r[k]["achieved"] == pytest.approx(r[k]["frac"] * r[k]["peak"], rel=1e-2)
     assert r["zfp_decode_kernel"]["in_step_avg_ms"] == pytest.approx(0.25)
+
+
+def test_pick_P_and_host_info():
+    assert bench.pick_P(1536, 64) == 64 and bench.pick_P(1536, 192) == 192
+    assert bench.pick_P(192, 64) == 64 and bench.pick_P(768, 96) == 96
+    assert bench.pick_P(40, 64) == 40          # nothing fits: the whole slab
+    info = bench.host_info()
+    assert info["logical_cpus"] >= 1 and info.get("mem_total_bytes", 1) > 0

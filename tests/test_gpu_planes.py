@@ -73,15 +73,60 @@ def test_plane_range_errors_and_partial_state():
             z.oocz_get_field_planes(s.ctx, z.OOCZ_U, 0, np.empty((4, ny, nx), np.float32))
         assert e.value.status == z.OOCZ_ESTATE
         z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, u[16:])
+        before = [z.oocz_save_store(s.ctx, f) for f in range(3)]
         bad = u[16:24].copy()
         bad[3, 2, 1] = np.nan
-        with pytest.raises(z.OoczError) as e:            # a failed range leaves its rows unset
+        with pytest.raises(z.OoczError) as e:            # a rejected call changes nothing
             z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, bad)
         assert e.value.status == z.OOCZ_ENONFINITE
-        with pytest.raises(z.OoczError):
-            z.oocz_step(s.ctx, 2)
-        z.oocz_set_field_planes(s.ctx, z.OOCZ_U, 16, u[16:24])
-        z.oocz_step(s.ctx, 2)
+        for f in range(3):
+            assert np.array_equal(z.oocz_save_store(s.ctx, f), before[f])
+        z.oocz_step(s.ctx, 2)                            # the old field still steps, bit for bit
+        got = s.get(z.OOCZ_U)
+    want, _ = oracle.run(u, up, m, 2, (16, 16, 16), 2)
+    assert np.array_equal(bits(got), bits(want))
+
+
+@pytest.mark.parametrize("store,m_resident", [(0, 0), (1, 1)])
+def test_rejected_set_field_leaves_state_unchanged(store, m_resident):
+    """SURVEY 8(b) "A failed validation leaves the state unchanged": a set_field
+    rejected for NaN (u), or for m out of range (negative, above m_max, or a
+    round trip RT(m) above m_max) keeps the previous field, which then steps
+    bit-exactly like the oracle."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 24, 16, 32, 2, 16, (16, 12, 2)
+    u, up, m = _fields(nx, ny, nz)
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
+                                m_resident=m_resident)
+    mmax = z.oocz_cfl_limit(z.default_coeffs())
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        before = [z.oocz_save_store(s.ctx, f) for f in range(3)]
+        bad_u = u.copy()
+        bad_u[5, 3, 2] = np.inf
+        bad_neg = m.copy()
+        bad_neg[1, 1, 1] = -1e-3
+        bad_big = m.copy()
+        bad_big[7, 2, 9] = np.float32(mmax * 1.01)
+        # every value <= m_max, but rate 2 cannot hold the block: its round trip
+        # overshoots the bound (what the stencil would read)
+        edge = np.full_like(m, np.float32(mmax))
+        edge[::2, ::2, ::2] = 0.0
+        cases = [(z.OOCZ_U, bad_u, z.OOCZ_ENONFINITE), (z.OOCZ_M, bad_neg, z.OOCZ_ECFL),
+                 (z.OOCZ_M, bad_big, z.OOCZ_ECFL)]
+        if oracle.roundtrip(edge, rates[2]).max() > mmax:
+            cases.append((z.OOCZ_M, edge, z.OOCZ_ECFL))
+        for f, a, code in cases:
+            with pytest.raises(z.OoczError) as e:
+                z.oocz_set_field(s.ctx, f, a)
+            assert e.value.status == code, (f, code)
+            for g in range(3):
+                assert np.array_equal(z.oocz_save_store(s.ctx, g), before[g])
+        assert len(cases) == 4
+        s.step(3)
+        got = s.get(z.OOCZ_U)
+    want, _ = oracle.run(u, up, m, T, rates, 3)
+    assert np.array_equal(bits(got), bits(want))
 
 
 def test_chunked_set_fp64():
