@@ -23,7 +23,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SRCS = ["zfp_ref.c", "zfp_ref64.c", "stencil_ref.c", "ooc_emul.c"]
+_SRCS = ["zfp_ref.c", "zfp_ref64.c", "stencil_ref.c", "ooc_emul.c", "ooc_emul64.c"]
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lock = threading.Lock()
 _lib = None
@@ -85,6 +85,9 @@ def lib():
                 "orc_advance": (ci, [f32p, f32p, f32p, ci, ci, ci, f32p, ci, i32p, C.c_long]),
                 "orc_ooc_emulate": (ci, [f32p, f32p, f32p, ci, ci, ci, f32p, ci, ci, ci, i32p,
                                          C.c_long, ci, u64p]),
+                "orc64_ooc_emulate": (ci, [f64p, f64p, f64p, ci, ci, ci, f64p, ci, ci, ci, i32p,
+                                           C.c_long, ci, u64p]),
+                "orc_step_planes_f64": (None, [f64p, f64p, f64p, f64p, ci, ci, ci, f64p, ci, ci]),
                 "orc64_exponent_max": (C.c_int32, [f64p]),
                 "orc64_fwd_cast": (None, [f64p, ci, i64p]),
                 "orc64_inv_cast": (None, [i64p, ci, f64p]),
@@ -282,6 +285,22 @@ def run(u0, uprev0, m0, T: int, rates, nsteps: int, c=None):
     up = roundtrip(uprev0, rates[1])
     m = roundtrip(m0, rates[2])
     return advance(u, up, m, T, rates, nsteps, c)
+
+
+def ooc_emulate64(u0, uprev0, m0, T: int, P: int, G: int, rates, nsteps: int,
+                  poison: bool = False, c=None):
+    """fp64 twin of ooc_emulate (ooc_emul64.c): the literal region-by-region
+    out-of-core emulator in the paper's precision; returns (u, uprev, stats)."""
+    u, up, m = _f64(u0).copy(), _f64(uprev0).copy(), _f64(m0)
+    c = C64 if c is None else _f64(c)
+    nx, ny, nz = _shape3(u)
+    stats = np.zeros(3, np.uint64)
+    r = np.array(list(rates), np.int32)
+    rc = lib().orc64_ooc_emulate(u, up, m, nx, ny, nz, c, int(T), int(P), int(G), r,
+                                 int(nsteps), int(bool(poison)), stats)
+    if rc:
+        raise ValueError("orc64_ooc_emulate: bad arguments")
+    return u, up, {"h2d": int(stats[0]), "d2h": int(stats[1]), "halo": int(stats[2])}
 
 
 def ooc_emulate(u0, uprev0, m0, T: int, P: int, G: int, rates, nsteps: int,

@@ -31,36 +31,50 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Element type and the codec / stencil of that precision.  Defaults: fp32.
+ * ooc_emul64.c defines these for fp64 and includes this file (the schedule
+ * below is written once, for both precisions). */
+#ifndef OOC_REAL
+#define OOC_REAL float
+#define OOC_BYTES orc_zfp_bytes
+#define OOC_ENCODE orc_zfp_encode
+#define OOC_DECODE orc_zfp_decode
+#define OOC_STEP_PLANES orc_step_planes
+#define OOC_EMULATE orc_ooc_emulate
+#define OOC_NAN nanf("")
+#endif
+typedef OOC_REAL real;
+
 typedef struct {
     int z0, z1;          /* global planes [z0, z1) */
     size_t bytes;
-    void* payload;       /* uint64 words (rate > 0) or raw fp32 (rate == 0) */
+    void* payload;       /* uint64 words (rate > 0) or raw values (rate == 0) */
 } region_t;
 
 static size_t plane_elems(int nx, int ny) { return (size_t)nx * (size_t)ny; }
 
 static size_t region_bytes(int nx, int ny, int nplanes, int rate)
 {
-    if (rate == 0) return plane_elems(nx, ny) * (size_t)nplanes * sizeof(float);
-    return orc_zfp_bytes(nx, ny, nplanes, rate);
+    if (rate == 0) return plane_elems(nx, ny) * (size_t)nplanes * sizeof(real);
+    return OOC_BYTES(nx, ny, nplanes, rate);
 }
 
 /* compress planes src[0 .. nplanes) into a region payload */
-static void region_put(region_t* r, const float* src, int nx, int ny, int rate)
+static void region_put(region_t* r, const real* src, int nx, int ny, int rate)
 {
     int np = r->z1 - r->z0;
     r->bytes = region_bytes(nx, ny, np, rate);
     free(r->payload);
     r->payload = malloc(r->bytes ? r->bytes : 8);
     if (rate == 0) memcpy(r->payload, src, r->bytes);
-    else orc_zfp_encode(src, nx, ny, np, rate, (uint64_t*)r->payload);
+    else OOC_ENCODE(src, nx, ny, np, rate, (uint64_t*)r->payload);
 }
 
-static void region_get(const region_t* r, float* dst, int nx, int ny, int rate)
+static void region_get(const region_t* r, real* dst, int nx, int ny, int rate)
 {
     int np = r->z1 - r->z0;
     if (rate == 0) memcpy(dst, r->payload, r->bytes);
-    else orc_zfp_decode((const uint64_t*)r->payload, nx, ny, np, rate, dst);
+    else OOC_DECODE((const uint64_t*)r->payload, nx, ny, np, rate, dst);
 }
 
 /* region index: 2i = R_i, 2i+1 = C_i */
@@ -78,7 +92,7 @@ static void region_bounds(int g, int i_reg, int S, int P, int h, int D, int* z0,
 }
 
 /* decode the planes [z0, z1) of slab g's field from whichever region holds them */
-static void slab_planes(region_t* regs, int nreg, int z0, int z1, float* dst,
+static void slab_planes(region_t* regs, int nreg, int z0, int z1, real* dst,
                         int nx, int ny, int rate)
 {
     size_t pe = plane_elems(nx, ny);
@@ -86,16 +100,16 @@ static void slab_planes(region_t* regs, int nreg, int z0, int z1, float* dst,
         int a = regs[r].z0, b = regs[r].z1;
         int lo = z0 > a ? z0 : a, hi = z1 < b ? z1 : b;
         if (lo >= hi) continue;
-        float* tmp = (float*)malloc(pe * (size_t)(b - a) * sizeof(float) + 4);
+        real* tmp = (real*)malloc(pe * (size_t)(b - a) * sizeof(real) + 4);
         region_get(&regs[r], tmp, nx, ny, rate);
-        memcpy(dst + pe * (size_t)(lo - z0), tmp + pe * (size_t)(lo - a), pe * (size_t)(hi - lo) * sizeof(float));
+        memcpy(dst + pe * (size_t)(lo - z0), tmp + pe * (size_t)(lo - a), pe * (size_t)(hi - lo) * sizeof(real));
         free(tmp);
     }
 }
 
-static void poison_outside(float* buf, int zlo, int L, int nz, int v0, int v1, size_t pe)
+static void poison_outside(real* buf, int zlo, int L, int nz, int v0, int v1, size_t pe)
 {
-    const float nanv = nanf("");
+    const real nanv = OOC_NAN;
     for (int zl = 0; zl < L; zl++) {
         int z = zlo + zl;
         if (z < 0 || z >= nz) continue;         /* Dirichlet ghost planes stay 0 */
@@ -104,8 +118,8 @@ static void poison_outside(float* buf, int zlo, int L, int nz, int v0, int v1, s
     }
 }
 
-int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int nz,
-                    const float c[5], int T, int P, int G, const int rate[3],
+int OOC_EMULATE(real* u, real* uprev, const real* m, int nx, int ny, int nz,
+                const real c[5], int T, int P, int G, const int rate[3],
                     long nsteps, int poison, uint64_t stats[3])
 {
     const int h = 4 * T;
@@ -120,7 +134,7 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
     /* store[f][g][r] */
     region_t* store = (region_t*)calloc((size_t)3 * G * nreg, sizeof(region_t));
     #define REG(f, g, r) store[((size_t)(f) * G + (g)) * nreg + (r)]
-    const float* init[3] = { u, uprev, m };
+    const real* init[3] = { u, uprev, m };
     /* set_field: initial compression of every region of every field */
     for (int f = 0; f < 3; f++)
         for (int g = 0; g < G; g++)
@@ -131,8 +145,8 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
             }
 
     /* m halos (read-only): exchanged once, compressed (reading R20) */
-    float* mtop = (float*)calloc(pe * (size_t)h * G + 1, sizeof(float));
-    float* mbot = (float*)calloc(pe * (size_t)h * G + 1, sizeof(float));
+    real* mtop = (real*)calloc(pe * (size_t)h * G + 1, sizeof(real));
+    real* mbot = (real*)calloc(pe * (size_t)h * G + 1, sizeof(real));
     for (int g = 0; g < G; g++) {
         if (g > 0) {
             slab_planes(&REG(2, g - 1, 0), nreg, g * S - h, g * S, mtop + pe * (size_t)h * g, nx, ny, rate[2]);
@@ -145,17 +159,17 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
     }
 
     const int L = P + 2 * h;                    /* slab planes per block */
-    float* A = (float*)malloc(pe * L * sizeof(float) + 4);
-    float* B = (float*)malloc(pe * L * sizeof(float) + 4);
-    float* M = (float*)malloc(pe * L * sizeof(float) + 4);
-    float* ccopy[3];                            /* time-t copy of C_i */
-    float* keep[2];                             /* t+T values of C_i's upper half */
-    for (int f = 0; f < 3; f++) ccopy[f] = (float*)malloc(pe * 2 * h * sizeof(float) + 4);
-    for (int f = 0; f < 2; f++) keep[f] = (float*)malloc(pe * h * sizeof(float) + 4);
-    float* top[2]; float* bot[2];
+    real* A = (real*)malloc(pe * L * sizeof(real) + 4);
+    real* B = (real*)malloc(pe * L * sizeof(real) + 4);
+    real* M = (real*)malloc(pe * L * sizeof(real) + 4);
+    real* ccopy[3];                            /* time-t copy of C_i */
+    real* keep[2];                             /* t+T values of C_i's upper half */
+    for (int f = 0; f < 3; f++) ccopy[f] = (real*)malloc(pe * 2 * h * sizeof(real) + 4);
+    for (int f = 0; f < 2; f++) keep[f] = (real*)malloc(pe * h * sizeof(real) + 4);
+    real* top[2]; real* bot[2];
     for (int f = 0; f < 2; f++) {
-        top[f] = (float*)calloc(pe * (size_t)h * G + 1, sizeof(float));
-        bot[f] = (float*)calloc(pe * (size_t)h * G + 1, sizeof(float));
+        top[f] = (real*)calloc(pe * (size_t)h * G + 1, sizeof(real));
+        bot[f] = (real*)calloc(pe * (size_t)h * G + 1, sizeof(real));
     }
 
     long done = 0;
@@ -176,15 +190,15 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
         for (int g = 0; g < G; g++) {
             for (int i = 0; i < D; i++) {
                 const int zlo = g * S + i * P - h, zhi = g * S + (i + 1) * P + h;
-                float* F[3] = { A, B, M };
-                for (int f = 0; f < 3; f++) memset(F[f], 0, pe * L * sizeof(float));
+                real* F[3] = { A, B, M };
+                for (int f = 0; f < 3; f++) memset(F[f], 0, pe * L * sizeof(real));
                 /* top 2h planes: C_{i-1} from the previous block, or the halo from slab g-1 */
                 if (i > 0) {
-                    for (int f = 0; f < 3; f++) memcpy(F[f], ccopy[f], pe * 2 * h * sizeof(float));
+                    for (int f = 0; f < 3; f++) memcpy(F[f], ccopy[f], pe * 2 * h * sizeof(real));
                 } else if (g > 0) {
-                    memcpy(A, top[0] + pe * (size_t)h * g, pe * h * sizeof(float));
-                    memcpy(B, top[1] + pe * (size_t)h * g, pe * h * sizeof(float));
-                    memcpy(M, mtop + pe * (size_t)h * g, pe * h * sizeof(float));
+                    memcpy(A, top[0] + pe * (size_t)h * g, pe * h * sizeof(real));
+                    memcpy(B, top[1] + pe * (size_t)h * g, pe * h * sizeof(real));
+                    memcpy(M, mtop + pe * (size_t)h * g, pe * h * sizeof(real));
                 }
                 /* Fig. 4a: decompress this block's remainder and common region */
                 int regs[2] = { 2 * i, 2 * i + 1 };
@@ -197,16 +211,16 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
                     }
                 if (i == D - 1 && g < G - 1) {
                     int off = (g + 1) * S - zlo;
-                    memcpy(A + pe * (size_t)off, bot[0] + pe * (size_t)h * g, pe * h * sizeof(float));
-                    memcpy(B + pe * (size_t)off, bot[1] + pe * (size_t)h * g, pe * h * sizeof(float));
-                    memcpy(M + pe * (size_t)off, mbot + pe * (size_t)h * g, pe * h * sizeof(float));
+                    memcpy(A + pe * (size_t)off, bot[0] + pe * (size_t)h * g, pe * h * sizeof(real));
+                    memcpy(B + pe * (size_t)off, bot[1] + pe * (size_t)h * g, pe * h * sizeof(real));
+                    memcpy(M + pe * (size_t)off, mbot + pe * (size_t)h * g, pe * h * sizeof(real));
                 }
                 /* keep the time-t C_i for block i+1 (reading R14) */
                 if (i < D - 1)
                     for (int f = 0; f < 3; f++)
-                        memcpy(ccopy[f], F[f] + pe * (size_t)(P), pe * 2 * h * sizeof(float));
+                        memcpy(ccopy[f], F[f] + pe * (size_t)(P), pe * 2 * h * sizeof(real));
                 /* temporal blocking: step s updates the cone [zlo+4s, zhi-4s) */
-                float* cu = A; float* cp = B;
+                real* cu = A; real* cp = B;
                 for (int s = 1; s <= ts; s++) {
                     if (poison) {
                         poison_outside(cu, zlo, L, nz, zlo + 4 * (s - 1), zhi - 4 * (s - 1), pe);
@@ -215,26 +229,26 @@ int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int 
                     int g0 = zlo + 4 * s > 0 ? zlo + 4 * s : 0;
                     int g1 = zhi - 4 * s < nz ? zhi - 4 * s : nz;
                     /* in place: u+ overwrites u- (only the same point is read) */
-                    orc_step_planes(cu, cp, M, cp, nx, ny, L, c, g0 - zlo, g1 - zlo);
-                    float* t = cu; cu = cp; cp = t;
+                    OOC_STEP_PLANES(cu, cp, M, cp, nx, ny, L, c, g0 - zlo, g1 - zlo);
+                    real* t = cu; cu = cp; cp = t;
                 }
                 /* Fig. 4b: compress R_i and C_{i-1} and write them back */
-                float* out[2] = { cu, cp };
+                real* out[2] = { cu, cp };
                 for (int f = 0; f < 2; f++) {
                     region_t* R = &REG(f, g, 2 * i);
                     region_put(R, out[f] + pe * (size_t)(R->z0 - zlo), nx, ny, rate[f]);
                     stats[1] += R->bytes;
                     if (i > 0) {
                         region_t* C = &REG(f, g, 2 * i - 1);
-                        float* tmp = (float*)malloc(pe * 2 * h * sizeof(float));
-                        memcpy(tmp, keep[f], pe * h * sizeof(float));
-                        memcpy(tmp + pe * h, out[f] + pe * (size_t)h, pe * h * sizeof(float));
+                        real* tmp = (real*)malloc(pe * 2 * h * sizeof(real));
+                        memcpy(tmp, keep[f], pe * h * sizeof(real));
+                        memcpy(tmp + pe * h, out[f] + pe * (size_t)h, pe * h * sizeof(real));
                         region_put(C, tmp, nx, ny, rate[f]);
                         stats[1] += C->bytes;
                         free(tmp);
                     }
                     if (i < D - 1)  /* upper half of C_i: own planes, kept for block i+1 */
-                        memcpy(keep[f], out[f] + pe * (size_t)P, pe * h * sizeof(float));
+                        memcpy(keep[f], out[f] + pe * (size_t)P, pe * h * sizeof(real));
                 }
             }
         }

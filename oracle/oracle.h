@@ -89,6 +89,9 @@ void orc_step_f64(const double* u, const double* uprev, const double* m, double*
 void orc_step_planes(const float* u, const float* uprev, const float* m, float* out,
                      int nx, int ny, int nz, const float c[5], int z0, int z1);
 
+void orc_step_planes_f64(const double* u, const double* uprev, const double* m, double* out,
+                         int nx, int ny, int nz, const double c[5], int z0, int z1);
+
 /* the schedule the out-of-core method reduces to.
  * Advances (u, uprev) by nsteps: floor(n/T) sweeps of T steps and one of
  * n mod T, with RT_rate[f] applied to u and uprev after every sweep.
@@ -109,6 +112,11 @@ int orc64_advance(double* u, double* uprev, const double* m, int nx, int ny, int
 int orc_ooc_emulate(float* u, float* uprev, const float* m, int nx, int ny, int nz,
                     const float c[5], int T, int P, int G, const int rate[3],
                     long nsteps, int poison, uint64_t stats[3]);
+/* the same literal emulation in the paper's precision (fp64 fields, the fp64
+ * codec orc64_* and orc_step_planes_f64; ooc_emul64.c instantiates ooc_emul.c) */
+int orc64_ooc_emulate(double* u, double* uprev, const double* m, int nx, int ny, int nz,
+                      const double c[5], int T, int P, int G, const int rate[3],
+                      long nsteps, int poison, uint64_t stats[3]);
 
 #ifdef __cplusplus
 }

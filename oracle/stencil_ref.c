@@ -79,12 +79,14 @@ void orc_step(const float* u, const float* uprev, const float* m, float* out,
     orc_step_planes(u, uprev, m, out, nx, ny, nz, c, 0, nz);
 }
 
-void orc_step_f64(const double* u, const double* uprev, const double* m, double* out,
-                  int nx, int ny, int nz, const double c[5])
+void orc_step_planes_f64(const double* u, const double* uprev, const double* m, double* out,
+                         int nx, int ny, int nz, const double c[5], int z0, int z1)
 {
     const double c0x3 = 3.0 * c[0];
+    if (z0 < 0) z0 = 0;
+    if (z1 > nz) z1 = nz;
     #pragma omp parallel for schedule(static)
-    for (long z = 0; z < nz; z++)
+    for (long z = z0; z < z1; z++)
         for (long y = 0; y < ny; y++)
             for (long x = 0; x < nx; x++) {
                 size_t idx = ((size_t)z * ny + (size_t)y) * nx + (size_t)x;
@@ -103,6 +105,12 @@ void orc_step_f64(const double* u, const double* uprev, const double* m, double*
                 L = fma(c[4], s[4], L);
                 out[idx] = fma(m[idx], L, fma(2.0, u0, -uprev[idx]));
             }
+}
+
+void orc_step_f64(const double* u, const double* uprev, const double* m, double* out,
+                  int nx, int ny, int nz, const double c[5])
+{
+    orc_step_planes_f64(u, uprev, m, out, nx, ny, nz, c, 0, nz);
 }
 
 int orc_advance(float* u, float* uprev, const float* m, int nx, int ny, int nz,

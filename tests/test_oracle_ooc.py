@@ -91,3 +91,52 @@ def test_region_sharing_byte_accounting(G, rates):
     D = nz // G // P
     naive_planes = G * (D * P + 2 * h * (D - 1))
     assert naive_planes - nz == G * (D - 1) * 2 * h
+
+
+# ----------------------------------------------------------------------------
+# the paper's own precision (fp64; rates 32/64 and 24/64,
+# PAPER.md:213-215): the literal emulator instantiated in fp64
+# (oracle/ooc_emul64.c) pins the reduced fp64 schedule orc64_advance at
+# rates > 0, which no closed form reaches.
+
+def _fields64(nx, ny, nz, seed):
+    u = synth.dense(nx, ny, nz, seed=seed).astype(np.float64)
+    up = u * 0.97
+    return u, up, synth.layered(nx, ny, nz).astype(np.float64)
+
+
+@pytest.mark.parametrize("nx,ny,nz,T,P,G,n", CASES)
+@pytest.mark.parametrize("rates", [(32, 32, 32), (0, 24, 24), (0, 32, 0), (16, 40, 8)])
+def test_compressed_ooc_equals_round_trip_schedule_fp64(nx, ny, nz, T, P, G, n, rates):
+    u, up, m = _fields64(nx, ny, nz, 24)
+    ru, rup = oracle.run64(u, up, m, T, rates, n)
+    eu, eup, st = oracle.ooc_emulate64(u, up, m, T, P, G, rates, n)
+    assert np.array_equal(eu.view(np.uint64), ru.view(np.uint64))
+    assert np.array_equal(eup.view(np.uint64), rup.view(np.uint64))
+    if n:
+        # rate r: 8r bytes per 4^3 block, raw: 8 B per value
+        rb = [(nx // 4) * (ny // 4) * 8 * r if r else nx * ny * 4 * 8 for r in rates]   # per block-row
+        sweeps = -(-n // T)
+        assert st["h2d"] == sweeps * sum(rb[f] * nz // 4 for f in range(3))
+        assert st["d2h"] == sweeps * sum(rb[f] * nz // 4 for f in range(2))
+
+
+def test_fp64_emulator_poisoned_cone_and_paper_decomposition():
+    # NaN outside the valid cone changes nothing; the paper's D = 8, T = 12 shape
+    u, up, m = _fields64(8, 8, 8 * 96, 25)
+    rates = (0, 24, 24)                                 # the paper's code 4
+    ru, rup = oracle.run64(u, up, m, 12, rates, 24)
+    eu, eup, _ = oracle.ooc_emulate64(u, up, m, 12, 96, 1, rates, 24, poison=True)
+    assert np.array_equal(eu.view(np.uint64), ru.view(np.uint64))
+    assert np.array_equal(eup.view(np.uint64), rup.view(np.uint64))
+
+
+def test_fp64_raw_schedule_is_plain_fp64_steps():
+    u, up, m = _fields64(8, 8, 48, 26)
+    a, b = u.copy(), up.copy()
+    for _ in range(5):
+        nxt = np.empty_like(a)
+        oracle.lib().orc_step_f64(a, b, m, nxt, 8, 8, 48, oracle.C64)
+        a, b = nxt, a
+    eu, eup, _ = oracle.ooc_emulate64(u, up, m, 2, 16, 1, (0, 0, 0), 5)
+    assert np.array_equal(eu, a) and np.array_equal(eup, b)

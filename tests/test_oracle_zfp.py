@@ -185,6 +185,84 @@ def test_xform_delta_is_outer_product_of_first_column():
     assert np.array_equal(got, want)
 
 
+def test_forward_lift_worked_example_with_truncation():
+    # (3, 1, 4, 1) by hand through the lifting steps of SURVEY App. A:
+    #   x += w -> 4; x >>= 1 -> 2; w -= x -> -1
+    #   z += y -> 5; z >>= 1 -> 2; y -= z -> -1
+    #   x += z -> 4; x >>= 1 -> 2; z -= x -> 0
+    #   w += y -> -2; w >>= 1 -> -1; y -= w -> 0
+    #   w += y >> 1 -> -1; y -= w >> 1 -> 0 - (-1) = 1
+    # (the exact A v = (2.25, 0.4375, 0.25, -1.375): the >>1 truncations matter)
+    assert list(oracle.fwd_lift([3, 1, 4, 1])) == [2, 1, 0, -1]
+    # e0 impulses: (2,0,0,0) -> (0,2,0,-1), (3,0,0,0) -> (0,2,0,-1),
+    # (1,0,0,0) -> 0, (-1,0,0,0) -> (-1,0,1,0)   (same steps by hand)
+    assert list(oracle.fwd_lift([2, 0, 0, 0])) == [0, 2, 0, -1]
+    assert list(oracle.fwd_lift([3, 0, 0, 0])) == [0, 2, 0, -1]
+    assert list(oracle.fwd_lift([1, 0, 0, 0])) == [0, 0, 0, 0]
+    assert list(oracle.fwd_lift([-1, 0, 0, 0])) == [-1, 0, 1, 0]
+
+
+def test_inverse_lift_worked_example_with_truncation():
+    # inv of (0, v, 0, 0) by hand: y += w>>1 -> v; w -= y>>1 -> -(v>>1);
+    # y += w -> v - (v>>1); w <<= 1; w -= y -> -(v>>1) - v; z += x -> 0 ...
+    # = (v + (v>>1), v - (v>>1), -(v - (v>>1)), -(v + (v>>1)))
+    for v, want in ((3, [4, 2, -2, -4]), (4, [6, 2, -2, -6]), (2, [3, 1, -1, -3]), (-2, [-3, -1, 1, 3]),
+                    (-4, [-6, -2, 2, 6]), (1, [1, 1, -1, -1]), (-1, [-2, 0, 0, 2])):
+        assert list(oracle.inv_lift([0, v, 0, 0])) == want, v
+
+
+def test_forward_xform_axis_order_x_then_y_then_z():
+    # A lone value 3 at l = 0 through the 3-D forward transform, by hand, with
+    # the 1-D results pinned above (l = i + 4j + 16k):
+    #   x (j=k=0):   (3,0,0,0) -> (0,2,0,-1)          at i = 0..3
+    #   y (i=1):     (2,0,0,0) -> (0,2,0,-1)          -> l = 5: 2, l = 13: -1
+    #     (i=3):     (-1,0,0,0) -> (-1,0,1,0)         -> l = 3: -1, l = 11: 1
+    #   z (l=5):     (2,0,0,0) -> (0,2,0,-1)          -> l = 21: 2, l = 53: -1
+    #     (l=13):    (-1,0,0,0) -> (-1,0,1,0)         -> l = 13: -1, l = 45: 1
+    #     (l=3):     (-1,0,0,0) -> (-1,0,1,0)         -> l = 3: -1, l = 35: 1
+    #     (l=11):    (1,0,0,0) -> 0
+    q = np.zeros(64, np.int64)
+    q[0] = 3
+    want = np.zeros(64, np.int64)
+    want[[3, 13, 21, 35, 45, 53]] = [-1, -1, 2, 1, 1, -1]
+    got = oracle.fwd_xform(q).astype(np.int64)
+    assert np.array_equal(got, want)
+    # the other order (z, y, x) gives the i <-> k transpose, which differs
+    zyx = want.reshape(4, 4, 4).transpose(2, 1, 0).reshape(64)
+    assert not np.array_equal(zyx, want)
+
+
+def test_inverse_xform_axis_order_z_then_y_then_x():
+    # A lone coefficient 3 at (i, j, k) = (1, 0, 1), l = 17, through the inverse:
+    #   z (i=1, j=0): (0,3,0,0) -> b = (4,2,-2,-4) along k
+    #   y (i=1, each k): (b_k,0,0,0) -> constant b_k along j
+    #   x (each j, k):  (0,b_k,0,0) -> row_k = inv(0,b_k,0,0) along i:
+    #     k=0: (6,2,-2,-6)  k=1: (3,1,-1,-3)  k=2: (-3,-1,1,3)  k=3: (-6,-2,2,6)
+    q = np.zeros(64, np.int64)
+    q[17] = 3
+    rows = np.array([[6, 2, -2, -6], [3, 1, -1, -3], [-3, -1, 1, 3], [-6, -2, 2, 6]], np.int64)
+    want = np.repeat(rows[:, None, :], 4, axis=1)          # [k][j][i]
+    got = oracle.inv_xform(q).astype(np.int64).reshape(4, 4, 4)
+    assert np.array_equal(got, want)
+    assert not np.array_equal(want.transpose(2, 1, 0), want)   # x-first would differ
+
+
+def test_xform_axis_order_fp64_twin():
+    # the fp64 codec's int64 lifting runs the same steps in the same axis order
+    q = np.zeros(64, np.int64)
+    q[0] = 3
+    want = np.zeros(64, np.int64)
+    want[[3, 13, 21, 35, 45, 53]] = [-1, -1, 2, 1, 1, -1]
+    a = q.copy()
+    oracle.lib().orc64_fwd_xform(a)
+    assert np.array_equal(a, want)
+    b = np.zeros(64, np.int64)
+    b[17] = 3
+    oracle.lib().orc64_inv_xform(b)
+    rows = np.array([[6, 2, -2, -6], [3, 1, -1, -3], [-3, -1, 1, 3], [-6, -2, 2, 6]], np.int64)
+    assert np.array_equal(b.reshape(4, 4, 4), np.repeat(rows[:, None, :], 4, axis=1))
+
+
 def test_forward_coefficients_fit_guard_bits():
     # |q| < 2^30 on input, so the transform never wraps (max |coeff| < 2^31)
     rng = np.random.default_rng(6)
