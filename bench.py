@@ -809,40 +809,46 @@ def _oracle_sweep_sample(planes: int, nx: int = C3N, ny: int = 64, z0: int = 0):
     return nx * ny * planes * T, dt
 
 
-def _oracle_worker(args):
-    planes, seconds, z0 = args
+def _oracle_timed(planes: int, seconds: float, max_sweeps: int = 16) -> dict:
     n_tot, s_tot, k = 0, 0.0, 0
-    while s_tot < seconds and k < 16:
-        n, dt = _oracle_sweep_sample(planes, z0=z0)
+    while s_tot < seconds and k < max_sweeps:
+        n, dt = _oracle_sweep_sample(planes)
         n_tot += n
         s_tot += dt
         k += 1
-    return n_tot, s_tot, k
+    return {"n": n_tot, "s": s_tot, "sweeps": k}
 
 
-def cpu_baseline(seconds: float = 15.0, info: dict | None = None):
-    """The oracle, as it stands (single-threaded C), on the host: whole sweeps of
-    4096 x 64 x 64 boxes of the C3 workload, (1) on one core and (2) as one
-    independent process per logical CPU (boxes at different z), each for about
-    `seconds`; cell-updates/s summed over the processes."""
-    import multiprocessing as mp
+def _oracle_subprocess(threads: int, seconds: float, planes: int) -> dict:
+    """The oracle in a fresh process with OMP_NUM_THREADS = threads (its stencil
+    loops are OpenMP; the codec round trips are serial C)."""
+    env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+    out = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-sample", str(seconds),
+                          "--oracle-planes", str(planes)], capture_output=True, text=True, env=env,
+                         timeout=600 + 4 * seconds)
+    if out.returncode:
+        raise RuntimeError(out.stderr[-500:])
+    return json.loads(out.stdout.strip().splitlines()[-1])
+
+
+def cpu_baseline(seconds: float = 16.0, info: dict | None = None):
+    """The oracle, as it stands (C, OpenMP stencil loops, serial codec), timed
+    on the host: whole sweeps of 4096 x 64 x 64 boxes of the C3 workload with
+    all logical CPUs (OMP_NUM_THREADS = nproc) and with one thread, each for
+    about seconds / 2."""
     import oracle
     oracle.build()
     info = info or host_info()
     planes = 64
-    n1, s1, k1 = _oracle_worker((planes, seconds / 2, 0))
     ncpu = os.cpu_count() or 1
-    # spawn, not fork: the parent holds CUDA and driver threads
-    with mp.get_context("spawn").Pool(ncpu) as pool:
-        t0 = time.perf_counter()
-        res = pool.map(_oracle_worker, [(planes, seconds / 2, (4 * i * planes) % (C3Z - planes)) for i in range(ncpu)])
-        wall = time.perf_counter() - t0
-    n_all = sum(r[0] for r in res)
-    return {"value": round(n_all / wall, 1), "unit": "cell-updates/s", "cores": ncpu, "kind": "oracle",
-            "sample": f"{ncpu} processes x {min(r[2] for r in res)}-{max(r[2] for r in res)} sweeps (T={T} steps + "
-                      f"rate-{RATE} round trips each) of 4096x64x{planes} boxes of the C3 workload, {wall:.1f} s "
-                      f"wall; the oracle itself is single-threaded C, run unchanged",
-            "single_thread": {"value": round(n1 / s1, 1), "sweeps": k1, "seconds": round(s1, 1)},
+    allc = _oracle_subprocess(ncpu, seconds / 2, planes)
+    one = _oracle_subprocess(1, seconds / 2, planes)
+    return {"value": round(allc["n"] / allc["s"], 1), "unit": "cell-updates/s", "cores": ncpu, "kind": "oracle",
+            "sample": f"{allc['sweeps']} sweep(s) (T={T} steps + rate-{RATE} round trips each) of a "
+                      f"4096x64x{planes} box of the C3 workload (DENSE(2) + LAYERED), {allc['s']:.1f} s, "
+                      f"OMP_NUM_THREADS={ncpu}",
+            "single_thread": {"value": round(one["n"] / one["s"], 1), "sweeps": one["sweeps"],
+                              "seconds": round(one["s"], 1)},
             "host": {k: info.get(k) for k in ("model", "sockets", "physical_cores", "logical_cpus", "hypervisor")}}
 
 
@@ -863,14 +869,15 @@ def reference_arm(args):
         tot_s += dt
     v = tot_n / tot_s
     sample = (f"each step: one sweep (T={T} steps + rate-{RATE} round trips) of a 4096x64x{planes} box of the C3 "
-              f"workload (DENSE(2) + LAYERED), single-threaded oracle")
+              f"workload (DENSE(2) + LAYERED), the oracle's OpenMP stencil on all logical CPUs")
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": round(v, 1), "unit": "cell-updates/s",
         "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(tot_s * 1e3 / args.steps, 3), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C3 sample: 4096x64x{planes} boxes of the {C3N}x{C3N}x{C3Z} grid, T={T}, rate {RATE}"},
-        "cpu_baseline": {"value": round(v, 1), "unit": "cell-updates/s", "cores": 1, "kind": "oracle",
+        "cpu_baseline": {"value": round(v, 1), "unit": "cell-updates/s",
+                         "cores": int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1)), "kind": "oracle",
                          "sample": sample, "host": {k: info.get(k) for k in ("model", "sockets", "physical_cores",
                                                                              "logical_cpus")}},
         "e2e": {"value": round(v, 1), "unit": "cell-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -889,7 +896,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
     ap.add_argument("--quick", action="store_true", help="the C3 headline and C2 rate 16 / raw only")
+    ap.add_argument("--oracle-sample", type=float, default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--oracle-planes", type=int, default=64, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.oracle_sample is not None:           # cpu_baseline's child process
+        import oracle
+        oracle.build()
+        print(json.dumps(_oracle_timed(args.oracle_planes, args.oracle_sample)))
+        return
     if args.warmup < 3:
         print("warning: --warmup < 3 is below the timing rules", file=sys.stderr)
     if args.impl == "reference":
