@@ -179,7 +179,7 @@ struct oocz_ctx {
     cudaStream_t s_h2d = nullptr, s_dec = nullptr, s_comp = nullptr, s_enc = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_decoded[kMaxSets] = {}, ev_slab_free[kMaxSets] = {}, ev_stepped[kMaxSets] = {};
     cudaEvent_t ev_join_enc = nullptr;
-    cudaEvent_t ev_halo = nullptr, ev_join_dec = nullptr;
+    cudaEvent_t ev_join_dec = nullptr;
     std::vector<cudaEvent_t> ev_in_ready, ev_in_free, ev_out_ready, ev_out_free, ev_written, ev_encoded;
     long long seq = 0;                      // global block sequence number
     std::vector<int> last_slot;             // staging slot of each block's latest encode (host store)
@@ -572,7 +572,6 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         CKC(cudaEventCreateWithFlags(&ctx->ev_stepped[k], cudaEventDisableTiming));
     }
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_enc, cudaEventDisableTiming));
-    CKC(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_dec, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&ctx->ev_g_fork, cudaEventDisableTiming));
     for (auto& e : ctx->ev_g_join) CKC(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -732,7 +731,6 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         if (ctx->ev_slab_free[k]) cudaEventDestroy(ctx->ev_slab_free[k]);
         if (ctx->ev_stepped[k]) cudaEventDestroy(ctx->ev_stepped[k]);
     }
-    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
     if (ctx->ev_join_dec) cudaEventDestroy(ctx->ev_join_dec);
     for (auto& kv : ctx->graph_cache) cudaGraphExecDestroy(kv.second.exec);
     if (ctx->ev_g_fork) cudaEventDestroy(ctx->ev_g_fork);
@@ -1192,7 +1190,6 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     }
     if (ctx->halo) {  // neighbour-rank halos received at the sweep start
         std::string herr;
-        CK(cudaStreamWaitEvent(sd, ctx->ev_halo, 0));
         if (!halo_insert(ctx->halo, i == 0, i == D - 1, slab, g.slab0, S, ctx->nx, ctx->ny, sd, &herr))
             return fail(ctx, OOCZ_ENCCL, "halo insert: %s", herr.c_str());
     }
@@ -1349,6 +1346,7 @@ static oocz_status step_begin(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t* base)
     CK(cudaStreamWaitEvent(ctx->s_enc, ctx->ev_t0, 0));
     CK(cudaStreamWaitEvent(ctx->s_dec, ctx->ev_t0, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_t0, 0));
+    halo_step_begin(ctx->halo);
     return OOCZ_OK;
 }
 
@@ -1364,7 +1362,15 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_dec, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_h2d, 0));
     CK(cudaStreamWaitEvent(ctx->s_d2h, ctx->ev_join_comp, 0));
+    if (ctx->halo) {
+        std::string herr;
+        if (!halo_join(ctx->halo, ctx->s_d2h, &herr)) return fail(ctx, OOCZ_ECUDA, "halo join: %s", herr.c_str());
+    }
     CK(cudaEventRecord(ctx->ev_t1, ctx->s_d2h));
+    if (ctx->halo) {      // NCCL: poll for asynchronous communicator errors instead of hanging
+        std::string herr;
+        if (!halo_wait(ctx->halo, ctx->ev_t1, &herr)) return fail(ctx, OOCZ_ENCCL, "halo: %s", herr.c_str());
+    }
     CK(cudaStreamSynchronize(ctx->s_h2d));
     CK(cudaStreamSynchronize(ctx->s_comp));
     CK(cudaStreamSynchronize(ctx->s_enc));
@@ -1534,14 +1540,12 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
         for (int r = 0; r < n; r++) {
             oocz_ctx* ctx = ctxs[r];
             if (ctx->halo) {
+                // both directions start as soon as their own captures (previous
+                // sweep) and inserts are done, on the halo's own streams
                 std::string herr;
                 CK(cudaSetDevice(ctx->device));
-                // the previous sweep's halo captures ran on the encode stream
-                CK(cudaEventRecord(ctx->ev_join_enc, ctx->s_enc));
-                CK(cudaStreamWaitEvent(ctx->s_comp, ctx->ev_join_enc, 0));
-                if (!halo_sweep_begin(ctx->halo, ctx->s_comp, &herr))
+                if (!halo_sweep_begin(ctx->halo, &herr))
                     return fail(ctx, OOCZ_ENCCL, "halo exchange: %s", herr.c_str());
-                CK(cudaEventRecord(ctx->ev_halo, ctx->s_comp));   // the decode stream inserts them
             }
         }
         const bool last_sweep = done + ts >= nsteps;
