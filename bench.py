@@ -342,7 +342,8 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     import torch
     S = nz // world
     store = opt.get("store", 0)
-    cfg = Z.oocz_default_config(nx, ny, nz, tb=T, block_planes=opt["P"], rate=list(rates), store=store,
+    tb = opt.get("tb", T)
+    cfg = Z.oocz_default_config(nx, ny, nz, tb=tb, block_planes=opt["P"], rate=list(rates), store=store,
                                 m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
                                 slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile)
     if callable(nccl_id):
@@ -358,14 +359,14 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     try:
         # a compressed store in HBM leaves little room for the generator's fp64 chunks
         t_set = set_fields_gpu(Z, ctx, nx, ny, nz, rank * S, S, C3SEED, chunk=16 if store == 0 else 4)
-        Z.oocz_step(ctx, warmup * T)
+        Z.oocz_step(ctx, warmup * tb)
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         st0 = Z.oocz_get_stats(ctx)
         l0 = Z.oocz_kernel_launch_count()
         h0 = time.perf_counter()
-        Z.oocz_step(ctx, steps * T)          # returns when every stream is done
+        Z.oocz_step(ctx, steps * tb)         # returns when every stream is done
         host_s = time.perf_counter() - h0
         launches = Z.oocz_kernel_launch_count() - l0
         torch.cuda.synchronize()
@@ -380,8 +381,8 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
         sweeps = st["sweeps"] - st0["sweeps"]
         h2d = (st["h2d_bytes"] - st0["h2d_bytes"]) / max(sweeps, 1)
         d2h = (st["d2h_bytes"] - st0["d2h_bytes"]) / max(sweeps, 1)
-        cells = nx * ny * nz * T * steps
-        res = {"label": label, "grid": [nx, ny, nz], "rates": list(rates), "P": opt["P"], "D": S // opt["P"],
+        cells = nx * ny * nz * tb * steps
+        res = {"label": label, "tb": tb, "grid": [nx, ny, nz], "rates": list(rates), "P": opt["P"], "D": S // opt["P"],
                "schedule": {k: v for k, v in opt.items() if k != "P"},
                "cups": cells / dev_s, "e2e_cups": cells / host_s, "device_s": dev_s, "host_s": host_s,
                "sweeps": steps, "warmup": warmup, "launches": launches,
@@ -427,6 +428,10 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
             clk.active = True
             out["pf"] = run_c3(Z, "c3_zfp_host_pf", nx, ny, nz, (RATE,) * 3, PF, arena, rank, world, nccl_id, local,
                                sw, wu, dist)
+            # the paper's own temporal depth T = 12 on the same grid: a third of
+            # the host bytes per step (P = 96: the slabs of h = 48 planes fit beside the staging)
+            out["t12"] = run_c3(Z, "c3_zfp_host_t12", nx, ny, nz, (RATE,) * 3, dict(P=96, serpentine=1, slots=2, tb=12),
+                                arena, rank, world, nccl_id, local, sw, wu, dist)
             # ZFP vs raw on the largest C3-shaped grid whose raw store fits this host
             planes = [0, raw_nz // 4, raw_nz // 2, 3 * raw_nz // 4 - 4, raw_nz - 4]
             HSr = dict(HS, P=pick_P(raw_nz, 64))
@@ -491,6 +496,15 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
             "sweeps": pf["sweeps"],
             "schedule": "the paper's: ascending sweeps, m streamed and decoded every sweep, 2 staging slots",
             "headline_over_paper_faithful": round(h["cups"] / pf["cups"], 3)}
+    if "t12" in c3:
+        t = c3["t12"]
+        rep["c3_paper_T12"] = {"value": round(t["cups"], 1), "e2e": round(t["e2e_cups"], 1), "tb": 12, "P": t["P"],
+                               "D": t["D"], "h2d_bytes_per_step": int(t["h2d_per_sweep"]),
+                               "d2h_bytes_per_step": int(t["d2h_per_sweep"]),
+                               "h2d_GBps": round(t["h2d_GBps"], 2), "d2h_GBps": round(t["d2h_GBps"], 2),
+                               "schedule": "serpentine, m streamed, 2 slots; one step = one sweep of 12 leapfrog steps",
+                               "what": "the paper's temporal blocking depth (PAPER.md:217, T = 12) on the C3 grid: "
+                                       "a third of the host bytes per cell-update of T = 4"}
     if "half_raw_pf" in c3:
         zr = {"grid": c3["half_raw_pf"]["grid"],
               "why": "the full C3 raw store (3 x 103.1 GB = 309.2 GB) cannot exist on this host "
@@ -780,6 +794,7 @@ def gpu_arm(args):
         "lanes": rep["lanes"],
         "zfp_vs_raw": rep.get("zfp_vs_raw"),
         "c3_paper_faithful": rep.get("c3_paper_faithful"),
+        "c3_paper_T12": rep.get("c3_paper_T12"),
         "c3_hbm_resident": rep.get("c3_hbm_resident"),
         "c3_arena": c3["arena"],
         "headline_run": rep["headline_run"],

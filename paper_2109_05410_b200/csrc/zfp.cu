@@ -89,7 +89,11 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         st[s] = zb::EncState{-1, 0, 0, false};
         bw[s] = zb::BitWriter{out + (size_t)b * rate, 0ull, 0, 0};
         if (b >= nblocks) continue;
+#ifdef OOCZ_ENC_L2IN        // A/B bound for fusion (tools/fusion_bound.py): inputs from a 1 MB, L2-resident range
+        const BlockPos p = block_pos(b & 4095, nbx, nby);
+#else
         const BlockPos p = block_pos(b, nbx, nby);
+#endif
         const float* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
         uint32_t v[64];
 #pragma unroll
@@ -229,6 +233,16 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
         // if-converts into both paths); emax >= -96 is the FMUL path of
         // zb::dequantize, the rest its fp64 path
         const int em = emax[s];
+#ifdef OOCZ_DEC_NOSTORE     // A/B bound for fusion (tools/fusion_bound.py): all the work, no output stores
+        if (em >= -96) {
+            const float sc = __int_as_float((em - 30 + 127) << 23);
+            uint32_t acc = 0;
+#pragma unroll
+            for (int l = 0; l < 64; l++) acc ^= __float_as_uint(__fmul_rn(__int2float_rn(q[l]), sc));
+            if (nx < 0) *reinterpret_cast<uint32_t*>(base) = acc;
+            continue;
+        }
+#endif
         if (em >= -96) {
             const float sc = __int_as_float((em - 30 + 127) << 23);
 #pragma unroll

@@ -14,7 +14,7 @@
 //     plane word / on the next <=63 stream bits), so the coder's cost is
 //     O(planes + newly significant coefficients) instead of O(bits).
 // Functions are __host__ __device__ only so that a stand-alone CPU build of
-// this header (tests/native/zfp_host_check.cu) can exercise the same logic; the
+// this header (tests/native/zb_host.cpp) can exercise the same logic; the
 // library itself only calls them from CUDA kernels.
 #pragma once
 #include <cmath>

@@ -3,7 +3,7 @@ test_random_configurations_bit_exact, 96 configurations per seed)."""
 import os
 import sys
 import time
-R = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+R = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(R, "tests"))
 sys.path.insert(0, R)
 import test_gpu_engine as E  # noqa: E402
