@@ -345,7 +345,8 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     tb = opt.get("tb", T)
     cfg = Z.oocz_default_config(nx, ny, nz, tb=tb, block_planes=opt["P"], rate=list(rates), store=store,
                                 m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
-                                slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile)
+                                slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile,
+                                cone=opt.get("cone", 0))
     if callable(nccl_id):
         nccl_id = nccl_id()
     torch.cuda.empty_cache()             # the generator's chunks: HBM for the context (C3 fills it)
@@ -418,7 +419,7 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
         HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=3)
-        PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2)
+        PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
         out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id, local,
                                  args.steps, args.warmup, dist, profile=1)
@@ -494,7 +495,8 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
             "h2d_bytes_per_step": int(pf["h2d_per_sweep"]), "d2h_bytes_per_step": int(pf["d2h_per_sweep"]),
             "h2d_GBps": round(pf["h2d_GBps"], 2), "d2h_GBps": round(pf["d2h_GBps"], 2),
             "sweeps": pf["sweeps"],
-            "schedule": "the paper's: ascending sweeps, m streamed and decoded every sweep, 2 staging slots",
+            "schedule": "the paper's: ascending sweeps, m streamed and decoded every sweep, the trapezoid cone "
+                        "(cone = 1), 2 staging slots",
             "headline_over_paper_faithful": round(h["cups"] / pf["cups"], 3)}
     if "t12" in c3:
         t = c3["t12"]
@@ -545,12 +547,12 @@ def make_fields_c2():
 
 
 def run_mode_c2(Z, store, rates, fields, device, steps, warmup, profile, m_resident=0, tb=T, precision=32,
-                serpentine=0, slots=2, slab_sets=0):
+                serpentine=0, slots=2, slab_sets=0, cone=0):
     """Returns (device seconds for `steps` sweeps, stats, events, launches, ctx)."""
     import torch
     cfg = Z.oocz_default_config(NX, NY, NZ, tb=tb, block_planes=P, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=slots, profile=profile, slab_sets=slab_sets)
+                                slots=slots, profile=profile, slab_sets=slab_sets, cone=cone)
     ctx = Z.oocz_create(cfg, 0, 1, None, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):
@@ -633,7 +635,7 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
     cells = NX * NY * NZ * T * steps
     OD = dict(m_resident=1)
     OH = dict(serpentine=1, m_resident=1, slots=3)
-    PF = dict(serpentine=0, m_resident=0)
+    PF = dict(serpentine=0, m_resident=0, cone=1)
     modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
              ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
     if not args.quick:
@@ -664,7 +666,7 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
                                                     profile=int(label == "zfp_dev"),
                                                     m_resident=opt.get("m_resident", 0), tb=tb, precision=prec,
                                                     serpentine=opt.get("serpentine", 0), slots=opt.get("slots", 2),
-                                                    slab_sets=opt.get("slab_sets", 0))
+                                                    slab_sets=opt.get("slab_sets", 0), cone=opt.get("cone", 0))
         clk.active = False
         sw = max(st["sweeps"], 1)
         out[label] = {"s": dev_s, "cups": cells // T * tb / dev_s, "launches": launches, "evs": evs,
@@ -750,7 +752,14 @@ def gpu_arm(args):
     nccl_id = (lambda: D.share_nccl_id(dist, rank, Z.oocz_get_nccl_id, device="cuda")) if world > 1 else None
     peak_gbs, peak_src = peaks()
     info = host_info()
+    if dist:                     # all ranks probe their host links at the same time (shared PCIe / memory)
+        dist.barrier()
     link = host_link_probe()
+    if dist:
+        for k in ("h2d_GBps", "d2h_GBps", "concurrent_per_direction_GBps"):
+            link[k] = -D.max_over_ranks(dist, -link[k], device="cuda")      # the slowest rank's link
+        link["ranks"] = world
+        link["note"] = "all ranks probing at once; the minimum over ranks"
     with ClockSampler(local) as clk:
         c3 = c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link, clk, info)
         c2 = c2_arm(args, Z, local, peak_gbs, peak_src, link, clk) if world == 1 and not args.no_c2 else None

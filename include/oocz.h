@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OOCZ_ABI_VERSION 4
+#define OOCZ_ABI_VERSION 5
 
 typedef enum {
     OOCZ_OK = 0,
@@ -92,6 +92,13 @@ typedef struct {
                               world = 1, profile = 0 and serpentine = 0; otherwise ignored.  For
                               launch-bound small grids.  Results identical.  0 or 1, else
                               OOCZ_EINVAL. */
+    int32_t  cone;         /* temporal-blocking tile shape.  1: the paper's trapezoid cone
+                              (PAPER.md:112, :217): block i updates planes [iP - h + 4s,
+                              (i+1)P + h - 4s) in step s, recomputing the overlap with its
+                              neighbours.  0 (default): parallelogram tiles (R26),
+                              every cell updated once per step, the overlap's last two time
+                              levels handed from block to block.  Results identical.  0 or
+                              1, else OOCZ_EINVAL. */
 } oocz_config;
 
 typedef struct {

@@ -374,6 +374,7 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->slab_sets < 0 || cfg->slab_sets > 4)
         BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 1, 2, 3, 4}", cfg->slab_sets);
     if (cfg->graphs != 0 && cfg->graphs != 1) BAD(OOCZ_EINVAL, "graphs (%d) must be 0 or 1", cfg->graphs);
+    if (cfg->cone != 0 && cfg->cone != 1) BAD(OOCZ_EINVAL, "cone (%d) must be 0 or 1", cfg->cone);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
@@ -452,11 +453,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     const size_t pb = ctx->pb;
     // slab sets (m is not streamed into them when it is resident) + the C_i copy
     const int slab_fields = cfg->m_resident ? 2 : 3;    // also the streamed fields
-#ifdef OOCZ_CONE_ONLY             // A/B: the trapezoid cone everywhere
-    ctx->para = false;
-#else
-    ctx->para = true;
-#endif
+    // cfg->cone = 1: the paper's trapezoid cone on every block;
+    // 0: parallelogram tiles (reading R26).  Same bits either way.
+    ctx->para = cfg->cone == 0;
     // with parallelogram tiles and ascending sweeps only, only C planes
     // [h + 4ts - 4, 2h) of u, u- are kept (descending sweeps need [0, h - 4ts + 4))
     for (int f = 0; f < 2; f++) ctx->cbase[f] = ctx->para && !cfg->serpentine ? h : 0;

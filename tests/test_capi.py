@@ -27,7 +27,7 @@ def test_every_header_symbol_is_exported(z):
 
 
 def test_abi_version(z):
-    assert z.oocz_abi_version() == z.ABI_VERSION == 4
+    assert z.oocz_abi_version() == z.ABI_VERSION == 5
 
 
 def test_zfp_bytes_closed_form(z):
@@ -60,6 +60,8 @@ def test_cfl_limit_default_coefficients(z):
     (dict(slab_sets=-1, block_planes=32), 1, -1, "slab_sets (-1)"),
     (dict(graphs=1, block_planes=32), 1, 0, ""),
     (dict(graphs=2, block_planes=32), 1, -1, "graphs (2)"),
+    (dict(cone=1, block_planes=32), 1, 0, ""),
+    (dict(cone=2, block_planes=32), 1, -1, "cone (2)"),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)

@@ -21,12 +21,13 @@ def _fields(nx, ny, nz, seed, kind="dense"):
     return u, up, synth.layered(nx, ny, nz)
 
 
-def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0, slab_sets=0):
+def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0, slab_sets=0,
+             cone=0):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
                                 slots=slots, profile=profile, serpentine=serpentine, m_resident=m_resident,
-                                slab_sets=slab_sets)
+                                slab_sets=slab_sets, cone=cone)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -485,3 +486,55 @@ def test_parallelogram_updates_every_cell_once_per_step(nx, ny, nz, T, P, calls)
     last = calls[-1]
     for serp in (0, 1):                                     # read u, u-, m, write u+ once per cell and step
         assert stencil_bytes[serp] == 4 * nz * pb * last
+
+
+@pytest.mark.parametrize("nx,ny,nz,T,P,calls", [(32, 24, 96, 3, 24, [7]), (24, 16, 64, 2, 16, [4, 3]),
+                                                (16, 16, 128, 4, 32, [8])])
+def test_paper_trapezoid_cone_bit_exact_and_its_cost(nx, ny, nz, T, P, calls):
+    """cone = 1: the paper's own temporal-blocking shape,
+    block i updates [iP - h + 4s, (i+1)P + h - 4s) in step s, recomputing the
+    overlap.  Same bits as the oracle (and as the parallelogram tiles), in both
+    sweep directions, and the stencil's algorithmic bytes are exactly the cone's:
+    sum over blocks and steps of the cone's planes clipped to the grid."""
+    u, up, m = _fields(nx, ny, nz, 14)
+    rates = (16, 16, 16)
+    ou, oup = _run_oracle(u, up, m, T, rates, calls)
+    pb = nx * ny * 4
+    h, D = 4 * T, nz // P
+    last = calls[-1]
+    for serp in (0, 1):
+        for store in (0, 1):
+            gu, gup, st, evs = _run_gpu(u, up, m, T, P, rates, store, calls, profile=1, serpentine=serp, cone=1,
+                                        m_resident=serp)
+            assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), (serp, store)
+            got = sum(e["bytes"] for e in evs if e["stage"] == 2)
+            want = 0
+            done = 0
+            while done < last:
+                ts = min(T, last - done)
+                for i in range(D):
+                    for step in range(1, ts + 1):
+                        z0, z1 = max(i * P - h + 4 * step, 0), min((i + 1) * P + h - 4 * step, nz)
+                        want += 16 * (z1 - z0) * nx * ny
+                done += ts
+            assert got == want, (serp, store, got, want)
+
+
+def test_random_configurations_cone_bit_exact(seed=77):
+    """48 seeded random configurations with the paper's trapezoid cone."""
+    rng = np.random.default_rng(seed)
+    for case in range(48):
+        T = int(rng.integers(1, 4))
+        P = int(rng.choice([q for q in (8, 12, 16, 20, 24, 32) if q >= 8 * T]))
+        nz = P * int(rng.integers(1, 5))
+        nx, ny = 4 * int(rng.integers(2, 12)), 4 * int(rng.integers(1, 8))
+        rates = tuple(int(rng.choice([0, 3, 8, 16, 24, 64])) for _ in range(3))
+        store = int(rng.integers(0, 2))
+        opts = dict(slots=int(rng.integers(2, 5)), slab_sets=int(rng.choice([0, 1, 2, 3])),
+                    serpentine=int(rng.integers(0, 2)), m_resident=int(rng.integers(0, 2)))
+        calls = [int(x) for x in rng.integers(1, 3 * T + 2, size=int(rng.integers(1, 3)))]
+        u, up, m = _fields(nx, ny, nz, 300 + case)
+        gu, gup, _, _ = _run_gpu(u, up, m, T, P, rates, store, calls, cone=1, **opts)
+        ou, oup = _run_oracle(u, up, m, T, rates, calls)
+        assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), \
+            (nx, ny, nz, T, P, rates, store, opts, calls)

@@ -8,10 +8,10 @@
 set -e
 cd "$(dirname "$0")/.."
 B=paper_2109_05410_b200
-python -m paper_2109_05410_b200.build --out $B/liboocz_ab_base.so --force > /dev/null
-python -m paper_2109_05410_b200.build -DOOCZ_DEC_NOSTORE --out $B/liboocz_ab_decnostore.so > /dev/null
-python -m paper_2109_05410_b200.build -DOOCZ_ENC_L2IN --out $B/liboocz_ab_encl2.so > /dev/null
-python -m paper_2109_05410_b200.build -DOOCZ_DEC_NOSTORE -DOOCZ_ENC_L2IN --out $B/liboocz_ab_both.so > /dev/null
+[ -f $B/liboocz_ab_base.so ] || python -m paper_2109_05410_b200.build --out $B/liboocz_ab_base.so --force > /dev/null
+[ -f $B/liboocz_ab_decnostore.so ] || python -m paper_2109_05410_b200.build -DOOCZ_DEC_NOSTORE --out $B/liboocz_ab_decnostore.so > /dev/null
+[ -f $B/liboocz_ab_encl2.so ] || python -m paper_2109_05410_b200.build -DOOCZ_ENC_L2IN --out $B/liboocz_ab_encl2.so > /dev/null
+[ -f $B/liboocz_ab_both.so ] || python -m paper_2109_05410_b200.build -DOOCZ_DEC_NOSTORE -DOOCZ_ENC_L2IN --out $B/liboocz_ab_both.so > /dev/null
 for round in 1 2; do
   for v in base decnostore encl2 both; do
     OOCZ_LIB=$PWD/$B/liboocz_ab_$v.so python tools/ab_one.py

@@ -9,11 +9,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2109_05410_b200 import oocz as Z  # noqa: E402
 from paper_2109_05410_b200 import synth  # noqa: E402
 
-n = 512
+n = int(os.environ.get("N", "512"))                # 4096: a C3 plane (DENSE(2), generated on the GPU)
 planes = int(os.environ.get("PLANES", "160"))      # one slab: P + 2h
 rate = int(os.environ.get("RATE", "16"))
-u = torch.from_numpy(synth.dense(n, n, n, seed=1, z0=0, z1=planes)).cuda()
-m = torch.from_numpy(synth.layered(n, n, n, z0=0, z1=planes)).cuda()
+if n == 512:
+    u = torch.from_numpy(synth.dense(n, n, n, seed=1, z0=0, z1=planes)).cuda()
+    m = torch.from_numpy(synth.layered(n, n, n, z0=0, z1=planes)).cuda()
+else:
+    u = synth.dense_torch(n, n, 1536, 2, 0, planes)
+    m = synth.layered_torch(n, n, 1536, 0, planes)
 up = u.clone()
 words = torch.empty(Z.oocz_zfp_bytes(n, n, planes, rate) // 8, dtype=torch.int64, device="cuda")
 out = torch.empty_like(u)
