@@ -204,7 +204,10 @@ def lanes_summary(evs) -> dict:
     return out
 
 
-TRAFFIC_JSON = {"stencil": "r01_stencil_instep_traffic.json"}
+# DRAM bytes / algorithmic bytes per launch of each hot kernel, from the committed
+# ncu --set full capture of the C3-wide launch shape (tools/ncu_r02.sh)
+TRAFFIC_JSON = "r02_stencil_c3_traffic.json"
+TRAFFIC_KEY = {"stencil": "traffic_over_algorithmic", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}
 ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
 
 
@@ -238,11 +241,11 @@ def roofline(evs, peak_gbs, peak_src):
     kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
     traffic, tsrc = None, None
     try:   # DRAM bytes per launch from a committed ncu capture of the same kind of launch
-        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON[dom])) as fh:
-            tj = json.load(fh)
-        traffic = int(tj["traffic_over_algorithmic"] * nbytes / n)
-        tsrc = (f"profiles/{TRAFFIC_JSON[dom]}: ncu dram read+write / algorithmic = "
-                f"{tj['traffic_over_algorithmic']}, x this run's algorithmic bytes per launch")
+        with open(os.path.join(ROOT, "profiles", TRAFFIC_JSON)) as fh:
+            ratio = float(json.load(fh)[TRAFFIC_KEY[dom]])
+        traffic = int(ratio * nbytes / n)
+        tsrc = (f"profiles/{TRAFFIC_JSON}: ncu dram read+write / algorithmic = {ratio} on a C3-wide "
+                f"launch, x this run's algorithmic bytes per launch")
     except Exception:
         pass
     return {"bound": "hbm", "kernel": kern, "achieved": round(achieved, 1), "peak": peak_gbs,
