@@ -260,15 +260,12 @@ def codec_alu_roofline(table) -> dict | None:
     """The codec kernels are bound by the integer ALU pipe,
     not by HBM: their fraction is the ALU pipe's share of its peak issue rate
     (148 SMs x 4 sub-partitions x one warp-instruction per 2 cycles at 1965 MHz),
-    measured by ncu (sm__inst_executed_pipe_alu) on the committed capture."""
-    for cand in ("r02_ncu_kernels.json", "r01_ncu_kernels.json"):
-        try:
-            with open(os.path.join(ROOT, "profiles", cand)) as fh:
-                kj = json.load(fh)
-            break
-        except Exception:
-            kj = None
-    if kj is None:
+    measured by ncu (sm__inst_executed_pipe_alu) on the committed capture of the
+    C3-wide launch shape (profiles/r02_ncu_kernels.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")) as fh:
+            kj = json.load(fh)["c3_slab"]
+    except Exception:
         return None
     out = {}
     for name, stage in (("zfp_decode_kernel", "decode"), ("zfp_encode_kernel", "encode")):
@@ -276,13 +273,12 @@ def codec_alu_roofline(table) -> dict | None:
         if not ks:
             continue
         k = ks[0]
-        frac = k["sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"] / 100.0
+        frac = k["alu_pipe_pct"] / 100.0
         out[name] = {"bound": "alu", "achieved": round(frac * ALU_PEAK, 1), "peak": round(ALU_PEAK, 1),
                      "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
-                     "issue_active": round(k["smsp__issue_active.avg.pct_of_peak_sustained_active"] / 100, 4),
-                     "isolated_us": k["gpu__time_duration.sum"],
+                     "issue_active": round(k["issue_active_pct"] / 100, 4), "isolated_us": k["us"],
                      "in_step_avg_ms": table[stage]["avg_launch_ms"] if stage in table else None,
-                     "source": f"profiles/{cand} (ncu --set full, one C2 slab, rate 16)"}
+                     "source": "profiles/r02_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16)"}
     return out or None
 
 
