@@ -10,25 +10,31 @@ using namespace oocz::zb;
 extern "C" int zb_encode_block(const float* x, int rate, uint64_t* out) {
     uint32_t v[64];
     std::memcpy(v, x, sizeof v);
-    BitWriter bw{out, 0ull, 0, 0};
+    uint64_t row[66];                      // the kernel's shared-memory row: rate + 1 words
+    std::memset(row, 0xa5, sizeof row);    // (garbage: every kept word must be written)
+    RowWriter bw{row, 0ull, 0, 0};
     const int Emax = block_exponent(v);
-    if (Emax < 0) { bw.put(0, 1); bw.finish(rate); return 0; }
-    bw.put(2u * (uint32_t)(Emax + 1) + 1u, kHeaderBits);
-    int32_t q[64];
-    for (int i = 0; i < 64; i++) q[i] = quantize(v[i], Emax);
-    fwd_xform(q);
-    const int perm[64] = OOCZ_PERM3;
-    uint32_t lo[32], hi[32];
-    for (int i = 0; i < 32; i++) {
-        lo[i] = ((uint32_t)q[perm[i]] + kNBMask) ^ kNBMask;
-        hi[i] = ((uint32_t)q[perm[i + 32]] + kNBMask) ^ kNBMask;
+    if (Emax < 0) {
+        bw.put(0, 1);
+    } else {
+        bw.put(2u * (uint32_t)(Emax + 1) + 1u, kHeaderBits);
+        int32_t q[64];
+        for (int i = 0; i < 64; i++) q[i] = quantize(v[i], Emax);
+        fwd_xform(q);
+        const int perm[64] = OOCZ_PERM3;
+        uint32_t lo[32], hi[32];
+        for (int i = 0; i < 32; i++) {
+            lo[i] = ((uint32_t)q[perm[i]] + kNBMask) ^ kNBMask;
+            hi[i] = ((uint32_t)q[perm[i + 32]] + kNBMask) ^ kNBMask;
+        }
+        transpose32(lo);
+        transpose32(hi);
+        uint64_t planes[32];
+        for (int k = 0; k < 32; k++) planes[k] = ((uint64_t)hi[k] << 32) | lo[k];
+        encode_planes_rows([&](int k) { return planes[k]; }, 31, 64 * rate, bw);
     }
-    transpose32(lo);
-    transpose32(hi);
-    uint64_t planes[32];
-    for (int k = 0; k < 32; k++) planes[k] = ((uint64_t)hi[k] << 32) | lo[k];
-    encode_planes([&](int k) { return planes[k]; }, 64 * rate - kHeaderBits, bw);
-    bw.finish(rate);
+    bw.zero_tail(rate);
+    std::memcpy(out, row, sizeof(uint64_t) * (size_t)rate);
     return 0;
 }
 
@@ -85,19 +91,25 @@ static void ints_from_planes64(const uint64_t planes[64], uint64_t u[64]) {
 extern "C" int zb_encode_block64(const double* x, int rate, uint64_t* out) {
     uint64_t v[64];
     std::memcpy(v, x, sizeof v);
-    BitWriter bw{out, 0ull, 0, 0};
+    uint64_t row[66];
+    std::memset(row, 0xa5, sizeof row);
+    RowWriter bw{row, 0ull, 0, 0};
     const int Emax = block_exponent64(v);
-    if (Emax < 0) { bw.put(0, 1); bw.finish(rate); return 0; }
-    bw.put(2ull * (uint64_t)(Emax + 1) + 1ull, kHeaderBits64);
-    int64_t q[64];
-    for (int i = 0; i < 64; i++) q[i] = quantize64(v[i], Emax);
-    fwd_xform(q);
-    const int perm[64] = OOCZ_PERM3;
-    uint64_t u[64], planes[64];
-    for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + kNBMask64) ^ kNBMask64;
-    planes_from_ints64(u, planes);
-    encode_planes([&](int k) { return planes[k]; }, 64 * rate - kHeaderBits64, bw, 63);
-    bw.finish(rate);
+    if (Emax < 0) {
+        bw.put(0, 1);
+    } else {
+        bw.put(2ull * (uint64_t)(Emax + 1) + 1ull, kHeaderBits64);
+        int64_t q[64];
+        for (int i = 0; i < 64; i++) q[i] = quantize64(v[i], Emax);
+        fwd_xform(q);
+        const int perm[64] = OOCZ_PERM3;
+        uint64_t u[64], planes[64];
+        for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + kNBMask64) ^ kNBMask64;
+        planes_from_ints64(u, planes);
+        encode_planes_rows([&](int k) { return planes[k]; }, 63, 64 * rate, bw);
+    }
+    bw.zero_tail(rate);
+    std::memcpy(out, row, sizeof(uint64_t) * (size_t)rate);
     return 0;
 }
 
