@@ -32,24 +32,29 @@ constexpr int kDecThreads = OOCZ_DEC_THREADS;       // fp32 decoder CTA size
 struct BlockPos { long long bx, by, bz; };
 
 // Coalesced stage-in of a CTA's contiguous stream words into shared memory,
-// block by block with a row stride of rate + 1 words (the spare word the 64-bit
-// windows may touch): word w goes to words[(w / rate) (rate + 1) + w % rate].
+// block by block with a row stride of S words: word w goes to words[(w / rate)
+// S + w % rate].  Then each row's words [rate, S) are zeroed: the padded
+// decoder reads up to 3 words past the stream.
 // The quotient and remainder advance with w instead of being recomputed (an
 // integer division per word was 7.5 % of the decoder's instructions).
 template <int NT>
-__device__ __forceinline__ void stage_words(uint64_t* words, const uint64_t* __restrict__ src, int total, int rate)
+__device__ __forceinline__ void stage_words(uint64_t* words, const uint64_t* __restrict__ src, int total, int rate,
+                                            int S)
 {
     const int t = threadIdx.x;
     const int dq = NT / rate, dr = NT - dq * rate;
     int q = t / rate, r = t - q * rate;
 #pragma unroll 4
     for (int w = t; w < total; w += NT) {
-        words[q * (rate + 1) + r] = __ldg(src + w);
+        words[q * S + r] = __ldg(src + w);
         q += dq;
         r += dr;
         if (r >= rate) { r -= rate; q++; }
     }
+    for (int w = rate; w < S; w++) words[t * S + w] = 0ull;
 }
+// decoder row stride: the stream, 3 zero words, odd (bank spread)
+__host__ __device__ __forceinline__ int dec_row_stride(int rate) { return (rate + 3) | 1; }
 
 __device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
     BlockPos p;
@@ -67,28 +72,56 @@ __device__ __forceinline__ BlockPos block_pos(long long b, int nbx, int nby) {
     return p;
 }
 
-// six CTAs per SM (<= 80 registers, 8 bytes of spill): more warps to hide the
-// latency of the block loads before the coder starts; measured 176 -> 168 us
+// Encoder shared memory: one row of S words per thread that holds both the
+// block's bit planes and its output stream.  Plane k sits at word kPlaneBase +
+// (top - k); the planes are consumed in the order top, top - 1, ... while the
+// stream is written from word 0 up, and the stream never overtakes an unread
+// plane: with c planes started, at most 9 + 64 c (heads) + 64 (zero runs and
+// ones, each position scanned once) + 64 (1 flags) + c (0 flags) = 137 + 65 c
+// bits are out (fp64: 140 + 65 c), so the writer's words w, w + 1 stay below
+// word kPlaneBase + c of the next unread plane for every c <= top (base 4 for
+// 32 planes, 5 for 64).  S is odd, so a warp's rows start in different banks
+// and the coalesced copy-out reads one row's consecutive words conflict-free.
+constexpr int kPlaneBase32 = 4, kPlaneBase64 = 5;
+
+// Coalesced copy of nb rows' first rate words (the CTA's contiguous streams)
+// from shared memory to global.  Word i = (row r, column c), advanced with i
+// instead of divided.
+__device__ __forceinline__ void copy_rows_out(const uint64_t* rows, int S, uint64_t* __restrict__ dst, int nb, int rate)
+{
+    const int t = threadIdx.x;
+    const int total = nb * rate;
+    const int dq = kThreads / rate, dr = kThreads - dq * rate;
+    int r = t / rate, c = t - r * rate;
+#pragma unroll 4
+    for (int i = t; i < total; i += kThreads) {
+        dst[i] = rows[r * S + c];
+        r += dq;
+        c += dr;
+        if (c >= rate) { c -= rate; r++; }
+    }
+}
+
+__host__ __device__ __forceinline__ int enc_row_stride(int rate, int planes, int base) {
+    const int need = rate + 1 > base + planes ? rate + 1 : base + planes;
+    return need | 1;
+}
+
 #ifndef OOCZ_ENC_MINB
-#define OOCZ_ENC_MINB 6
+#define OOCZ_ENC_MINB 5
 #endif
 __global__ void __launch_bounds__(kThreads, OOCZ_ENC_MINB)
 zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, uint64_t* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t smem[];   // [NB][32][kThreads]
+    extern __shared__ __align__(16) uint64_t rows[];   // [kThreads][S]: planes and stream (above)
+    const int S = enc_row_stride(rate, 32, kPlaneBase32);
     const int t = threadIdx.x;
     const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
-    zb::BitWriter bw[NB];
-    zb::EncState st[NB];
-
-#pragma unroll
-    for (int s = 0; s < NB; s++) {
-        const long long b = b0 + s * kThreads + t;
-        uint64_t* planes = smem + s * 32 * kThreads;
-        st[s] = zb::EncState{-1, 0, 0, false};
-        bw[s] = zb::BitWriter{out + (size_t)b * rate, 0ull, 0, 0};
-        if (b >= nblocks) continue;
+    const long long b = b0 + t;
+    zb::RowWriter bw{rows + t * S, 0, 0};
+    bw.row[0] = 0ull;
+    if (b < nblocks) {
 #ifdef OOCZ_ENC_L2IN        // A/B bound for fusion (tools/fusion_bound.py): inputs from a 1 MB, L2-resident range
         const BlockPos p = block_pos(b & 4095, nbx, nby);
 #else
@@ -100,11 +133,7 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         for (int k = 0; k < 4; k++)
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-#ifdef OOCZ_DEBUG_LDCG
-                const float4 f = __ldcg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
-#else
                 const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
-#endif
                 v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
                 v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
                 v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
@@ -112,89 +141,73 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
             }
         const int Emax = zb::block_exponent(v);
         if (Emax < 0) {
-            bw[s].put(0, 1);                           // all-zero block: one 0 bit
-            continue;
-        }
-        const uint32_t e = (uint32_t)Emax + 1u;        // emax + 127, emax = Emax - 126
-        bw[s].put(2u * e + 1u, zb::kHeaderBits);
-        // q = trunc(x 2^(30 - emax)).  When 2^(30 - emax) is a normal fp32 (emax >= -97)
-        // and the block is finite, x * 2^(30 - emax) is exact wherever |q| >= 1 (an
-        // underflowing product is < 1 in magnitude and truncates to 0 either way):
-        // one FMUL + one F2I.TRUNC per value, off the integer ALU pipe that binds
-        // this kernel.  Otherwise the bit-field path.
-        int32_t q[64];
-        if (Emax >= 29 && Emax < 255) {
-            const float sc = __int_as_float((283 - Emax) << 23);   // 2^(30 - emax), emax = Emax - 126
-#pragma unroll
-            for (int i = 0; i < 64; i++) q[i] = __float2int_rz(__fmul_rn(__uint_as_float(v[i]), sc));
+            bw.put(0, 1);                              // all-zero block: one 0 bit
         } else {
+            const uint32_t e = (uint32_t)Emax + 1u;    // emax + 127, emax = Emax - 126
+            bw.put(2u * e + 1u, zb::kHeaderBits);
+            // q = trunc(x 2^(30 - emax)).  When 2^(30 - emax) is a normal fp32 (emax >= -97)
+            // and the block is finite, x * 2^(30 - emax) is exact wherever |q| >= 1 (an
+            // underflowing product is < 1 in magnitude and truncates to 0 either way):
+            // one FMUL + one F2I.TRUNC per value, off the integer ALU pipe that binds
+            // this kernel.  Otherwise the bit-field path.
+            int32_t q[64];
+            if (Emax >= 29 && Emax < 255) {
+                const float sc = __int_as_float((283 - Emax) << 23);   // 2^(30 - emax), emax = Emax - 126
 #pragma unroll
-            for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+                for (int i = 0; i < 64; i++) q[i] = __float2int_rz(__fmul_rn(__uint_as_float(v[i]), sc));
+            } else {
+#pragma unroll
+                for (int i = 0; i < 64; i++) q[i] = zb::quantize(v[i], Emax);
+            }
+            zb::fwd_xform(q);
+            constexpr int perm[64] = OOCZ_PERM3;
+            uint32_t lo[32], hi[32];
+#pragma unroll
+            for (int i = 0; i < 32; i++) {
+                lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
+                hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
+            }
+            zb::transpose32(lo);
+            zb::transpose32(hi);
+#pragma unroll
+            uint64_t* pl = rows + t * S + kPlaneBase32 + 31;      // plane k at pl[-k]
+#pragma unroll
+            for (int k = 0; k < 32; k++) pl[-k] = ((uint64_t)hi[k] << 32) | lo[k];
+            zb::encode_planes_rows([&](int k) { return pl[-k]; }, 31, 64 * rate, bw);
         }
-        zb::fwd_xform(q);
-        constexpr int perm[64] = OOCZ_PERM3;
-        uint32_t lo[32], hi[32];
-#pragma unroll
-        for (int i = 0; i < 32; i++) {
-            lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
-            hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
-        }
-        zb::transpose32(lo);
-        zb::transpose32(hi);
-#pragma unroll
-        for (int k = 0; k < 32; k++) planes[k * kThreads + t] = ((uint64_t)hi[k] << 32) | lo[k];
-        st[s] = zb::EncState{31, 0, 64 * rate - zb::kHeaderBits, false};
+        bw.zero_tail(rate);
     }
-    // the event stream: no budget cut while >= 65 bits are left, then the
-    // (at most a few) events that may be cut
-    static_assert(NB == 1, "one event stream per thread");
-    {
-        const uint64_t* planes = smem;
-        auto plane_at = [&](int k) { return planes[k * kThreads + t]; };
-        while (st[0].k >= 0 && st[0].bits >= 65) zb::encode_event_merged(st[0], plane_at, bw[0]);
-        while (st[0].active()) zb::encode_event(st[0], plane_at, bw[0]);
-    }
-#pragma unroll
-    for (int s = 0; s < NB; s++)
-        if (b0 + s * kThreads + t < nblocks) bw[s].finish(rate);
+    __syncthreads();
+    copy_rows_out(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kThreads ? (int)(nblocks - b0) : kThreads, rate);
 }
 
 __global__ void __launch_bounds__(kDecThreads)
 zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, float* __restrict__ out)
 {
-    __shared__ uint64_t planes_all[NB * 32 * kDecThreads];   // [NB][32][kDecThreads]
-    extern __shared__ __align__(16) uint64_t words[];      // [NB*kDecThreads][rate + 1] + 1 spare
+    __shared__ uint64_t planes_all[NB * 32 * kDecThreads];   // [32][kDecThreads]
+    extern __shared__ __align__(16) uint64_t words[];      // [kDecThreads][S]
     const int t = threadIdx.x;
-    const int stride = rate + 1;
+    const int S = dec_row_stride(rate);
     const long long b0 = (long long)blockIdx.x * kDecThreads;
     const long long nb = nblocks - b0 < kDecThreads ? nblocks - b0 : kDecThreads;
-    stage_words<kDecThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
+    stage_words<kDecThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate, S);
     __syncthreads();
 
-    zb::BitReader br[NB];
-    zb::DecState st[NB];
     int emax[NB];
     bool zero[NB];
-#pragma unroll
-    for (int s = 0; s < NB; s++) {
-        const int bb = s * kDecThreads + t;
-        br[s] = zb::BitReader{words + (size_t)bb * stride, 0};
-        st[s] = zb::DecState{-1, 0, 0, false, 0u, 0u};
-        emax[s] = 0;
-        zero[s] = true;
-        if (bb >= nb) continue;
-        if (!br[s].read(1)) continue;                  // zero block
-        zero[s] = false;
-        emax[s] = (int)br[s].read(zb::kEBits) - 127;
-        st[s] = zb::DecState{31, 0, 64 * rate - zb::kHeaderBits, false, 0u, 0u};
-    }
+    static_assert(NB == 1, "one event stream per thread");
     {
+        const uint32_t* row = reinterpret_cast<const uint32_t*>(words + (size_t)t * S);
+        emax[0] = 0;
+        zero[0] = true;
         uint64_t* planes = planes_all + t;
-        auto plane_set = [&](int k, uint64_t x) { planes[k * kDecThreads] = x; };
-        while (st[0].k >= 0 && st[0].bits >= 131) zb::decode_event_merged(st[0], br[0], plane_set);
-        while (st[0].k >= 0 && st[0].bits >= 66) zb::decode_event_fast(st[0], br[0], plane_set);
-        while (st[0].active()) zb::decode_event(st[0], br[0], plane_set);
+        if (t < nb && (row[0] & 1u)) {
+            zero[0] = false;
+            emax[0] = (int)((row[0] >> 1) & 0xffu) - 127;
+            zb::decode_planes_padded([&](int k, uint64_t x) { planes[k * kDecThreads] = x; }, 31, 64 * rate,
+                                     zb::kHeaderBits, row);
+        }
     }
 #pragma unroll
     for (int s = 0; s < NB; s++) {
@@ -211,7 +224,6 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
             continue;
         }
         uint64_t* planes = planes_all + s * 32 * kDecThreads;
-        for (int k = st[s].k; k >= 0; --k) planes[k * kDecThreads + t] = 0ull;   // planes past the budget
         uint32_t lo[32], hi[32];
 #pragma unroll
         for (int k = 0; k < 32; k++) {
@@ -273,7 +285,8 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
 // 64 bit planes of 64 coefficients each, formed by four 32x32 transposes
 // (coefficients 0-31 / 32-63 x integer bits 0-31 / 32-63).  Both kernels keep
 // the planes in dynamic shared memory, [64][kThreads].
-__device__ __forceinline__ void planes_from_ints64(const uint64_t u[64], uint64_t* planes, int t) {
+// plane k (0..63) of the 64 negabinary integers to pl[-k]
+__device__ __forceinline__ void planes_from_ints64(const uint64_t u[64], uint64_t* pl) {
     uint32_t a[32], b[32];
 #pragma unroll
     for (int half = 0; half < 2; half++) {     // integer bits 0-31, then 32-63
@@ -285,53 +298,59 @@ __device__ __forceinline__ void planes_from_ints64(const uint64_t u[64], uint64_
         zb::transpose32(a);
         zb::transpose32(b);
 #pragma unroll
-        for (int k = 0; k < 32; k++) planes[(32 * half + k) * kThreads + t] = ((uint64_t)b[k] << 32) | a[k];
+        for (int k = 0; k < 32; k++) pl[-(32 * half + k)] = ((uint64_t)b[k] << 32) | a[k];
     }
 }
 
-// three CTAs per SM: 64 KiB of planes each, and <= 168 registers (the default
-// allocation of 188 allowed two; measured 378 -> 344 us at rate 32 on a C2 slab)
+// three CTAs per SM: a 69-word row per thread (planes and stream, as the fp32
+// encoder), <= 168 registers
 __global__ void __launch_bounds__(kThreads, 3)
 zfp_encode64_kernel(const double* __restrict__ in, int nx, int ny, int nbx, int nby,
                     long long nblocks, int rate, uint64_t* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t smem[];   // [64][kThreads]
+    extern __shared__ __align__(16) uint64_t rows[];   // [kThreads][S]
+    const int S = enc_row_stride(rate, 64, kPlaneBase64);
     const int t = threadIdx.x;
-    const long long b = (long long)blockIdx.x * kThreads + t;
-    if (b >= nblocks) return;
-    zb::BitWriter bw{out + (size_t)b * rate, 0ull, 0, 0};
-    const BlockPos p = block_pos(b, nbx, nby);
-    const double* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
-    uint64_t v[64];
+    const long long b0 = (long long)blockIdx.x * kThreads;
+    const long long b = b0 + t;
+    zb::RowWriter bw{rows + t * S, 0, 0};
+    bw.row[0] = 0ull;
+    if (b < nblocks) {
+        const BlockPos p = block_pos(b, nbx, nby);
+        const double* base = in + ((size_t)(4 * p.bz) * ny + (size_t)(4 * p.by)) * nx + 4 * p.bx;
+        uint64_t v[64];
 #pragma unroll
-    for (int k = 0; k < 4; k++)
+        for (int k = 0; k < 4; k++)
 #pragma unroll
-        for (int j = 0; j < 4; j++) {
-            const double2* row = reinterpret_cast<const double2*>(base + ((size_t)k * ny + j) * nx);
-            const double2 f0 = __ldg(row), f1 = __ldg(row + 1);
-            v[16 * k + 4 * j + 0] = (uint64_t)__double_as_longlong(f0.x);
-            v[16 * k + 4 * j + 1] = (uint64_t)__double_as_longlong(f0.y);
-            v[16 * k + 4 * j + 2] = (uint64_t)__double_as_longlong(f1.x);
-            v[16 * k + 4 * j + 3] = (uint64_t)__double_as_longlong(f1.y);
+            for (int j = 0; j < 4; j++) {
+                const double2* row = reinterpret_cast<const double2*>(base + ((size_t)k * ny + j) * nx);
+                const double2 f0 = __ldg(row), f1 = __ldg(row + 1);
+                v[16 * k + 4 * j + 0] = (uint64_t)__double_as_longlong(f0.x);
+                v[16 * k + 4 * j + 1] = (uint64_t)__double_as_longlong(f0.y);
+                v[16 * k + 4 * j + 2] = (uint64_t)__double_as_longlong(f1.x);
+                v[16 * k + 4 * j + 3] = (uint64_t)__double_as_longlong(f1.y);
+            }
+        const int Emax = zb::block_exponent64(v);
+        if (Emax < 0) {
+            bw.put(0, 1);                                  // all-zero block: one 0 bit
+        } else {
+            bw.put(2ull * (uint64_t)(Emax + 1) + 1ull, zb::kHeaderBits64);   // e = emax + 1023
+            int64_t q[64];
+#pragma unroll
+            for (int i = 0; i < 64; i++) q[i] = zb::quantize64(v[i], Emax);
+            zb::fwd_xform(q);
+            constexpr int perm[64] = OOCZ_PERM3;
+            uint64_t u[64];
+#pragma unroll
+            for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + zb::kNBMask64) ^ zb::kNBMask64;
+            uint64_t* pl = rows + t * S + kPlaneBase64 + 63;   // plane k at pl[-k]
+            planes_from_ints64(u, pl);
+            zb::encode_planes_rows([&](int k) { return pl[-k]; }, 63, 64 * rate, bw);
         }
-    const int Emax = zb::block_exponent64(v);
-    if (Emax < 0) {                                    // all-zero block: one 0 bit
-        bw.put(0, 1);
-        bw.finish(rate);
-        return;
+        bw.zero_tail(rate);
     }
-    bw.put(2ull * (uint64_t)(Emax + 1) + 1ull, zb::kHeaderBits64);   // e = emax + 1023
-    int64_t q[64];
-#pragma unroll
-    for (int i = 0; i < 64; i++) q[i] = zb::quantize64(v[i], Emax);
-    zb::fwd_xform(q);
-    constexpr int perm[64] = OOCZ_PERM3;
-    uint64_t u[64];
-#pragma unroll
-    for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + zb::kNBMask64) ^ zb::kNBMask64;
-    planes_from_ints64(u, smem, t);
-    zb::encode_planes([&](int k) { return smem[k * kThreads + t]; }, 64 * rate - zb::kHeaderBits64, bw, 63);
-    bw.finish(rate);
+    __syncthreads();
+    copy_rows_out(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kThreads ? (int)(nblocks - b0) : kThreads, rate);
 }
 
 // Two phases of 32 planes so that only 32 planes (32 KiB) are in shared memory
@@ -345,13 +364,12 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
 {
     extern __shared__ __align__(16) uint64_t smem[];   // planes [32][kThreads], then words
     uint64_t* planes = smem;
-    uint64_t* words = smem + 32 * kThreads;            // [kThreads][rate + 1] + 1 spare
+    uint64_t* words = smem + 32 * kThreads;            // [kThreads][S]
     const int t = threadIdx.x;
-    const int stride = rate + 1;
+    const int stride = dec_row_stride(rate);
     const long long b0 = (long long)blockIdx.x * kThreads;
     const long long nb = nblocks - b0 < kThreads ? nblocks - b0 : kThreads;
-    stage_words<kThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate);
-    if (t == 0) words[nb * stride] = 0ull;
+    stage_words<kThreads>(words, in + (size_t)b0 * rate, (int)nb * rate, rate, stride);
     __syncthreads();
     if (t >= nb) return;
     const BlockPos p = block_pos(b0 + t, nbx, nby);
@@ -370,16 +388,14 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
     }
     const int emax = (int)br.read(zb::kEBits64) - 1023;
     uint64_t* pl = planes + t;
-    zb::DecState st{63, 0, 64 * rate - zb::kHeaderBits64, false, 0u, 0u};
+    zb::PadDecState st{63, 0, zb::kHeaderBits64, 0u, 0u, 0u};
+    const uint32_t* p32 = reinterpret_cast<const uint32_t*>(words + (size_t)t * stride);
     uint32_t hi[64];                                   // bits 32..63 of the 64 coefficients
 #pragma unroll
     for (int half = 1; half >= 0; half--) {
         const int kmin = 32 * half;
-        auto set = [&](int k, uint64_t x) { pl[(k - kmin) * kThreads] = x; };
-        while (st.k >= kmin && st.bits >= 131) zb::decode_event_merged(st, br, set);
-        while (st.k >= kmin && st.bits >= 66) zb::decode_event_fast(st, br, set);
-        while (st.k >= kmin && st.active()) zb::decode_event(st, br, set);
-        for (; st.k >= kmin; --st.k) set(st.k, 0ull);      // planes past the budget
+        zb::decode_planes_padded(st, kmin, [&](int k, uint64_t x) { pl[(k - kmin) * kThreads] = x; }, 64 * rate,
+                                 p32);
         uint32_t a[32], b[32];
 #pragma unroll
         for (int k = 0; k < 32; k++) {
@@ -430,13 +446,11 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
     }
 }
 
-size_t encode64_smem_bytes() { return sizeof(uint64_t) * (size_t)(64 * kThreads); }
-size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * (rate + 1) + 1); }
+size_t encode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kThreads * enc_row_stride(rate, 64, kPlaneBase64); }
+size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * dec_row_stride(rate)); }
 
-size_t encode_smem_bytes() { return sizeof(uint64_t) * (size_t)(NB * 32 * kThreads); }
-// the 64-bit stream window reads up to one word past a block's last word: the
-// row padding, and one spare word after the last row
-size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(kDecThreads * (rate + 1) + 1); }
+size_t encode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kThreads * enc_row_stride(rate, 32, kPlaneBase32); }
+size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kDecThreads * dec_row_stride(rate); }
 
 bool codec_args_ok(int nx, int ny, int nz, int rate) {
     return nx >= 0 && ny >= 0 && nz >= 0 && nx % 4 == 0 && ny % 4 == 0 && nz % 4 == 0 &&
@@ -453,11 +467,11 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
     if (nblocks == 0) return cudaSuccess;
     static std::atomic<uint64_t> attr_done{0};
     {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes(), attr_done);
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
     }
     const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
-    zfp_encode_kernel<<<(unsigned)grid, kThreads, encode_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
+    zfp_encode_kernel<<<(unsigned)grid, kThreads, encode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
                                                                            nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
@@ -489,11 +503,11 @@ cudaError_t launch_zfp_encode64(const double* in, int nx, int ny, int nz, int ra
     if (nblocks == 0) return cudaSuccess;
     static std::atomic<uint64_t> attr_done{0};
     {
-        cudaError_t e = kernel_smem_setup((const void*)zfp_encode64_kernel, (int)encode64_smem_bytes(), attr_done);
+        cudaError_t e = kernel_smem_setup((const void*)zfp_encode64_kernel, (int)encode64_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
     }
     const long long grid = (nblocks + kThreads - 1) / kThreads;
-    zfp_encode64_kernel<<<(unsigned)grid, kThreads, encode64_smem_bytes(), s>>>(in, nx, ny, nx / 4, ny / 4,
+    zfp_encode64_kernel<<<(unsigned)grid, kThreads, encode64_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
                                                                                nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();

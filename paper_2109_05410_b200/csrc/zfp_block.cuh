@@ -126,14 +126,25 @@ ZB_UNROLL
             a[k + 8] = __byte_perm(x, y, 0x7351);  // (x.b1, y.b1, x.b3, y.b3)
         }
     }
+    // the 4-, 2- and 1-bit levels: the logical right shift as a high multiply
+    // (IMAD.HI on the FMA pipe; the ALU pipe binds the codec kernels) and the
+    // left shift as IMAD.SHL, leaving the three XOR/AND LOP3s on the ALU
     uint32_t m = 0x0f0f0f0fu;
 ZB_UNROLL
     for (int j = 4; j != 0; j >>= 1) {
+ZB_UNROLL
+        for (int k = 0; k < 32; k++) {
+            if ((k & j) == 0) {
+                const uint32_t t = (__umulhi(a[k], 1u << (32 - j)) ^ a[k + j]) & m;
+                a[k + j] ^= t;
+                a[k] ^= t * (1u << j);
+            }
+        }
+        m ^= m << (j >> 1);
+    }
 #else
     uint32_t m = 0x0000ffffu;
     for (int j = 16; j != 0; j >>= 1) {
-#endif
-ZB_UNROLL
         for (int k = 0; k < 32; k++) {
             if ((k & j) == 0) {
                 uint32_t t = ((a[k] >> j) ^ a[k + j]) & m;
@@ -143,6 +154,7 @@ ZB_UNROLL
         }
         m ^= m << (j >> 1);
     }
+#endif
 }
 
 // Common exponent from fp32 bit patterns: returns the biased exponent E of the
@@ -420,6 +432,128 @@ ZB_HD void encode_event_merged(EncState& st, PlaneAt plane_at, BitWriter& bw) {
     st.inplane = !done;
 }
 
+// ---------------------------------------------------------------- lean encoder
+// 64-bit shifts with PTX's clamping (an amount >= 64 gives 0): one SHF pair,
+// no select for the edge cases.
+ZB_HD uint64_t shl64c(uint64_t v, int s) {
+#if defined(__CUDA_ARCH__)
+    uint64_t r;
+    asm("shl.b64 %0, %1, %2;" : "=l"(r) : "l"(v), "r"(s));
+    return r;
+#else
+    return s >= 64 ? 0ull : v << s;
+#endif
+}
+ZB_HD uint64_t shr64c(uint64_t v, int s) {
+#if defined(__CUDA_ARCH__)
+    uint64_t r;
+    asm("shr.b64 %0, %1, %2;" : "=l"(r) : "l"(v), "r"(s));
+    return r;
+#else
+    return s >= 64 ? 0ull : v >> s;
+#endif
+}
+// low min(m, 32) bits set for m >= 0: one BMSK
+ZB_HD uint32_t bmask32p(int m) {
+#if defined(__CUDA_ARCH__)
+    uint32_t r;
+    asm("bmsk.clamp.b32 %0, 0, %1;" : "=r"(r) : "r"(m));
+    return r;
+#else
+    return m >= 32 ? ~0u : ((1u << m) - 1u);
+#endif
+}
+// x >> s with PTX's clamping (s >= 32 gives 0), s >= 0
+ZB_HD uint32_t shr32c(uint32_t x, int s) {
+#if defined(__CUDA_ARCH__)
+    uint32_t r;
+    asm("shr.b32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(s));
+    return r;
+#else
+    return s >= 32 ? 0u : x >> s;
+#endif
+}
+// low clamp(m, 0, 64) bits set: two BMSK
+ZB_HD uint64_t bmask64(int m) { return ((uint64_t)bmask32(m - 32) << 32) | bmask32(m); }
+
+// A thread's output stream as a row of words in shared memory.  Each emission
+// writes the word being filled and the next one unconditionally (no branch, no
+// global address arithmetic); the partial word is not kept in registers but
+// read back from the row (an LDS instead of the selects that would track it),
+// so the row must hold 0 at word 0 before the first put, and a 65-bit emission
+// that ends exactly on a word boundary zeroes the word after (the only case
+// where the next word was not just written).  The row needs two words of room
+// past the last one kept; the caller copies the row out (coalesced).
+struct RowWriter {
+    uint64_t* row;
+    int nb, w;        // bits [0, nb) of word w are written
+    ZB_HD int pos() const { return 64 * w + nb; }
+    // append the low len bits of v (len <= 65: bit 64 of a 65-bit emission is
+    // the closing 0 flag; v has no bits at or above len)
+    ZB_HD void put(uint64_t v, int len) {
+        row[w] |= shl64c(v, nb);
+        row[w + 1] = shr64c(v, 64 - nb);
+        const int t = nb + len;
+        if (t >= 128) row[w + 2] = 0ull;
+        w += t >> 6;
+        nb = t & 63;
+    }
+    // zero the words of [pos, 64 * words) not yet written
+    ZB_HD void zero_tail(int words) {
+        for (int i = w + (nb ? 1 : 0); i < words; i++) row[i] = 0ull;
+    }
+};
+
+// The encoder as one flat loop of straight-line events with no budget test
+// inside: the fixed-rate stream is a prefix of the unbounded one (zfp stops
+// writing when the budget is spent and writes nothing else), so the loop
+// emits until 64 * rate bits are out and the caller keeps the first rate
+// words.  State: x = plane k at a plane start, else only its ones not yet
+// coded (all at or above n); ip = inside plane k's group tests.  Each event
+// is a head (plane start: the n verbatim bits) plus a unit:
+//   ones left r = x & ~mask(n):
+//     none      : the 0 group flag (when n < 64); plane done;
+//     next at tz: flag 1, the tz - n zeros, the one (implied at 63: not sent),
+//                 and the closing 0 flag when it was the last one (tz < 63).
+// A plane start with new ones is merged with its first unit, so a plane with
+// j >= 1 new ones takes j events (encode_event_merged's schedule, ~half the
+// instructions: no both-alternatives select, no budget clamps, no global
+// stores).
+template <class PlaneAt>
+ZB_HD void encode_planes_rows(PlaneAt plane_at, int top_plane, int limit, RowWriter& bw) {
+    int k = top_plane, n = 0;
+    uint32_t ipm = 0u;                                 // ~0 inside a plane's group tests
+    uint64_t x = plane_at(k);
+    const int wlimit = limit >> 6;                     // (limit is a whole number of words)
+    while (k >= 0 && bw.w < wlimit) {
+        const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+        const uint32_t ml = bmask32p(n), mh = shr32c(~0u, 64 - n);
+        // head (plane start only): x & mask(n); ones left: x & ~mask(n) (inside a
+        // plane x holds no bit below n, so the same masking gives x)
+        const uint64_t head = ((uint64_t)(xh & mh & ~ipm) << 32) | (xl & ml & ~ipm);
+        const uint32_t rl = xl & ~ml, rh = xh & ~mh;
+        const bool lnz = rl != 0u;
+        const bool has = lnz || rh != 0u;
+        const int tz = lnz ? ctz32nz(rl | (lnz ? 0u : 1u)) : 32 + ctz32nz(rh | 0x80000000u);
+        const uint64_t r = ((uint64_t)rh << 32) | rl;
+        const uint64_t r2 = r & (r - 1ull);
+        const bool last = r2 == 0ull;
+        const bool implied = tz == 63;
+        const int nsub = n & (int)ipm;                 // unit start: 0 at a plane start, n inside
+        const int onep = tz + 1 - nsub;                // position of the one in the emission
+        const int fpos = has ? (n & ~(int)ipm) : 64;   // the 1 flag after the head (none: no bit)
+        const int opos = (has && !implied) ? onep : 64;
+        const uint64_t v = head | shl64c(1ull, fpos) | shl64c(1ull, opos);
+        const int len = has ? onep + (implied ? 0 : 1 + (last ? 1 : 0)) : (n < 64 ? n + 1 : 64);
+        bw.put(v, len);
+        const bool done = !has || last;
+        n = has ? tz + 1 : n;
+        k -= done ? 1 : 0;
+        ipm = done ? 0u : ~0u;
+        x = done ? plane_at(k & top_plane) : r2;      // (k = -1 reads a valid plane, unused)
+    }
+}
+
 template <class PlaneAt>
 ZB_HD void encode_planes(PlaneAt plane_at, int bits, BitWriter& bw, int top_plane = 31) {
     EncState st{top_plane, 0, bits, false};
@@ -571,6 +705,75 @@ ZB_HD void decode_event_merged(DecState& st, BitReader& br, PlaneSet plane_set) 
     plane_set(st.k, ((uint64_t)st.xhi << 32) | st.xlo);   // unconditional: the last store is final
     st.k -= cont ? 0 : 1;
     st.inplane = cont;
+}
+
+// The decoder as one flat loop of merged events with a single budget term.
+// The stream must be followed by >= 3 zero words past the limit (64 * rate
+// bits incl. the header).  Reading past the budget then reproduces zfp's
+// truncation everywhere but in one place: verbatim bits and group flags past
+// the budget read as 0 (zfp leaves those bits 0 and stops), and the one place
+// that differs -- a zero-run scan cut by the budget, after which zfp deposits
+// the one where the budget ended -- is the scan length clamp L = min(63 - n,
+// limit - u0).  The loop ends once the position reaches the limit; the planes
+// not reached stay 0 (the caller's).  Event (state: plane k being assembled in
+// xl:xh, n, ipm = ~0 inside the plane's group tests):
+//   plane start : the n verbatim bits, then the group flag (n < 64);
+//   unit        : (in-plane, or after a 1 flag) the zero run r <= L from u0,
+//                 the deposit at n + r, then the next flag unless n + r == 63.
+struct PadDecState {
+    int k, n, pos;
+    uint32_t ipm, xl, xh;
+};
+
+// planes k >= kmin (resumable: the fp64 decoder runs it in two halves)
+template <class PlaneSet>
+ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, int limit, const uint32_t* p32) {
+    int k = st.k, n = st.n, pos = st.pos;
+    uint32_t ipm = st.ipm, xl = st.xl, xh = st.xh;
+    // (a 1 flag that is the budget's last bit still gets its deposit: zfp's
+    // scan reads nothing and puts the one at n, the event below with L = 0)
+    while (k >= kmin && (pos < limit || ipm != 0u)) {
+        const uint32_t* q = p32 + (pos >> 5);
+        const int o = pos & 31;
+        const uint32_t wl = fshr32(q[0], q[1], o), wh = fshr32(q[1], q[2], o);
+        const uint32_t ml = bmask32p(n), mh = shr32c(~0u, 64 - n);
+        const uint32_t aLo = wl & ml, aHi = wh & mh;                 // head
+        const uint32_t fA = (uint32_t)(n < 64);
+        const uint32_t flagA = fA & bit64(wl, wh, n & 63);
+        const bool unit = ipm != 0u || flagA != 0u;
+        const int u0 = pos + ((n + (int)fA) & ~(int)ipm);          // after the head and its flag
+        const uint32_t* qu = p32 + (u0 >> 5);
+        const int ou = u0 & 31;
+        const uint32_t ul = fshr32(qu[0], qu[1], ou), uh = fshr32(qu[1], qu[2], ou);
+        const int rem = limit - u0;
+        const int L = 63 - n < rem ? 63 - n : rem;                   // (>= 0 whenever unit)
+        const uint32_t tLo = ul | ~bmask32p(L), tHi = uh | ~shr32c(~0u, 64 - L);
+        const int r = tLo ? ctz32nz(tLo) : 32 + ctz32nz(tHi);        // (bit 63 of ~mask(L) is set)
+        const int c0 = r + (r < L ? 1 : 0);
+        const int nB = n + r;
+        const uint32_t baseLo = ipm ? xl : aLo, baseHi = ipm ? xh : aHi;
+        const uint32_t one = 1u << (nB & 31);
+        const uint32_t bLo = baseLo | (nB < 32 ? one : 0u);
+        const uint32_t bHi = baseHi | (nB >= 32 ? one : 0u);
+        const uint32_t fB = (uint32_t)(nB < 63);
+        const uint32_t contB = fB & bit64(ul, uh, c0 & 63);
+        xl = unit ? bLo : aLo;
+        xh = unit ? bHi : aHi;
+        const bool cont = unit && contB != 0u;
+        n = unit ? nB + 1 : n;
+        pos = u0 + (unit ? c0 + (int)fB : 0);
+        plane_set(k, ((uint64_t)xh << 32) | xl);   // unconditional: the last store of plane k is final
+        k -= cont ? 0 : 1;
+        ipm = cont ? ~0u : 0u;
+    }
+    for (; k >= kmin; --k) plane_set(k, 0ull);
+    st = PadDecState{k, n, pos, ipm, xl, xh};
+}
+
+template <class PlaneSet>
+ZB_HD void decode_planes_padded(PlaneSet plane_set, int top_plane, int limit, int pos, const uint32_t* p32) {
+    PadDecState st{top_plane, 0, pos, 0u, 0u, 0u};
+    decode_planes_padded(st, 0, plane_set, limit, p32);
 }
 
 template <class PlaneSet>

@@ -30,6 +30,9 @@ def zb():
     L.zb_decode_block.argtypes = [u64p, C.c_int, f32p]
     f64p = np.ctypeslib.ndpointer(np.float64, flags="C_CONTIGUOUS")
     L.zb_encode_block64.argtypes = [f64p, C.c_int, u64p]
+    u32p = np.ctypeslib.ndpointer(np.uint32, flags="C_CONTIGUOUS")
+    L.zb_encode_ints_rows.argtypes = [u32p, C.c_int, C.c_int, u64p]
+    L.zb_encode_ints64_rows.argtypes = [u64p, C.c_int, C.c_int, u64p]
     L.zb_decode_block64.argtypes = [u64p, C.c_int, f64p]
     return L
 
@@ -121,3 +124,61 @@ def test_decode64_matches_oracle(zb):
         got = np.zeros(64)
         zb.zb_decode_block64(words, rate, got)
         assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), (n, rate)
+
+
+def _adversarial_ints(n, seed, bits):
+    """Negabinary coefficient sets that make the plane coder emit as much as
+    possible as early as possible (dense top planes: up to 129 bits for the
+    first plane) -- the worst case of the encoder's overlapped shared-memory
+    row, where the stream is written over planes already consumed."""
+    rng = np.random.default_rng(seed)
+    top = (1 << bits) - 1
+    out = []
+    for b in range(n):
+        kind = b % 5
+        if kind == 0:
+            u = np.full(64, top, dtype=np.uint64)                       # every plane all ones
+        elif kind == 1:
+            u = rng.integers(0, 1 << 62, 64, dtype=np.uint64) * 4 + rng.integers(0, 4, 64, dtype=np.uint64)
+        elif kind == 2:                                                 # top bit set everywhere, rest random
+            u = (rng.integers(0, 1 << 62, 64, dtype=np.uint64) | np.uint64(1 << (bits - 1)))
+        elif kind == 3:                                                 # alternating dense / empty planes
+            u = np.full(64, int("10" * 32, 2) & top, dtype=np.uint64)
+        else:                                                           # ones arriving one per plane
+            u = np.zeros(64, np.uint64)
+            for i in range(64):
+                u[i] = np.uint64(1 << max(bits - 1 - i % bits, 0))
+        out.append(u & np.uint64(top))
+    return out
+
+
+def _bits_after(words, header, budget):
+    """stream bits [header, header + budget) of a row of words, as an int"""
+    v = 0
+    for i, w in enumerate(words):
+        v |= int(w) << (64 * i)
+    return (v >> header) & ((1 << budget) - 1)
+
+
+def _as_int(words):
+    v = 0
+    for i, w in enumerate(words):
+        v |= int(w) << (64 * i)
+    return v
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+def test_plane_coder_overlapped_row_worst_cases(zb, precision):
+    bits, header = (32, 9) if precision == 32 else (64, 12)
+    for n, u in enumerate(_adversarial_ints(200, 51 + precision, bits)):
+        for rate in RATES[n % 2::2]:
+            budget = 64 * rate - header
+            got = np.zeros(rate, np.uint64)
+            if precision == 32:
+                zb.zb_encode_ints_rows(np.ascontiguousarray(u.astype(np.uint32)), header, rate, got)
+                want, _ = oracle.encode_ints(u.astype(np.uint32), budget)
+            else:
+                zb.zb_encode_ints64_rows(np.ascontiguousarray(u), header, rate, got)
+                want, _ = oracle.encode_ints64(u, budget)
+            assert _bits_after(got, header, budget) == _as_int(want) & ((1 << budget) - 1), (n, rate)
+            assert _as_int(got) & ((1 << header) - 1) == 0
