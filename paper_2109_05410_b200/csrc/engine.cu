@@ -394,10 +394,17 @@ extern "C" oocz_status oocz_get_nccl_id(uint8_t id[128])
 // bytes of one field's store, rounded up so that stores carved from one arena stay 4 KiB aligned
 static size_t arena_field_bytes(size_t b) { return (b + 4095) / 4096 * 4096; }
 
+#ifdef OOCZ_DEC_NOSTORE
+namespace oocz { void zfp_ab_reset(); }
+using oocz::zfp_ab_reset;
+#endif
 static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t world, const uint8_t* nccl_id,
                                int32_t device, HaloComm* preset_halo, uint8_t* arena, size_t arena_bytes,
                                oocz_ctx** out)
 {
+#ifdef OOCZ_DEC_NOSTORE
+    zfp_ab_reset();   // A/B bound only (zfp.cu)
+#endif
     if (!out) return OOCZ_EINVAL;
     *out = nullptr;
     char msg[256];
@@ -1248,6 +1255,12 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
             z0 = std::max(h - 4 * (ts - s), g.vlo);
             if (has_c) z1 = P + h - 4 * (ts - s);
         }
+#ifdef OOCZ_AB_HALF_STEPS
+        // A/B bound only (tools/fusion_bound.sh): every second step's launch is
+        // skipped, i.e. two leapfrog steps cost one pass over the slab -- the
+        // ceiling of on-chip temporal blocking by 2 with no halo recompute
+        if (s % 2 == 0) { std::swap(cu, cp); continue; }
+#endif
         // algorithmic bytes: read u, u-, m and write u+ once per updated cell
         prof_begin(ctx, sweep, i, OOCZ_ST_STENCIL, 1, sc, 4ull * (uint64_t)std::max(z1 - z0, 0) * pb);
         CK(stencil_step(ctx, cu, cp, slab[OOCZ_M], z0, z1, g.vlo, g.vhi, sc));

@@ -31,6 +31,34 @@ constexpr int kDecThreads = OOCZ_DEC_THREADS;       // fp32 decoder CTA size
 
 struct BlockPos { long long bx, by, bz; };
 
+#ifdef OOCZ_DEC_NOSTORE
+// A/B bound only (tools/fusion_bound.sh): the decoder skips its slab stores once
+// a context has made OOCZ_DEC_NOSTORE_AFTER decode launches (default 40: the
+// warm-up sweeps), so the slabs hold real data from earlier blocks and the
+// stencil and encoder see realistic values (with stores skipped from the first
+// launch the slabs stay zero and the encoder codes all-zero blocks -- the
+// round-2 bound measured that, not the stores)
+__device__ int g_dec_skip_store;
+std::atomic<int> g_dec_launches{0};
+#endif
+
+// Cache policy of the decoder's slab stores / the encoder's slab loads (A/B:
+// OOCZ_DEC_STCS = streaming stores, OOCZ_ENC_LDCS = streaming loads)
+__device__ __forceinline__ void st_slab(float* p, float4 v) {
+#ifdef OOCZ_DEC_STCS
+    __stcs(reinterpret_cast<float4*>(p), v);
+#else
+    *reinterpret_cast<float4*>(p) = v;
+#endif
+}
+__device__ __forceinline__ float4 ld_slab(const float* p) {
+#ifdef OOCZ_ENC_LDCS
+    return __ldcs(reinterpret_cast<const float4*>(p));
+#else
+    return __ldg(reinterpret_cast<const float4*>(p));
+#endif
+}
+
 // Coalesced stage-in of a CTA's contiguous stream words into shared memory,
 // block by block with a row stride of S words: word w goes to words[(w / rate)
 // S + w % rate].  Then each row's words [rate, S) are zeroed: the padded
@@ -133,7 +161,7 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         for (int k = 0; k < 4; k++)
 #pragma unroll
             for (int j = 0; j < 4; j++) {
-                const float4 f = __ldg(reinterpret_cast<const float4*>(base + ((size_t)k * ny + j) * nx));
+                const float4 f = ld_slab(base + ((size_t)k * ny + j) * nx);
                 v[16 * k + 4 * j + 0] = __float_as_uint(f.x);
                 v[16 * k + 4 * j + 1] = __float_as_uint(f.y);
                 v[16 * k + 4 * j + 2] = __float_as_uint(f.z);
@@ -220,7 +248,7 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
             for (int k = 0; k < 4; k++)
 #pragma unroll
                 for (int j = 0; j < 4; j++)
-                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) = make_float4(0.f, 0.f, 0.f, 0.f);
+                    st_slab(base + ((size_t)k * ny + j) * nx, make_float4(0.f, 0.f, 0.f, 0.f));
             continue;
         }
         uint64_t* planes = planes_all + s * 32 * kDecThreads;
@@ -245,8 +273,8 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
         // if-converts into both paths); emax >= -96 is the FMUL path of
         // zb::dequantize, the rest its fp64 path
         const int em = emax[s];
-#ifdef OOCZ_DEC_NOSTORE     // A/B bound for fusion (tools/fusion_bound.py): all the work, no output stores
-        if (em >= -96) {
+#ifdef OOCZ_DEC_NOSTORE     // A/B bound for fusion (tools/fusion_bound.sh): all the work, no output stores
+        if (em >= -96 && g_dec_skip_store) {
             const float sc = __int_as_float((em - 30 + 127) << 23);
             uint32_t acc = 0;
 #pragma unroll
@@ -262,9 +290,9 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const int l = 16 * k + 4 * j;
-                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
-                        make_float4(__fmul_rn(__int2float_rn(q[l]), sc), __fmul_rn(__int2float_rn(q[l + 1]), sc),
-                                    __fmul_rn(__int2float_rn(q[l + 2]), sc), __fmul_rn(__int2float_rn(q[l + 3]), sc));
+                    st_slab(base + ((size_t)k * ny + j) * nx,
+                            make_float4(__fmul_rn(__int2float_rn(q[l]), sc), __fmul_rn(__int2float_rn(q[l + 1]), sc),
+                                        __fmul_rn(__int2float_rn(q[l + 2]), sc), __fmul_rn(__int2float_rn(q[l + 3]), sc)));
                 }
         } else {
 #pragma unroll
@@ -272,9 +300,9 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
 #pragma unroll
                 for (int j = 0; j < 4; j++) {
                     const int l = 16 * k + 4 * j;
-                    *reinterpret_cast<float4*>(base + ((size_t)k * ny + j) * nx) =
-                        make_float4(zb::dequantize(q[l], em), zb::dequantize(q[l + 1], em),
-                                    zb::dequantize(q[l + 2], em), zb::dequantize(q[l + 3], em));
+                    st_slab(base + ((size_t)k * ny + j) * nx,
+                            make_float4(zb::dequantize(q[l], em), zb::dequantize(q[l + 1], em),
+                                        zb::dequantize(q[l + 2], em), zb::dequantize(q[l + 3], em)));
                 }
         }
     }
@@ -489,6 +517,16 @@ cudaError_t launch_zfp_decode(const uint64_t* in, int nx, int ny, int nz, int ra
         if (e != cudaSuccess) return e;
     }
     const long long grid = (nblocks + kDecThreads - 1) / kDecThreads;
+#ifdef OOCZ_DEC_NOSTORE
+    {
+        static const int after = getenv("OOCZ_DEC_NOSTORE_AFTER") ? atoi(getenv("OOCZ_DEC_NOSTORE_AFTER")) : 40;
+        const int nth = g_dec_launches++;
+        if (nth == 0 || nth == after) {
+            const int v = nth >= after ? 1 : 0;
+            cudaMemcpyToSymbolAsync(g_dec_skip_store, &v, sizeof v, 0, cudaMemcpyHostToDevice, s);
+        }
+    }
+#endif
     zfp_decode_kernel<<<(unsigned)grid, kDecThreads, decode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
                                                                                nblocks, rate, out);
     note_launches(1);
@@ -552,6 +590,10 @@ cudaError_t field_decode(const void* src, int esz, int nx, int ny, int nplanes, 
                     : launch_zfp_decode(static_cast<const uint64_t*>(src), nx, ny, nplanes, rate,
                                         static_cast<float*>(dst), s);
 }
+
+#ifdef OOCZ_DEC_NOSTORE
+void zfp_ab_reset() { g_dec_launches = 0; }
+#endif
 
 }  // namespace oocz
 

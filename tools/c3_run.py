@@ -89,6 +89,7 @@ def main():
     ap.add_argument("--samples", type=int, default=8)
     ap.add_argument("--chunk", type=int, default=16)
     ap.add_argument("--schedules", default="paper_faithful,serpentine")
+    ap.add_argument("--no-parity", action="store_true", help="timing only (A/B variants)")
     args = ap.parse_args()
     nx = ny = args.nx
     nz, P, T, rate = args.nz, args.P, args.T, args.rate
@@ -161,6 +162,9 @@ def main():
                    "device_bytes": st["device_bytes_used"], "pinned_host_bytes": st["host_bytes_pinned"],
                    "create_s": round(t_create, 1), "set_fields_s": round(t_set, 1), "steps_total": nsteps}
             print(sched, json.dumps(run), flush=True)
+            if args.no_parity:
+                res["runs"][spec] = run
+                continue
             # 2) sampled parity vs the oracle on sub-boxes
             # corruption from a cut edge moves 4 cells per step, plus up to 3 cells
             # (one ZFP block) at each of the W + K round trips
