@@ -153,10 +153,11 @@ def host_info() -> dict:
     return info
 
 
-def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
+def host_link_probe(nbytes: int = 1 << 30, reps: int = 6) -> dict:
     """Measured host-link peak (the out-of-core roofline's denominator):
     pinned cudaMemcpyAsync H2D alone, D2H alone, and both at once on two
-    streams (the pipeline's situation), CUDA events, best of `reps`."""
+    streams (the pipeline's situation; each direction's rate from its own
+    stream's elapsed time), CUDA events, best of `reps`."""
     import torch
     h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
     h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
@@ -164,8 +165,8 @@ def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
     d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
 
-    def run(h2d: bool, d2h: bool) -> float:
-        best = 0.0
+    def run(h2d: bool, d2h: bool):
+        best = [0.0, 0.0]
         for _ in range(reps):
             torch.cuda.synchronize()
             e0 = torch.cuda.Event(enable_timing=True)
@@ -181,12 +182,16 @@ def host_link_probe(nbytes: int = 512 << 20, reps: int = 5) -> dict:
             e1.record(s1)
             e2.record(s2)
             torch.cuda.synchronize()
-            ms = max(e0.elapsed_time(e1), e0.elapsed_time(e2))
-            best = max(best, nbytes / (ms / 1e3) / 1e9)
+            for i, e in enumerate((e1, e2)):
+                best[i] = max(best[i], nbytes / (e0.elapsed_time(e) / 1e3) / 1e9)
         return best
 
-    return {"h2d_GBps": round(run(True, False), 2), "d2h_GBps": round(run(False, True), 2),
-            "concurrent_per_direction_GBps": round(run(True, True), 2), "bytes": nbytes}
+    h2d_alone = run(True, False)[0]
+    d2h_alone = run(False, True)[1]
+    both = run(True, True)
+    return {"h2d_GBps": round(h2d_alone, 2), "d2h_GBps": round(d2h_alone, 2),
+            "concurrent_h2d_GBps": round(both[0], 2), "concurrent_d2h_GBps": round(both[1], 2),
+            "concurrent_per_direction_GBps": round(min(both), 2), "bytes": nbytes}
 
 
 def lanes_summary(evs) -> dict:
@@ -261,9 +266,9 @@ def codec_alu_roofline(table) -> dict | None:
     not by HBM: their fraction is the ALU pipe's share of its peak issue rate
     (148 SMs x 4 sub-partitions x one warp-instruction per 2 cycles at 1965 MHz),
     measured by ncu (sm__inst_executed_pipe_alu) on the committed capture of the
-    C3-wide launch shape (profiles/r02_ncu_kernels.json)."""
+    C3-wide launch shape (profiles/r02b_ncu_kernels.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r02_ncu_kernels.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02b_ncu_kernels.json")) as fh:
             kj = json.load(fh)["c3_slab"]
     except Exception:
         return None
@@ -278,7 +283,7 @@ def codec_alu_roofline(table) -> dict | None:
                      "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
                      "issue_active": round(k["issue_active_pct"] / 100, 4), "isolated_us": k["us"],
                      "in_step_avg_ms": table[stage]["avg_launch_ms"] if stage in table else None,
-                     "source": "profiles/r02_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16)"}
+                     "source": "profiles/r02b_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16, round-2 codec)"}
     return out or None
 
 
@@ -460,7 +465,8 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
     h = c3["headline"]
     roof, table = roofline(h["evs"], peak_gbs, peak_src)
     busier = max(h["h2d_per_sweep"], h["d2h_per_sweep"])
-    link_peak = link["concurrent_per_direction_GBps"]
+    # the busier direction against its own rate with both directions busy
+    link_peak = link["concurrent_d2h_GBps" if h["d2h_per_sweep"] >= h["h2d_per_sweep"] else "concurrent_h2d_GBps"]
     rep = {
         "value": round(h["cups"], 1),
         "ms_per_step": round(h["device_s"] * 1e3 / args.steps, 3),
@@ -478,7 +484,7 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
             "h2d_GBps": round(h["h2d_GBps"], 2), "d2h_GBps": round(h["d2h_GBps"], 2),
             "peak_source": "measured in this run: pinned H2D and D2H at once on two streams (host_link_probe)",
             "what": "the out-of-core roofline (SURVEY 8(d)): bytes the busier direction must move per sweep / "
-                    "time, over the measured concurrent per-direction bandwidth",
+                    "time, over that direction's measured bandwidth with both directions busy",
             "host_link_probe": link},
         "kernels_in_step": table,
         "codec_alu_roofline": codec_alu_roofline(table),
@@ -683,7 +689,8 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
            "value_hbm_resident": round(v["cups"], 1),
            "e2e_out_of_core": round(e["cups"], 1),
            "e2e_host_link_frac": round(max(e["h2d_per_sweep"], e["d2h_per_sweep"]) / (e["s"] / steps) / 1e9 /
-                                       link["concurrent_per_direction_GBps"], 4),
+                                       link["concurrent_d2h_GBps" if e["d2h_per_sweep"] >= e["h2d_per_sweep"]
+                                            else "concurrent_h2d_GBps"], 4),
            "e2e_h2d_bytes_per_step": int(e["h2d_per_sweep"]), "e2e_d2h_bytes_per_step": int(e["d2h_per_sweep"]),
            "raw": {"value_hbm_resident": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1)},
            "speedup_zfp_vs_raw": {"hbm_resident": round(v["cups"] / out["raw_dev"]["cups"], 3),
@@ -755,7 +762,7 @@ def gpu_arm(args):
         dist.barrier()
     link = host_link_probe()
     if dist:
-        for k in ("h2d_GBps", "d2h_GBps", "concurrent_per_direction_GBps"):
+        for k in ("h2d_GBps", "d2h_GBps", "concurrent_h2d_GBps", "concurrent_d2h_GBps", "concurrent_per_direction_GBps"):
             link[k] = -D.max_over_ranks(dist, -link[k], device="cuda")      # the slowest rank's link
         link["ranks"] = world
         link["note"] = "all ranks probing at once; the minimum over ranks"

@@ -130,11 +130,7 @@ __device__ __forceinline__ V4<double> ld4(const double* p) {
 }
 // store the lane's 4 results; gx = x of its first cell (columns >= nx are not stored)
 __device__ __forceinline__ void st4(float* p, const float r[4], int gx, int nx) {
-#ifdef OOCZ_STENCIL_STCS
-    if (gx < nx) __stcs(reinterpret_cast<float4*>(p), make_float4(r[0], r[1], r[2], r[3]));
-#else
     if (gx < nx) *reinterpret_cast<float4*>(p) = make_float4(r[0], r[1], r[2], r[3]);
-#endif
 }
 __device__ __forceinline__ void st4(double* p, const double r[4], int gx, int nx) {
     if (gx < nx) *reinterpret_cast<double2*>(p) = make_double2(r[0], r[1]);

@@ -42,22 +42,11 @@ __device__ int g_dec_skip_store;
 std::atomic<int> g_dec_launches{0};
 #endif
 
-// Cache policy of the decoder's slab stores / the encoder's slab loads (A/B:
-// OOCZ_DEC_STCS = streaming stores, OOCZ_ENC_LDCS = streaming loads)
-__device__ __forceinline__ void st_slab(float* p, float4 v) {
-#ifdef OOCZ_DEC_STCS
-    __stcs(reinterpret_cast<float4*>(p), v);
-#else
-    *reinterpret_cast<float4*>(p) = v;
-#endif
-}
-__device__ __forceinline__ float4 ld_slab(const float* p) {
-#ifdef OOCZ_ENC_LDCS
-    return __ldcs(reinterpret_cast<const float4*>(p));
-#else
-    return __ldg(reinterpret_cast<const float4*>(p));
-#endif
-}
+// the decoder's slab stores / the encoder's slab loads (streaming cache hints
+// measured no different on the pipelined device path: DESIGN.md section 13)
+__device__ __forceinline__ void st_slab(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+__device__ __forceinline__ float4 ld_slab(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+
 
 // Coalesced stage-in of a CTA's contiguous stream words into shared memory,
 // block by block with a row stride of S words: word w goes to words[(w / rate)
@@ -189,15 +178,16 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
             }
             zb::fwd_xform(q);
             constexpr int perm[64] = OOCZ_PERM3;
+            // negabinary (q + M) ^ M, M = 0xaaaaaaaa: the add here, the XOR folded into
+            // the transposes (it complements the odd planes)
             uint32_t lo[32], hi[32];
 #pragma unroll
             for (int i = 0; i < 32; i++) {
-                lo[i] = ((uint32_t)q[perm[i]] + zb::kNBMask) ^ zb::kNBMask;
-                hi[i] = ((uint32_t)q[perm[i + 32]] + zb::kNBMask) ^ zb::kNBMask;
+                lo[i] = (uint32_t)q[perm[i]] + zb::kNBMask;
+                hi[i] = (uint32_t)q[perm[i + 32]] + zb::kNBMask;
             }
-            zb::transpose32(lo);
-            zb::transpose32(hi);
-#pragma unroll
+            zb::transpose32<true>(lo);
+            zb::transpose32<true>(hi);
             uint64_t* pl = rows + t * S + kPlaneBase32 + 31;      // plane k at pl[-k]
 #pragma unroll
             for (int k = 0; k < 32; k++) pl[-k] = ((uint64_t)hi[k] << 32) | lo[k];

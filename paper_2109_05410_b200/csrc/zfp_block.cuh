@@ -106,8 +106,27 @@ ZB_UNROLL
     for (int l = 0; l < 16; l++) { int b = 4 * l; inv_lift(q[b], q[b + 1], q[b + 2], q[b + 3]); }
 }
 
+#if defined(__CUDA_ARCH__)
+// (m & a) | (~m & b) and its complement as ONE LOP3 (written out, ptxas splits the
+// disjoint OR into two LOP3s and an add)
+__device__ __forceinline__ uint32_t bitsel(uint32_t m, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xca;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // m ? a : b (LUT over 0xf0, 0xcc, 0xaa)
+    return r;
+}
+__device__ __forceinline__ uint32_t bitsel_not(uint32_t m, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x35;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // ~(m ? a : b)
+    return r;
+}
+#endif
+
 // In-place 32x32 bit transpose, LSB = column 0: afterwards bit i of a[k] is
 // the former bit k of a[i].  5 butterfly levels of 16 masked swaps.
+// NB_ODD: also complement the odd output words, i.e. transpose the input
+// XORed with 0xaaaaaaaa in every word (the negabinary XOR, folded into the
+// last level's LOP3s for free).
+template <bool NB_ODD = false>
 ZB_HD void transpose32(uint32_t a[32]) {
 #if defined(__CUDA_ARCH__)
     // the 16- and 8-bit levels are whole half-word / byte exchanges: one PRMT
@@ -126,18 +145,21 @@ ZB_UNROLL
             a[k + 8] = __byte_perm(x, y, 0x7351);  // (x.b1, y.b1, x.b3, y.b3)
         }
     }
-    // the 4-, 2- and 1-bit levels: the logical right shift as a high multiply
-    // (IMAD.HI on the FMA pipe; the ALU pipe binds the codec kernels) and the
-    // left shift as IMAD.SHL, leaving the three XOR/AND LOP3s on the ALU
+    // the 4-, 2- and 1-bit levels as two bit-selects per pair,
+    //   a' = (a & ~(m << j)) | ((b << j) & (m << j)),  b' = (b & ~m) | ((a >> j) & m),
+    // each one LOP3 on the ALU pipe, with the shifts on the FMA pipe (IMAD.SHL,
+    // and the logical right shift as IMAD.HI): the ALU pipe binds the codec
     uint32_t m = 0x0f0f0f0fu;
 ZB_UNROLL
     for (int j = 4; j != 0; j >>= 1) {
+        const uint32_t mj = m << j;
 ZB_UNROLL
         for (int k = 0; k < 32; k++) {
             if ((k & j) == 0) {
-                const uint32_t t = (__umulhi(a[k], 1u << (32 - j)) ^ a[k + j]) & m;
-                a[k + j] ^= t;
-                a[k] ^= t * (1u << j);
+                const uint32_t x = a[k], y = a[k + j];
+                const uint32_t xs = __umulhi(x, 1u << (32 - j)), ys = y * (1u << j);
+                a[k] = bitsel(mj, ys, x);
+                a[k + j] = (NB_ODD && j == 1) ? bitsel_not(m, xs, y) : bitsel(m, xs, y);   // (k + 1 is odd)
             }
         }
         m ^= m << (j >> 1);
@@ -154,6 +176,8 @@ ZB_UNROLL
         }
         m ^= m << (j >> 1);
     }
+    if (NB_ODD)
+        for (int k = 1; k < 32; k += 2) a[k] = ~a[k];
 #endif
 }
 
@@ -161,10 +185,12 @@ ZB_UNROLL
 // largest magnitude (emax = E - 126, i.e. max(frexp exponent, -126); E = 0 for
 // an all-denormal block), or -1 for an all-zero block.
 ZB_HD int block_exponent(const uint32_t v[64]) {
+    // max of the bit patterns shifted left by one (the sign bit dropped: a
+    // multiply by 2 on the FMA pipe instead of an AND on the ALU pipe)
     uint32_t mx = 0;
 ZB_UNROLL
-    for (int i = 0; i < 64; i++) { uint32_t a = v[i] & 0x7fffffffu; mx = a > mx ? a : mx; }
-    return mx == 0 ? -1 : (int)(mx >> 23);
+    for (int i = 0; i < 64; i++) { uint32_t a = v[i] * 2u; mx = a > mx ? a : mx; }
+    return mx == 0 ? -1 : (int)(mx >> 24);
 }
 
 // q = trunc(x * 2^(30 - emax)), built from the bit fields: x = mant * 2^(max(E,1)-150)
