@@ -761,34 +761,32 @@ ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, i
     while (k >= kmin && (pos < limit || ipm != 0u)) {
         const uint32_t* q = p32 + (pos >> 5);
         const int o = pos & 31;
-        const uint32_t wl = fshr32(q[0], q[1], o), wh = fshr32(q[1], q[2], o);
-        const uint32_t ml = bmask32p(n), mh = shr32c(~0u, 64 - n);
-        const uint32_t aLo = wl & ml, aHi = wh & mh;                 // head
+        const uint64_t W = ((uint64_t)fshr32(q[1], q[2], o) << 32) | fshr32(q[0], q[1], o);
+        const uint64_t head = W & (((uint64_t)shr32c(~0u, 64 - n) << 32) | bmask32p(n));
         const uint32_t fA = (uint32_t)(n < 64);
-        const uint32_t flagA = fA & bit64(wl, wh, n & 63);
-        const bool unit = ipm != 0u || flagA != 0u;
+        const uint32_t flagA = fA & (uint32_t)(W >> (n & 63));    // (bit 0 only)
+        const bool unit = ipm != 0u || (flagA & 1u) != 0u;
         const int u0 = pos + ((n + (int)fA) & ~(int)ipm);          // after the head and its flag
         const uint32_t* qu = p32 + (u0 >> 5);
         const int ou = u0 & 31;
-        const uint32_t ul = fshr32(qu[0], qu[1], ou), uh = fshr32(qu[1], qu[2], ou);
+        const uint64_t U = ((uint64_t)fshr32(qu[1], qu[2], ou) << 32) | fshr32(qu[0], qu[1], ou);
         const int rem = limit - u0;
         const int L = 63 - n < rem ? 63 - n : rem;                   // (>= 0 whenever unit)
-        const uint32_t tLo = ul | ~bmask32p(L), tHi = uh | ~shr32c(~0u, 64 - L);
+        const uint32_t tLo = (uint32_t)U | ~bmask32p(L), tHi = (uint32_t)(U >> 32) | ~shr32c(~0u, 64 - L);
         const int r = tLo ? ctz32nz(tLo) : 32 + ctz32nz(tHi);        // (bit 63 of ~mask(L) is set)
         const int c0 = r + (r < L ? 1 : 0);
-        const int nB = n + r;
-        const uint32_t baseLo = ipm ? xl : aLo, baseHi = ipm ? xh : aHi;
-        const uint32_t one = 1u << (nB & 31);
-        const uint32_t bLo = baseLo | (nB < 32 ? one : 0u);
-        const uint32_t bHi = baseHi | (nB >= 32 ? one : 0u);
+        const int nB = n + r;                                        // <= 63
+        const uint64_t x = ipm ? (((uint64_t)xh << 32) | xl) : head;
+        const uint64_t b = x | (1ull << nB);
         const uint32_t fB = (uint32_t)(nB < 63);
-        const uint32_t contB = fB & bit64(ul, uh, c0 & 63);
-        xl = unit ? bLo : aLo;
-        xh = unit ? bHi : aHi;
-        const bool cont = unit && contB != 0u;
+        const uint32_t contB = fB & (uint32_t)(U >> (c0 & 63));     // (bit 0 only)
+        const uint64_t xn = unit ? b : head;
+        xl = (uint32_t)xn;
+        xh = (uint32_t)(xn >> 32);
+        const bool cont = unit && (contB & 1u) != 0u;
         n = unit ? nB + 1 : n;
         pos = u0 + (unit ? c0 + (int)fB : 0);
-        plane_set(k, ((uint64_t)xh << 32) | xl);   // unconditional: the last store of plane k is final
+        plane_set(k, xn);                          // unconditional: the last store of plane k is final
         k -= cont ? 0 : 1;
         ipm = cont ? ~0u : 0u;
     }
