@@ -767,9 +767,15 @@ ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, i
         const uint32_t flagA = fA & (uint32_t)(W >> (n & 63));    // (bit 0 only)
         const bool unit = ipm != 0u || (flagA & 1u) != 0u;
         const int u0 = pos + ((n + (int)fA) & ~(int)ipm);          // after the head and its flag
-        const uint32_t* qu = p32 + (u0 >> 5);
-        const int ou = u0 & 31;
-        const uint64_t U = ((uint64_t)fshr32(qu[1], qu[2], ou) << 32) | fshr32(qu[0], qu[1], ou);
+        // the unit's window: inside a plane it starts at pos (the window above);
+        // at a plane start after the head (predicated loads: no shared-memory
+        // wavefronts for the lanes that are inside a plane)
+        uint64_t U = W;
+        if (ipm == 0u) {
+            const uint32_t* qu = p32 + (u0 >> 5);
+            const int ou = u0 & 31;
+            U = ((uint64_t)fshr32(qu[1], qu[2], ou) << 32) | fshr32(qu[0], qu[1], ou);
+        }
         const int rem = limit - u0;
         const int L = 63 - n < rem ? 63 - n : rem;                   // (>= 0 whenever unit)
         const uint32_t tLo = (uint32_t)U | ~bmask32p(L), tHi = (uint32_t)(U >> 32) | ~shr32c(~0u, 64 - L);
