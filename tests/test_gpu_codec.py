@@ -19,6 +19,11 @@ def _fields():
         "adversarial": synth.blocks_to_field(rb, 5, 3, 7),       # ragged: 105 blocks < 128 per CTA
         "zeros": np.zeros((8, 8, 8), np.float32),
         "wide": synth.dense(1032, 8, 4, seed=2),                  # 258 blocks: 3 CTAs, ragged tail
+        # white noise: every coefficient significant within the first planes, the
+        # densest early planes -- the worst case of the encoder's overlapped
+        # shared-memory row (planes and stream in one row, zfp.cu)
+        "noise": np.random.default_rng(43).uniform(-1, 1, (16, 16, 32)).astype(np.float32),
+        "noise_signs": (np.random.default_rng(44).integers(0, 2, (8, 8, 64)) * 2 - 1).astype(np.float32),
     }
 
 
