@@ -155,15 +155,19 @@ def host_info() -> dict:
 
 def host_link_probe(nbytes: int = 1 << 30, reps: int = 6) -> dict:
     """Measured host-link peak (the out-of-core roofline's denominator):
-    pinned cudaMemcpyAsync H2D alone, D2H alone, and both at once on two
-    streams (the pipeline's situation; each direction's rate from its own
-    stream's elapsed time), CUDA events, best of `reps`."""
+    cudaMemcpyAsync H2D alone, D2H alone, and both at once on two streams (the
+    pipeline's situation; each direction's rate from its own stream's elapsed
+    time), CUDA events, best of `reps`.  The host buffers come from the same
+    allocator as the store (oocz_host_alloc: THP pages registered with
+    cudaHostRegister), so probe and pipeline copy the same kind of memory."""
     import torch
-    h_in = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
-    h_out = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    from cuda.bindings import runtime as rt
+    from paper_2109_05410_b200 import oocz as Z
+    h_in, h_out = Z.oocz_host_alloc(nbytes), Z.oocz_host_alloc(nbytes)
     d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    H2D, D2H = rt.cudaMemcpyKind.cudaMemcpyHostToDevice, rt.cudaMemcpyKind.cudaMemcpyDeviceToHost
 
     def run(h2d: bool, d2h: bool):
         best = [0.0, 0.0]
@@ -173,11 +177,9 @@ def host_link_probe(nbytes: int = 1 << 30, reps: int = 6) -> dict:
             e0.record(s1)
             s2.wait_event(e0)
             if h2d:
-                with torch.cuda.stream(s1):
-                    d_a.copy_(h_in, non_blocking=True)
+                rt.cudaMemcpyAsync(d_a.data_ptr(), h_in, nbytes, H2D, s1.cuda_stream)
             if d2h:
-                with torch.cuda.stream(s2):
-                    h_out.copy_(d_b, non_blocking=True)
+                rt.cudaMemcpyAsync(h_out, d_b.data_ptr(), nbytes, D2H, s2.cuda_stream)
             e1, e2 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e1.record(s1)
             e2.record(s2)
@@ -186,12 +188,17 @@ def host_link_probe(nbytes: int = 1 << 30, reps: int = 6) -> dict:
                 best[i] = max(best[i], nbytes / (e0.elapsed_time(e) / 1e3) / 1e9)
         return best
 
-    h2d_alone = run(True, False)[0]
-    d2h_alone = run(False, True)[1]
-    both = run(True, True)
+    try:
+        h2d_alone = run(True, False)[0]
+        d2h_alone = run(False, True)[1]
+        both = run(True, True)
+    finally:
+        Z.oocz_host_free(h_in)
+        Z.oocz_host_free(h_out)
     return {"h2d_GBps": round(h2d_alone, 2), "d2h_GBps": round(d2h_alone, 2),
             "concurrent_h2d_GBps": round(both[0], 2), "concurrent_d2h_GBps": round(both[1], 2),
-            "concurrent_per_direction_GBps": round(min(both), 2), "bytes": nbytes}
+            "concurrent_per_direction_GBps": round(min(both), 2), "bytes": nbytes,
+            "host_memory": "oocz_host_alloc (THP pages + cudaHostRegister), as the store"}
 
 
 def lanes_summary(evs) -> dict:
