@@ -264,14 +264,15 @@ zfp_decode_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, int 
             lo[k] = (uint32_t)x;
             hi[k] = (uint32_t)(x >> 32);
         }
-        zb::transpose32(lo);
-        zb::transpose32(hi);
+        // negabinary (u ^ M) - M, M = 0xaaaaaaaa: the XOR folded into the transposes
+        zb::transpose32<false, true>(lo);
+        zb::transpose32<false, true>(hi);
         constexpr int perm[64] = OOCZ_PERM3;
         int32_t q[64];
 #pragma unroll
         for (int i = 0; i < 32; i++) {
-            q[perm[i]] = (int32_t)((lo[i] ^ zb::kNBMask) - zb::kNBMask);
-            q[perm[i + 32]] = (int32_t)((hi[i] ^ zb::kNBMask) - zb::kNBMask);
+            q[perm[i]] = (int32_t)(lo[i] - zb::kNBMask);
+            q[perm[i + 32]] = (int32_t)(hi[i] - zb::kNBMask);
         }
         zb::inv_xform(q);
         // dequantise: one branch per block (not per value, which the compiler

@@ -114,6 +114,16 @@ __device__ __forceinline__ uint32_t bitsel(uint32_t m, uint32_t a, uint32_t b) {
     asm("lop3.b32 %0, %1, %2, %3, 0xca;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // m ? a : b (LUT over 0xf0, 0xcc, 0xaa)
     return r;
 }
+__device__ __forceinline__ uint32_t bitsel_na(uint32_t m, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0x3a;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // m ? ~a : b
+    return r;
+}
+__device__ __forceinline__ uint32_t bitsel_nb(uint32_t m, uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("lop3.b32 %0, %1, %2, %3, 0xc5;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // m ? a : ~b
+    return r;
+}
 __device__ __forceinline__ uint32_t bitsel_not(uint32_t m, uint32_t a, uint32_t b) {
     uint32_t r;
     asm("lop3.b32 %0, %1, %2, %3, 0x35;" : "=r"(r) : "r"(m), "r"(a), "r"(b));   // ~(m ? a : b)
@@ -123,10 +133,16 @@ __device__ __forceinline__ uint32_t bitsel_not(uint32_t m, uint32_t a, uint32_t 
 
 // In-place 32x32 bit transpose, LSB = column 0: afterwards bit i of a[k] is
 // the former bit k of a[i].  5 butterfly levels of 16 masked swaps.
-// NB_ODD: also complement the odd output words, i.e. transpose the input
-// XORed with 0xaaaaaaaa in every word (the negabinary XOR, folded into the
-// last level's LOP3s for free).
-template <bool NB_ODD = false>
+// NB_ODD (encoder): also complement the odd output words, i.e. transpose the
+// input XORed with 0xaaaaaaaa in every word (the negabinary XOR, folded into
+// the last level's LOP3s for free).
+// NB_IN (decoder): transpose the input with its odd words complemented, i.e.
+// XOR every output word with 0xaaaaaaaa.  The 16-, 8-, 4- and 2-bit levels only
+// combine words of equal parity, so the complement of the odd words carries
+// through them untouched (the shifted-in bits fall outside the select masks);
+// the 1-bit level, which pairs word k with k + 1, applies it with two other
+// LOP3 tables.
+template <bool NB_ODD = false, bool NB_IN = false>
 ZB_HD void transpose32(uint32_t a[32]) {
 #if defined(__CUDA_ARCH__)
     // the 16- and 8-bit levels are whole half-word / byte exchanges: one PRMT
@@ -158,8 +174,13 @@ ZB_UNROLL
             if ((k & j) == 0) {
                 const uint32_t x = a[k], y = a[k + j];
                 const uint32_t xs = __umulhi(x, 1u << (32 - j)), ys = y * (1u << j);
-                a[k] = bitsel(mj, ys, x);
-                a[k + j] = (NB_ODD && j == 1) ? bitsel_not(m, xs, y) : bitsel(m, xs, y);   // (k + 1 is odd)
+                if (NB_IN && j == 1) {                      // y is an odd word: use ~y
+                    a[k] = bitsel_na(mj, ys, x);
+                    a[k + j] = bitsel_nb(m, xs, y);
+                } else {
+                    a[k] = bitsel(mj, ys, x);
+                    a[k + j] = (NB_ODD && j == 1) ? bitsel_not(m, xs, y) : bitsel(m, xs, y);   // (k + 1 is odd)
+                }
             }
         }
         m ^= m << (j >> 1);
@@ -178,6 +199,8 @@ ZB_UNROLL
     }
     if (NB_ODD)
         for (int k = 1; k < 32; k += 2) a[k] = ~a[k];
+    if (NB_IN)
+        for (int k = 0; k < 32; k++) a[k] ^= 0xaaaaaaaau;
 #endif
 }
 
