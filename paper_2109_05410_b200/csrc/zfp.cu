@@ -329,8 +329,8 @@ __device__ __forceinline__ void planes_from_ints64(const uint64_t u[64], uint64_
             a[i] = (uint32_t)(u[i] >> (32 * half));
             b[i] = (uint32_t)(u[i + 32] >> (32 * half));
         }
-        zb::transpose32(a);
-        zb::transpose32(b);
+        zb::transpose32<true>(a);             // (the negabinary XOR: odd planes complemented)
+        zb::transpose32<true>(b);
 #pragma unroll
         for (int k = 0; k < 32; k++) pl[-(32 * half + k)] = ((uint64_t)b[k] << 32) | a[k];
     }
@@ -376,7 +376,7 @@ zfp_encode64_kernel(const double* __restrict__ in, int nx, int ny, int nbx, int 
             constexpr int perm[64] = OOCZ_PERM3;
             uint64_t u[64];
 #pragma unroll
-            for (int i = 0; i < 64; i++) u[i] = ((uint64_t)q[perm[i]] + zb::kNBMask64) ^ zb::kNBMask64;
+            for (int i = 0; i < 64; i++) u[i] = (uint64_t)q[perm[i]] + zb::kNBMask64;   // (^ M in the transposes)
             uint64_t* pl = rows + t * S + kPlaneBase64 + 63;   // plane k at pl[-k]
             planes_from_ints64(u, pl);
             zb::encode_planes_rows([&](int k) { return pl[-k]; }, 63, 64 * rate, bw);
@@ -437,8 +437,8 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
             a[k] = (uint32_t)x;
             b[k] = (uint32_t)(x >> 32);
         }
-        zb::transpose32(a);
-        zb::transpose32(b);
+        zb::transpose32<false, true>(a);      // (the negabinary XOR folded in)
+        zb::transpose32<false, true>(b);
         if (half == 1) {
 #pragma unroll
             for (int i = 0; i < 32; i++) { hi[i] = a[i]; hi[i + 32] = b[i]; }
@@ -449,8 +449,8 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
 #pragma unroll
         for (int i = 0; i < 32; i++) {
             const uint64_t u0 = ((uint64_t)hi[i] << 32) | a[i], u1 = ((uint64_t)hi[i + 32] << 32) | b[i];
-            q[perm[i]] = (int64_t)((u0 ^ zb::kNBMask64) - zb::kNBMask64);
-            q[perm[i + 32]] = (int64_t)((u1 ^ zb::kNBMask64) - zb::kNBMask64);
+            q[perm[i]] = (int64_t)(u0 - zb::kNBMask64);
+            q[perm[i + 32]] = (int64_t)(u1 - zb::kNBMask64);
         }
         zb::inv_xform(q);
         // one branch per block: emax >= -960 is zb::dequantize64's one-DMUL path
