@@ -161,8 +161,11 @@ def host_link_probe(nbytes: int = 1 << 30, reps: int = 6) -> dict:
     allocator as the store (oocz_host_alloc: THP pages registered with
     cudaHostRegister), so probe and pipeline copy the same kind of memory."""
     import torch
-    from cuda.bindings import runtime as rt
     from paper_2109_05410_b200 import oocz as Z
+    try:
+        from cuda.bindings import runtime as rt
+    except ImportError:                    # older cuda-python layout
+        from cuda import cudart as rt
     h_in, h_out = Z.oocz_host_alloc(nbytes), Z.oocz_host_alloc(nbytes)
     d_a = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
     d_b = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
