@@ -24,6 +24,10 @@ namespace {
 constexpr int kThreads = 128;
 constexpr int NB = 1;                       // blocks (event streams) per thread
 constexpr int kBlocksPerCTA = kThreads * NB;
+#ifndef OOCZ_ENC_THREADS
+#define OOCZ_ENC_THREADS 128
+#endif
+constexpr int kEncThreads = OOCZ_ENC_THREADS;       // fp32 encoder CTA size
 #ifndef OOCZ_DEC_THREADS
 #define OOCZ_DEC_THREADS 128
 #endif
@@ -113,14 +117,15 @@ constexpr int kPlaneBase32 = 4, kPlaneBase64 = 5;
 // Coalesced copy of nb rows' first rate words (the CTA's contiguous streams)
 // from shared memory to global.  Word i = (row r, column c), advanced with i
 // instead of divided.
+template <int NT>
 __device__ __forceinline__ void copy_rows_out(const uint64_t* rows, int S, uint64_t* __restrict__ dst, int nb, int rate)
 {
     const int t = threadIdx.x;
     const int total = nb * rate;
-    const int dq = kThreads / rate, dr = kThreads - dq * rate;
+    const int dq = NT / rate, dr = NT - dq * rate;
     int r = t / rate, c = t - r * rate;
 #pragma unroll 4
-    for (int i = t; i < total; i += kThreads) {
+    for (int i = t; i < total; i += NT) {
         dst[i] = rows[r * S + c];
         r += dq;
         c += dr;
@@ -136,14 +141,14 @@ __host__ __device__ __forceinline__ int enc_row_stride(int rate, int planes, int
 #ifndef OOCZ_ENC_MINB
 #define OOCZ_ENC_MINB 5
 #endif
-__global__ void __launch_bounds__(kThreads, OOCZ_ENC_MINB)
+__global__ void __launch_bounds__(kEncThreads, OOCZ_ENC_MINB)
 zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby,
                   long long nblocks, int rate, uint64_t* __restrict__ out)
 {
-    extern __shared__ __align__(16) uint64_t rows[];   // [kThreads][S]: planes and stream (above)
+    extern __shared__ __align__(16) uint64_t rows[];   // [kEncThreads][S]: planes and stream (above)
     const int S = enc_row_stride(rate, 32, kPlaneBase32);
     const int t = threadIdx.x;
-    const long long b0 = (long long)blockIdx.x * kBlocksPerCTA;
+    const long long b0 = (long long)blockIdx.x * kEncThreads;
     const long long b = b0 + t;
     zb::RowWriter bw{rows + t * S, 0, 0};
     bw.row[0] = 0ull;
@@ -205,7 +210,8 @@ zfp_encode_kernel(const float* __restrict__ in, int nx, int ny, int nbx, int nby
         bw.zero_tail(rate);
     }
     __syncthreads();
-    copy_rows_out(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kThreads ? (int)(nblocks - b0) : kThreads, rate);
+    copy_rows_out<kEncThreads>(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kEncThreads ? (int)(nblocks - b0) : kEncThreads,
+                              rate);
 }
 
 __global__ void __launch_bounds__(kDecThreads)
@@ -384,7 +390,7 @@ zfp_encode64_kernel(const double* __restrict__ in, int nx, int ny, int nbx, int 
         bw.zero_tail(rate);
     }
     __syncthreads();
-    copy_rows_out(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kThreads ? (int)(nblocks - b0) : kThreads, rate);
+    copy_rows_out<kThreads>(rows, S, out + (size_t)b0 * rate, nblocks - b0 < kThreads ? (int)(nblocks - b0) : kThreads, rate);
 }
 
 // Two phases of 32 planes so that only 32 planes (32 KiB) are in shared memory
@@ -483,7 +489,7 @@ zfp_decode64_kernel(const uint64_t* __restrict__ in, int nx, int ny, int nbx, in
 size_t encode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kThreads * enc_row_stride(rate, 64, kPlaneBase64); }
 size_t decode64_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)(32 * kThreads + kThreads * dec_row_stride(rate)); }
 
-size_t encode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kThreads * enc_row_stride(rate, 32, kPlaneBase32); }
+size_t encode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kEncThreads * enc_row_stride(rate, 32, kPlaneBase32); }
 size_t decode_smem_bytes(int rate) { return sizeof(uint64_t) * (size_t)kDecThreads * dec_row_stride(rate); }
 
 // resident CTAs of a codec kernel on the whole GPU at this rate's shared memory
@@ -518,8 +524,8 @@ cudaError_t launch_zfp_encode(const float* in, int nx, int ny, int nz, int rate,
         cudaError_t e = kernel_smem_setup((const void*)zfp_encode_kernel, (int)encode_smem_bytes(64), attr_done);
         if (e != cudaSuccess) return e;
     }
-    const long long grid = (nblocks + kBlocksPerCTA - 1) / kBlocksPerCTA;
-    zfp_encode_kernel<<<(unsigned)grid, kThreads, encode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
+    const long long grid = (nblocks + kEncThreads - 1) / kEncThreads;
+    zfp_encode_kernel<<<(unsigned)grid, kEncThreads, encode_smem_bytes(rate), s>>>(in, nx, ny, nx / 4, ny / 4,
                                                                            nblocks, rate, out);
     note_launches(1);
     return cudaGetLastError();
