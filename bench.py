@@ -471,6 +471,61 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     return out
 
 
+def paper_problem(Z, device, sweeps: int = 2, warmup: int = 1) -> dict:
+    """The paper's own experiment on this GPU: PAPER.md:182-192 (Table I: 1152^3
+    points, fp64), :208-217 (T = 12, 8 divisions), :212-215 (codes 1-4), the
+    paper's schedule (ascending sweeps, m streamed, the trapezoid cone) out of
+    core from pinned host memory; speedup of each code vs code 1 and its error,
+    next to the paper's 1.16x / 1.18x / 1.20x on V100-PCIe.
+    Inputs DENSE(1) + LAYERED in fp64, generated on the GPU."""
+    import torch
+    from paper_2109_05410_b200 import synth
+    n, tb, P = 1152, 12, 144
+    sample = [0, n // 4, n // 2, 3 * n // 4 - 4, n - 4]
+    out = {"what": "the paper's problem (1152^3 fp64, T = 12, P = 144: 8 z-blocks, its codes 1-4, its schedule), "
+                   "out of core; speedup vs code 1 (the paper: 1.16x / 1.18x / 1.20x, V100-PCIe, PAPER.md:227)",
+           "sweeps": sweeps, "warmup": warmup}
+    ref = None
+    for key, rates in (("1_original", (0, 0, 0)), ("2_rw_32", (0, 32, 0)), ("3_ro_32", (0, 0, 32)),
+                       ("4_rw_ro_24", (0, 24, 24))):
+        cfg = Z.oocz_default_config(n, n, n, tb=tb, block_planes=P, rate=list(rates), store=0, precision=64,
+                                    serpentine=0, m_resident=0, slots=2, cone=1)
+        log(f"paper problem {key}")
+        ctx = Z.oocz_create(cfg, 0, 1, None, device)
+        try:
+            for z0 in range(0, n, 16):
+                d = synth.dense_torch(n, n, n, 1, z0, z0 + 16, fp64=True)
+                Z.oocz_set_field_planes(ctx, Z.OOCZ_U, z0, d)
+                Z.oocz_set_field_planes(ctx, Z.OOCZ_UPREV, z0, d)
+                del d
+                Z.oocz_set_field_planes(ctx, Z.OOCZ_M, z0, synth.layered_torch(n, n, n, z0, z0 + 16, fp64=True))
+            Z.oocz_step(ctx, tb * warmup)
+            torch.cuda.synchronize()
+            s0 = Z.oocz_get_stats(ctx)
+            h0 = time.perf_counter()
+            Z.oocz_step(ctx, tb * sweeps)
+            host_s = time.perf_counter() - h0
+            st = Z.oocz_get_stats(ctx)
+            dev_s = st["last_step_device_ms"] / 1e3
+            cells = n ** 3 * tb * sweeps
+            u = np.concatenate([Z.oocz_get_field_planes(ctx, Z.OOCZ_U, z0, np.empty((4, n, n), np.float64))
+                                for z0 in sample])
+            row = {"rates": list(rates), "value": round(cells / dev_s, 1), "e2e": round(cells / host_s, 1),
+                   "h2d_bytes_per_sweep": (st["h2d_bytes"] - s0["h2d_bytes"]) // sweeps,
+                   "d2h_bytes_per_sweep": (st["d2h_bytes"] - s0["d2h_bytes"]) // sweeps}
+        finally:
+            Z.oocz_destroy(ctx)
+        if ref is None:
+            ref = (row, u)
+        else:
+            err = rel_errors(u, ref[1])
+            row["speedup"] = round(row["value"] / ref[0]["value"], 3)
+            row["normwise_max_rel_error"] = err["normwise_max"]
+            row["mean_pointwise_rel_error"] = err["mean_pointwise_significant"]
+        out[key] = row
+    return out
+
+
 def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
     h = c3["headline"]
     roof, table = roofline(h["evs"], peak_gbs, peak_src)
@@ -779,6 +834,12 @@ def gpu_arm(args):
     with ClockSampler(local) as clk:
         c3 = c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link, clk, info)
         c2 = c2_arm(args, Z, local, peak_gbs, peak_src, link, clk) if world == 1 and not args.no_c2 else None
+        pp = None
+        if world == 1 and not args.quick and not args.no_paper:
+            try:
+                pp = paper_problem(Z, local)
+            except Exception as e:          # a context number: report, do not lose the headline
+                pp = {"error": f"{type(e).__name__}: {e}"[:300]}
     clocks = clk.summary()
     if rank != 0:
         if dist:
@@ -824,6 +885,7 @@ def gpu_arm(args):
         "c3_arena": c3["arena"],
         "headline_run": rep["headline_run"],
         "c2": c2,
+        "paper_problem": pp,
         "host": info,
         "clocks": clocks,
     }
@@ -935,6 +997,7 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=16.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c2", action="store_true")
+    ap.add_argument("--no-paper", action="store_true", help="skip the paper's own 1152^3 fp64 problem")
     ap.add_argument("--quick", action="store_true", help="the C3 headline and C2 rate 16 / raw only")
     ap.add_argument("--oracle-sample", type=float, default=None, help=argparse.SUPPRESS)
     ap.add_argument("--oracle-planes", type=int, default=64, help=argparse.SUPPRESS)

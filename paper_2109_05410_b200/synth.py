@@ -103,8 +103,9 @@ def layered(nx: int, ny: int, nz: int, z0: int = 0, z1: int | None = None,
 # same order, so the values are bit-identical to dense() / layered() (checked
 # by tests/test_synth_gpu.py and on every run of the C3-scale parity test).
 
-def dense_torch(nx: int, ny: int, nz: int, seed: int, z0: int, z1: int, device="cuda"):
-    """Planes [z0, z1) of DENSE(seed) as an fp32 torch tensor on `device`."""
+def dense_torch(nx: int, ny: int, nz: int, seed: int, z0: int, z1: int, device="cuda", fp64: bool = False):
+    """Planes [z0, z1) of DENSE(seed) as an fp32 (or, fp64 = True, the unrounded
+    fp64) torch tensor on `device`."""
     import torch
     i = np.arange(nx, dtype=np.float64)
     j = np.arange(ny, dtype=np.float64)
@@ -115,11 +116,11 @@ def dense_torch(nx: int, ny: int, nz: int, seed: int, z0: int, z1: int, device="
         sy = torch.from_numpy(np.sin(2 * np.pi * j / lam[1] + ph[1])).to(device)
         asz = torch.from_numpy(a * np.sin(2 * np.pi * k / lam[2] + ph[2])).to(device)   # a * sz, as numpy
         out += asz[:, None, None] * (sy[:, None] * sx[None, :])[None, :, :]
-    return out.to(torch.float32)
+    return out if fp64 else out.to(torch.float32)
 
 
-def layered_torch(nx: int, ny: int, nz: int, z0: int, z1: int, device="cuda", _lat={}):
-    """Planes [z0, z1) of LAYERED as an fp32 torch tensor on `device`."""
+def layered_torch(nx: int, ny: int, nz: int, z0: int, z1: int, device="cuda", fp64: bool = False, _lat={}):
+    """Planes [z0, z1) of LAYERED as an fp32 (or fp64) torch tensor on `device`."""
     import torch
     key = (nx, ny, str(device))
     if key not in _lat:
@@ -131,7 +132,7 @@ def layered_torch(nx: int, ny: int, nz: int, z0: int, z1: int, device="cuda", _l
     k = np.arange(z0, z1)
     vel = torch.from_numpy(np.array([1500.0, 2500.0, 3500.0, 4500.0])[np.minimum((4 * k) // max(nz, 1), 3)]).to(device)
     t = vel[:, None, None] * _lat[key][None, :, :] * 0.4 / 4500.0
-    return (t * t).to(torch.float32)
+    return t * t if fp64 else (t * t).to(torch.float32)
 
 
 def random_blocks(nblocks: int, seed: int) -> np.ndarray:
