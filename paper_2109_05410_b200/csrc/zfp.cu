@@ -23,7 +23,6 @@ namespace {
 
 constexpr int kThreads = 128;
 constexpr int NB = 1;                       // blocks (event streams) per thread
-constexpr int kBlocksPerCTA = kThreads * NB;
 #ifndef OOCZ_ENC_THREADS
 #define OOCZ_ENC_THREADS 128
 #endif
