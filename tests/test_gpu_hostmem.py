@@ -57,3 +57,27 @@ def test_host_store_context_uses_pinned_store():
         finally:
             Z.oocz_destroy(ctx)
     assert np.array_equal(out[Z.OOCZ_STORE_HOST].view(np.uint32), out[Z.OOCZ_STORE_DEVICE].view(np.uint32))
+
+
+def test_host_alloc_without_thp_falls_back_to_cudahostalloc():
+    """OOCZ_NO_THP=1 (read at allocation time): the >= 1 GiB path is cudaHostAlloc
+    instead, usable and freed the same way (a fresh process: the variable is read
+    by the library, not cached by this one)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import ctypes as C, numpy as np, torch\n"
+        "from paper_2109_05410_b200 import oocz as Z\n"
+        "n = (1 << 30) + (1 << 20)\n"
+        "p = Z.oocz_host_alloc(n)\n"
+        "h = np.ctypeslib.as_array(C.cast(p, C.POINTER(C.c_uint8)), shape=(n,))\n"
+        "h[-4096:] = 7\n"
+        "d = torch.from_numpy(h[-4096:]).to('cuda')\n"
+        "assert int(d.sum()) == 7 * 4096\n"
+        "Z.oocz_host_free(p)\n"
+        "print('ok')\n")
+    env = dict(os.environ, OOCZ_NO_THP="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-2000:]
