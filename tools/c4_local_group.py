@@ -25,7 +25,8 @@ from paper_2109_05410_b200 import synth  # noqa: E402
 def run(world, args, planes):
     n, nz = 4096, 1536
     # (m streamed: two ranks' resident m would not fit one GPU's HBM)
-    cfg = Z.oocz_default_config(n, n, nz, tb=4, block_planes=args.P, rate=[16] * 3, serpentine=1, slots=2)
+    cfg = Z.oocz_default_config(n, n, nz, tb=4, block_planes=args.P, rate=[16] * 3, serpentine=1, slots=2,
+                                slab_sets=args.sets if world > 1 else 0)
     S = nz // world
     ctxs = Z.oocz_create_local_group(cfg, world) if world > 1 else [Z.oocz_create(cfg)]
     try:
@@ -59,6 +60,7 @@ def main():
     ap.add_argument("--world", type=int, default=2)
     ap.add_argument("--sweeps", type=int, default=2)
     ap.add_argument("--P", type=int, default=64)
+    ap.add_argument("--sets", type=int, default=0, help="slab sets per rank (0: the library default)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     S = 1536 // args.world
