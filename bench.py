@@ -221,7 +221,7 @@ def lanes_summary(evs) -> dict:
 
 # DRAM bytes / algorithmic bytes per launch of each hot kernel, from the committed
 # ncu --set full capture of the C3-wide launch shape (tools/ncu_r02.sh)
-TRAFFIC_JSON = "r02_stencil_c3_traffic.json"
+TRAFFIC_JSON = "r02e_stencil_c3_traffic.json"
 TRAFFIC_KEY = {"stencil": "traffic_over_algorithmic", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}
 ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
 
@@ -276,9 +276,9 @@ def codec_alu_roofline(table) -> dict | None:
     not by HBM: their fraction is the ALU pipe's share of its peak issue rate
     (148 SMs x 4 sub-partitions x one warp-instruction per 2 cycles at 1965 MHz),
     measured by ncu (sm__inst_executed_pipe_alu) on the committed capture of the
-    C3-wide launch shape (profiles/r02d_ncu_kernels.json)."""
+    C3-wide launch shape (profiles/r02e_ncu_kernels.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r02d_ncu_kernels.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02e_ncu_kernels.json")) as fh:
             kj = json.load(fh)["c3_slab"]
     except Exception:
         return None
@@ -293,7 +293,7 @@ def codec_alu_roofline(table) -> dict | None:
                      "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
                      "issue_active": round(k["issue_active_pct"] / 100, 4), "isolated_us": k["us"],
                      "in_step_avg_ms": table[stage]["avg_launch_ms"] if stage in table else None,
-                     "source": "profiles/r02d_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16, round-2 codec)"}
+                     "source": "profiles/r02e_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16, round-2 codec)"}
     return out or None
 
 
@@ -643,6 +643,37 @@ def run_mode_c2(Z, store, rates, fields, device, steps, warmup, profile, m_resid
         raise
 
 
+def in_core_c2(Z, fields, steps, warmup, ref_u, peak_gbs) -> dict:
+    """C2 in core (BASELINE configs[1] "in-core vs compressed-transit"): raw u, u-, m
+    resident in HBM, stepped by the stateless leapfrog entry point (one stencil
+    launch per step over all 512 planes: no z-blocks, no codec, no copies).  The
+    same (warmup + steps) x T steps as the engine's raw run, whose u it must equal
+    bit for bit (the block schedule computes the in-core leapfrog)."""
+    import torch
+    u = torch.from_numpy(np.ascontiguousarray(fields[0])).cuda()
+    up = torch.from_numpy(np.ascontiguousarray(fields[1])).cuda()
+    m = torch.from_numpy(np.ascontiguousarray(fields[2])).cuda()
+    s = torch.cuda.current_stream()
+    c = Z.default_coeffs()
+    Z.oocz_stencil_steps(u, up, m, NX, NY, NZ, c, warmup * T, s)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    l0 = Z.oocz_kernel_launch_count()
+    a.record(s)
+    Z.oocz_stencil_steps(u, up, m, NX, NY, NZ, c, steps * T, s)
+    b.record(s)
+    torch.cuda.synchronize()
+    t = a.elapsed_time(b) / 1e3
+    upd = NX * NY * NZ * steps * T
+    got = u.cpu().numpy()
+    return {"value": round(upd / t, 1), "steps": steps * T, "launches": Z.oocz_kernel_launch_count() - l0,
+            "achieved_GBps": round(16 * upd / t / 1e9, 1), "hbm_frac": round(16 * upd / t / 1e9 / peak_gbs, 4),
+            "bit_identical_to_engine_raw": bool(np.array_equal(got.view(np.uint32), ref_u.view(np.uint32))),
+            "what": "raw fields in HBM stepped by oocz_stencil_steps (16 B per cell-update); the compressed "
+                    "paths' value_hbm_resident is set against this; hbm_frac is against the 1:1 copy peak, "
+                    "which the stencil's 3:1 read:write mix can exceed"}
+
+
 def isolated_kernels(Z, fields, peak_gbs, reps: int = 10) -> dict:
     """Each hot kernel alone on one block's slab (P + 2h planes of the C2 data),
     CUDA events on the launching stream, L2 flushed between launches; achieved =
@@ -761,6 +792,7 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
            "speedup_zfp_vs_raw": {"hbm_resident": round(v["cups"] / out["raw_dev"]["cups"], 3),
                                   "out_of_core": round(e["cups"] / out["raw_host"]["cups"], 3)},
            "max_rel_error": err,
+           "in_core": in_core_c2(Z, fields, steps, warmup, out["raw_dev"]["u"], peak_gbs),
            "roofline_in_step": roof, "kernels_in_step": table, "lanes": lanes_summary(v["evs"]),
            "schedule": "HBM-resident: m_resident=1; out of core: serpentine=1, m_resident=1, slots=3"}
     if "pf_raw_host" in out:
