@@ -502,6 +502,28 @@ ZB_HD uint64_t shr64c(uint64_t v, int s) {
     return s >= 64 ? 0ull : v >> s;
 #endif
 }
+// a + b on the FMA pipe: an IMAD whose multiplier is a constant-bank word
+// ptxas cannot fold (so it does not turn it back into an IADD3).  The decoder's
+// event loop is bound by the integer ALU pipe while the FMA pipe has room
+// (ncu: ALU 78 %, FMA 27 %): its additions go there (ALU-pipe instructions per
+// event 53 -> 47; decode64 288.8 -> 283.5 us, fp32 decode within the noise; the
+// same in the encoder's loop measured no faster: tools/ab_fma_adds.sh,
+// profiles/r02_ab_fma_adds.txt).  OOCZ_FMA_ADDS=0 gives plain additions.
+#ifndef OOCZ_FMA_ADDS
+#define OOCZ_FMA_ADDS 1
+#endif
+#if defined(__CUDACC__)
+static __constant__ int zb_one = 1;
+#endif
+ZB_HD int addf(int a, int b) {
+#if defined(__CUDA_ARCH__) && OOCZ_FMA_ADDS
+    int r;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(zb_one), "r"(b));
+    return r;
+#else
+    return a + b;
+#endif
+}
 // low min(m, 32) bits set for m >= 0: one BMSK
 ZB_HD uint32_t bmask32p(int m) {
 #if defined(__CUDA_ARCH__)
@@ -583,20 +605,22 @@ ZB_HD void encode_planes_rows(PlaneAt plane_at, int top_plane, int limit, RowWri
         const uint32_t rl = xl & ~ml, rh = xh & ~mh;
         const bool lnz = rl != 0u;
         const bool has = lnz || rh != 0u;
-        const int tz = lnz ? ctz32nz(rl | (lnz ? 0u : 1u)) : 32 + ctz32nz(rh | 0x80000000u);
+        const int tz = ctz32nz(lnz ? rl : (rh | 0x80000000u)) + (lnz ? 0 : 32);
         const uint64_t r = ((uint64_t)rh << 32) | rl;
         const uint64_t r2 = r & (r - 1ull);
         const bool last = r2 == 0ull;
         const bool implied = tz == 63;
         const int nsub = n & (int)ipm;                 // unit start: 0 at a plane start, n inside
-        const int onep = tz + 1 - nsub;                // position of the one in the emission
+        const int tz1 = tz + 1;
+        const int onep = tz1 - nsub;             // position of the one in the emission
         const int fpos = has ? (n & ~(int)ipm) : 64;   // the 1 flag after the head (none: no bit)
         const int opos = (has && !implied) ? onep : 64;
         const uint64_t v = head | shl64c(1ull, fpos) | shl64c(1ull, opos);
-        const int len = has ? onep + (implied ? 0 : 1 + (last ? 1 : 0)) : (n < 64 ? n + 1 : 64);
+        const int n1 = n + 1, lenu = onep + (implied ? 0 : (last ? 2 : 1));
+        const int len = has ? lenu : (n < 64 ? n1 : 64);
         bw.put(v, len);
         const bool done = !has || last;
-        n = has ? tz + 1 : n;
+        n = has ? tz1 : n;
         k -= done ? 1 : 0;
         ipm = done ? 0u : ~0u;
         x = done ? plane_at(k & top_plane) : r2;      // (k = -1 reads a valid plane, unused)
@@ -785,11 +809,11 @@ ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, i
         const uint32_t* q = p32 + (pos >> 5);
         const int o = pos & 31;
         const uint64_t W = ((uint64_t)fshr32(q[1], q[2], o) << 32) | fshr32(q[0], q[1], o);
-        const uint64_t head = W & (((uint64_t)shr32c(~0u, 64 - n) << 32) | bmask32p(n));
+        const uint64_t head = W & (((uint64_t)shr32c(~0u, addf(-n, 64)) << 32) | bmask32p(n));
         const uint32_t fA = (uint32_t)(n < 64);
         const uint32_t flagA = fA & (uint32_t)(W >> (n & 63));    // (bit 0 only)
         const bool unit = ipm != 0u || (flagA & 1u) != 0u;
-        const int u0 = pos + ((n + (int)fA) & ~(int)ipm);          // after the head and its flag
+        const int u0 = addf(pos, addf(n, (int)fA) & ~(int)ipm);   // after the head and its flag
         // the unit's window: inside a plane it starts at pos (the window above);
         // at a plane start after the head (predicated loads: no shared-memory
         // wavefronts for the lanes that are inside a plane)
@@ -801,10 +825,10 @@ ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, i
         }
         const int rem = limit - u0;
         const int L = 63 - n < rem ? 63 - n : rem;                   // (>= 0 whenever unit)
-        const uint32_t tLo = (uint32_t)U | ~bmask32p(L), tHi = (uint32_t)(U >> 32) | ~shr32c(~0u, 64 - L);
-        const int r = tLo ? ctz32nz(tLo) : 32 + ctz32nz(tHi);        // (bit 63 of ~mask(L) is set)
-        const int c0 = r + (r < L ? 1 : 0);
-        const int nB = n + r;                                        // <= 63
+        const uint32_t tLo = (uint32_t)U | ~bmask32p(L), tHi = (uint32_t)(U >> 32) | ~shr32c(~0u, addf(-L, 64));
+        const int r = addf(ctz32nz(tLo ? tLo : tHi), tLo ? 0 : 32);  // (bit 63 of ~mask(L) is set)
+        const int c0 = addf(r, r < L ? 1 : 0);
+        const int nB = addf(n, r);                                   // <= 63
         const uint64_t x = ipm ? (((uint64_t)xh << 32) | xl) : head;
         const uint64_t b = x | (1ull << nB);
         const uint32_t fB = (uint32_t)(nB < 63);
@@ -813,10 +837,11 @@ ZB_HD void decode_planes_padded(PadDecState& st, int kmin, PlaneSet plane_set, i
         xl = (uint32_t)xn;
         xh = (uint32_t)(xn >> 32);
         const bool cont = unit && (contB & 1u) != 0u;
-        n = unit ? nB + 1 : n;
-        pos = u0 + (unit ? c0 + (int)fB : 0);
+        const int nB1 = addf(nB, 1), pn = addf(u0, addf(c0, (int)fB));
+        n = unit ? nB1 : n;
+        pos = unit ? pn : u0;
         plane_set(k, xn);                          // unconditional: the last store of plane k is final
-        k -= cont ? 0 : 1;
+        k = addf(k, cont ? 0 : -1);
         ipm = cont ? ~0u : 0u;
     }
     for (; k >= kmin; --k) plane_set(k, 0ull);
