@@ -174,3 +174,26 @@ def test_random_shapes_and_cones_bit_exact(seed):
             got = dup.cpu().numpy()
             assert np.array_equal(bits(got[z0:z1]), bits(want[z0 - zv0:z1 - zv0])), (nx, ny, nz, z0, z1, zv0, zv1)
             assert np.array_equal(bits(got[:z0]), bits(up[:z0])) and np.array_equal(bits(got[z1:]), bits(up[z1:]))
+
+
+@pytest.mark.parametrize("shape", [(64, 30, 24), (1024, 304, 24)])   # one tile column each / chunked (168 tiles)
+def test_every_short_plane_range_bit_exact(shape):
+    """The fp32 kernel marches two planes per iteration (the second predicated
+    off at an odd range end) and, with more tiles than SMs, in z chunks: every
+    update range [z0, z0 + n) with n = 1..9 at the slab's ends and middle,
+    against the oracle bit for bit, planes outside the range untouched."""
+    import torch
+    nx, ny, nz = shape
+    u, up, m = _state(nx, ny, nz, 21)
+    want = oracle.step(u, up, m)
+    du, dm = to_dev(u), to_dev(m)
+    z = Z()
+    for n in range(1, 10):
+        for z0 in sorted({0, (nz - n) // 2, nz - n}):
+            dup = to_dev(up)
+            z.oocz_stencil_step_planes(du, dup, dm, nx, ny, nz, z.default_coeffs(), z0, z0 + n, 0, nz,
+                                       torch.cuda.current_stream())
+            torch.cuda.synchronize()
+            got = dup.cpu().numpy()
+            assert np.array_equal(bits(got[z0:z0 + n]), bits(want[z0:z0 + n])), (n, z0)
+            assert np.array_equal(bits(got[:z0]), bits(up[:z0])) and np.array_equal(bits(got[z0 + n:]), bits(up[z0 + n:]))
