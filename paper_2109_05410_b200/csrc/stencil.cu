@@ -227,9 +227,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
 }
 // a consumer thread's release of a ring slot: every consumer thread arrives
 // (the empty barriers count threads), at an address that depends on the
-// thread's own loads from the slot (acc, see dep_add; zero is 0 at run time)
-__device__ __forceinline__ void release_slot(uint64_t* bar, uint32_t acc, uint32_t zero) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar) + (acc & zero)) : "memory");
+// thread's own loads from the slot (acc, see dep_add; zero is 0 at run time).
+// Barriers are passed as shared-window addresses computed once per thread: the
+// compiler does not hoist the generic-to-shared conversion across the asm's
+// memory clobbers, so per-plane conversions cost instructions.
+__device__ __forceinline__ void release_slot_s(uint32_t bar, uint32_t acc, uint32_t zero) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar + (acc & zero)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_s(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(bar), "r"(parity)
+        : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -336,6 +347,8 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
     constexpr int LS = Lanes<T>::kLaneStride;
     const int cidx = (ty + 4) * SW + 4 + LS * lane;  // this thread's (first) centre in a u stage
     const int ridx = ty * TX + LS * lane;            // ... in a u- / m tile
+    const uint32_t ufull_s = smem_u32(ufull), uempty_s = smem_u32(uempty);
+    const uint32_t rfull_s = smem_u32(rfull), rempty_s = smem_u32(rempty);
     long it = blockIdx.x;
     unsigned gu0 = 0, gr0 = 0;                       // global index of the segment's first u / u- plane
     Seg sg;
@@ -347,10 +360,10 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
         auto uslot = [&](int p) { return (gu0 + (unsigned)(p - pfirst)) % NU; };
         auto wait_u = [&](int p) -> const T* {
             const unsigned g = gu0 + (unsigned)(p - pfirst);
-            mbar_wait(&ufull[g % NU], (g / NU) & 1);
+            mbar_wait_s(ufull_s + 8 * (g % NU), (g / NU) & 1);
             return uring + (g % NU) * kUStage;
         };
-        auto release_u = [&](int p, uint32_t acc) { release_slot(&uempty[uslot(p)], acc, zero); };
+        auto release_u = [&](int p, uint32_t acc) { release_slot_s(uempty_s + 8 * uslot(p), acc, zero); };
 
         V4<T> q[8 + kZU];
         // centres of planes zb-4 .. zb+3; a plane outside [zb, ze) is released as soon
@@ -368,7 +381,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
         }
 
         // one plane z of the march; qq[0..8] are the u centres of planes z-4 .. z+4
-        auto plane_step = [&](const int z, const V4<T>* qq) {
+        auto plane_step = [&](const int z, const V4<T>* qq, T* outz) {
                 const unsigned g = gr0 + (unsigned)(z - zb);
                 const T* rt = rring + (g % NR) * kRStage;
                 const T* crow = uring + uslot(z) * kUStage + cidx;  // plane z already landed
@@ -376,7 +389,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                 if constexpr (kPacked) {
                     // the same arithmetic on the lane's cell pairs (0, 1) and (2, 3)
                     float2 ay[4][2];
-    #pragma unroll
+#pragma unroll
                     for (int d = 1; d <= 4; d++) {
                         const V4<T> a = ld4(crow - d * SW);
                         const V4<T> b = ld4(crow + d * SW);
@@ -390,9 +403,9 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                     // x pairs at even distance are aligned register pairs; at odd distance
                     // they straddle two pairs, so those are two scalar additions
                     float2 ax[4][2];
-    #pragma unroll
+#pragma unroll
                     for (int p = 0; p < 2; p++)
-    #pragma unroll
+#pragma unroll
                         for (int d = 1; d <= 4; d++) {
                             const int lo = 4 + 2 * p - d, hi = 4 + 2 * p + d;
                             ax[d - 1][p] = (d & 1) ? make_float2(__fadd_rn(w[lo], w[hi]), __fadd_rn(w[lo + 1], w[hi + 1]))
@@ -400,7 +413,7 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                         }
                     // the release depends on every load from slot z (see the scalar path)
                     uint32_t acc = 0;
-    #pragma unroll
+#pragma unroll
                     for (int d = 0; d < 4; d++) dep_add(acc, ay[d][0].x);
                     dep_add(acc, ax[3][0].x);
                     release_u(z, acc);
@@ -413,10 +426,10 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                                  c2 = make_float2(cf.c2, cf.c2), c3 = make_float2(cf.c3, cf.c3),
                                  c4 = make_float2(cf.c4, cf.c4);
                     float2 Lv[2];
-    #pragma unroll
+#pragma unroll
                     for (int p = 0; p < 2; p++) {
                         float2 sd[4];
-    #pragma unroll
+#pragma unroll
                         for (int d = 1; d <= 4; d++) {
                             const float2 az = __fadd2_rn(half2of(qq[4 - d], p), half2of(qq[4 + d], p));
                             sd[d - 1] = __fadd2_rn(__fadd2_rn(ax[d - 1][p], ay[d - 1][p]), az);
@@ -428,10 +441,10 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                         L = __ffma2_rn(c4, sd[3], L);
                         Lv[p] = L;
                     }
-                    mbar_wait(&rfull[g % NR], (g / NR) & 1);
+                    mbar_wait_s(rfull_s + 8 * (g % NR), (g / NR) & 1);
                     const V4<T> upv = ld4(rt + ridx);
                     const V4<T> mv = ld4(rt + TX * TY + ridx);
-    #pragma unroll
+#pragma unroll
                     for (int p = 0; p < 2; p++) {
                         const float2 up2 = half2of(upv, p);
                         const float2 r = __ffma2_rn(half2of(mv, p), Lv[p],
@@ -443,16 +456,16 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                     uint32_t accr = 0;
                     dep_add4(accr, upv);
                     dep_add4(accr, mv);
-                    release_slot(&rempty[g % NR], accr, zero);
+                    release_slot_s(rempty_s + 8 * (g % NR), accr, zero);
                 } else {
                     // y-neighbour pairs are summed as they arrive (ay[d][o] = u[y-d] + u[y+d]),
                     // which is the first addition of the prescribed order anyway
                     T ay[4][4];
-    #pragma unroll
+#pragma unroll
                     for (int d = 1; d <= 4; d++) {
                         const V4<T> a = ld4(crow - d * SW);
                         const V4<T> b = ld4(crow + d * SW);
-    #pragma unroll
+#pragma unroll
                         for (int o = 0; o < 4; o++) ay[d - 1][o] = add_rn(a.v[o], b.v[o]);
                     }
                     // x-neighbour pairs (the first addition of the prescribed order too)
@@ -464,11 +477,11 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                     // loads; fp64 loads each 4-cell vector in two halves, 64 apart, so also
                     // ay[d][2], and its x pairs come from four loads per half (ax[3] and ax[1])
                     uint32_t acc = 0;
-    #pragma unroll
+#pragma unroll
                     for (int d = 0; d < 4; d++) dep_add(acc, ay[d][0]);
                     dep_add(acc, ax[3][0]);
                     if (sizeof(T) == 8) {
-    #pragma unroll
+#pragma unroll
                         for (int d = 0; d < 4; d++) dep_add(acc, ay[d][2]);
                         dep_add(acc, ax[1][0]);
                         dep_add(acc, ax[3][2]);
@@ -482,11 +495,11 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                     }
 
                     T Lv[4];
-    #pragma unroll
+#pragma unroll
                     for (int o = 0; o < 4; o++) {
                         const T u0 = uc.v[o];
                         T sd[4];
-    #pragma unroll
+#pragma unroll
                         for (int d = 1; d <= 4; d++) {
                             const T az = add_rn(qq[4 - d].v[o], qq[4 + d].v[o]);
                             sd[d - 1] = add_rn(add_rn(ax[d - 1][o], ay[d - 1][o]), az);
@@ -499,26 +512,27 @@ stencil25_kernel(const __grid_constant__ CUtensorMap tm_u, const __grid_constant
                         Lv[o] = L;
                     }
                     // u- and m are read only now, when they are needed
-                    mbar_wait(&rfull[g % NR], (g / NR) & 1);
+                    mbar_wait_s(rfull_s + 8 * (g % NR), (g / NR) & 1);
                     const V4<T> upv = ld4(rt + ridx);
                     const V4<T> mv = ld4(rt + TX * TY + ridx);
-    #pragma unroll
+#pragma unroll
                     for (int o = 0; o < 4; o++) res[o] = fma_rn(mv.v[o], Lv[o], fma_rn((T)2, uc.v[o], -upv.v[o]));
                     {
                         uint32_t accr = 0;
                         dep_add4(accr, upv);
                         dep_add4(accr, mv);
-                        release_slot(&rempty[g % NR], accr, zero);
+                        release_slot_s(rempty_s + 8 * (g % NR), accr, zero);
                     }
                 }
-                if (active) st4(uprev + (size_t)z * plane + col, res, gx, nx);
+                if (active) st4(outz, res, gx, nx);
         };
-        for (int z = zb; z < ze; z += kZU) {
+        T* outz = uprev + (size_t)zb * plane + col;   // u+ of plane z (advanced per plane)
+        for (int z = zb; z < ze; z += kZU, outz += kZU * plane) {
 #pragma unroll
             for (int j = 0; j < kZU; j++) {
                 if (z + j < ze) {
                     q[8 + j] = ld4(wait_u(z + j + 4) + cidx);
-                    plane_step(z + j, q + j);
+                    plane_step(z + j, q + j, outz + j * plane);
                 }
             }
             // shift the queue by kZU planes (kZU = 2 halves the moves per plane; an
