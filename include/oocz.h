@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define OOCZ_ABI_VERSION 5
+#define OOCZ_ABI_VERSION 6
 
 typedef enum {
     OOCZ_OK = 0,
@@ -99,6 +99,16 @@ typedef struct {
                               every cell updated once per step, the overlap's last two time
                               levels handed from block to block.  Results identical.  0 or
                               1, else OOCZ_EINVAL. */
+    int32_t  resident_blocks; /* K: with store = OOCZ_STORE_HOST, the compressed rows of
+                              z-blocks 0 .. K-1 (all three fields) live in HBM and never cross
+                              the host link; blocks K .. D-1 stream from pinned host memory
+                              as usual.  The host store then holds only the streamed rows,
+                              so a store larger than host RAM runs when its resident part
+                              fits HBM (a hybrid of the two placements; the paper streams
+                              everything, PAPER.md:254 names orchestration future work).
+                              0 (default) = all rows on the host; K = D equals
+                              OOCZ_STORE_DEVICE.  Needs world = 1 and store = HOST for
+                              K > 0; 0 <= K <= D, else OOCZ_EINVAL.  Results identical. */
 } oocz_config;
 
 typedef struct {

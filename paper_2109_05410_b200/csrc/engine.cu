@@ -177,7 +177,12 @@ struct oocz_ctx {
     size_t in_slot_bytes = 0, out_slot_bytes = 0;
     unsigned int* d_flags = nullptr;        // two scan records (input, RT(m)): [0] flags, [1] fp32 max bits, [2..3] fp64 max bits
     // store
+    // The stored rows of planes [0, zres) are in HBM (dstore), those of [zres, S) in
+    // store: zres = S with OOCZ_STORE_DEVICE (dstore aliases store), K * P with
+    // resident_blocks = K on a host store (a hybrid), 0 otherwise.  rows_ptr() maps.
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
+    uint8_t* dstore[3] = {nullptr, nullptr, nullptr};
+    int zres = 0;
     size_t store_bytes[3] = {0, 0, 0};
     bool store_external = false;            // host store carved from a caller-owned arena (oocz_create_ex)
     // streams / events
@@ -255,6 +260,15 @@ double cfl_limit(const C c[5])
 
 // one 4-aligned plane range of a field's store as a byte range
 inline size_t rows_off(const oocz_ctx* c, int f, int plane) { return (size_t)(plane / 4) * c->row_bytes[f]; }
+// where the stored rows from `plane` on live (a block's rows are all in one place)
+inline bool rows_on_device(const oocz_ctx* c, int plane) { return plane < c->zres; }
+inline uint8_t* rows_ptr(const oocz_ctx* c, int f, int plane)
+{
+    return plane < c->zres ? c->dstore[f] + rows_off(c, f, plane)
+                           : c->store[f] + (rows_off(c, f, plane) - rows_off(c, f, c->zres));
+}
+// the end of a chunk of stored rows starting at plane z that stays in one place
+inline int rows_chunk_end(const oocz_ctx* c, int z, int end) { return z < c->zres ? std::min(end, c->zres) : end; }
 
 cudaError_t encode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, uint8_t* dst, cudaStream_t s)
 {
@@ -380,6 +394,13 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
         BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 1, 2, 3, 4}", cfg->slab_sets);
     if (cfg->graphs != 0 && cfg->graphs != 1) BAD(OOCZ_EINVAL, "graphs (%d) must be 0 or 1", cfg->graphs);
     if (cfg->cone != 0 && cfg->cone != 1) BAD(OOCZ_EINVAL, "cone (%d) must be 0 or 1", cfg->cone);
+    if (cfg->resident_blocks < 0 || cfg->resident_blocks > cfg->nz / world / cfg->block_planes)
+        BAD(OOCZ_EINVAL, "resident_blocks (%d) outside [0, D = %d]", cfg->resident_blocks,
+            cfg->nz / world / cfg->block_planes);
+    if (cfg->resident_blocks > 0 && cfg->store != OOCZ_STORE_HOST)
+        BAD(OOCZ_EINVAL, "resident_blocks (%d) needs store = OOCZ_STORE_HOST", cfg->resident_blocks);
+    if (cfg->resident_blocks > 0 && world > 1)
+        BAD(OOCZ_EINVAL, "resident_blocks (%d) needs world = 1", cfg->resident_blocks);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
@@ -493,7 +514,8 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         need += (size_t)cfg->slots * (ctx->in_slot_bytes + ctx->out_slot_bytes);
     }
     for (int f = 0; f < 3; f++) ctx->store_bytes[f] = (size_t)(S / 4) * ctx->row_bytes[f];
-    if (!host) need += ctx->store_bytes[0] + ctx->store_bytes[1] + ctx->store_bytes[2];
+    ctx->zres = host ? std::min(cfg->resident_blocks * P, S) : S;
+    for (int f = 0; f < 3; f++) need += rows_off(ctx, f, ctx->zres);   // the rows kept in HBM
     if (world > 1) need += halo_device_bytes(ctx->plane_elems, h, cfg->rate, ctx->row_bytes);
     if (cfg->m_resident) need += (size_t)(S + 2 * h) * pb;
     {
@@ -528,9 +550,12 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             ctx->in_slot.push_back(a);
             ctx->out_slot.push_back(b);
         }
+        if (ctx->zres > 0)
+            for (int f = 0; f < 3; f++) CKC(cudaMalloc(&ctx->dstore[f], std::max<size_t>(rows_off(ctx, f, ctx->zres), 1)));
+        auto host_part = [&](int f) { return ctx->store_bytes[f] - rows_off(ctx, f, ctx->zres); };
         if (arena) {
             size_t want = 0;
-            for (int f = 0; f < 3; f++) want += arena_field_bytes(ctx->store_bytes[f]);
+            for (int f = 0; f < 3; f++) want += arena_field_bytes(host_part(f));
             cudaPointerAttributes pa{};
             CKC(cudaPointerGetAttributes(&pa, arena));
             if (pa.type != cudaMemoryTypeHost) {
@@ -544,16 +569,20 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             ctx->store_external = true;
             for (int f = 0; f < 3; f++) {
                 ctx->store[f] = arena;
-                arena += arena_field_bytes(ctx->store_bytes[f]);
+                arena += arena_field_bytes(host_part(f));
             }
         } else {
             for (int f = 0; f < 3; f++) {
-                CKC(pinned_alloc(reinterpret_cast<void**>(&ctx->store[f]), ctx->store_bytes[f], cudaHostAllocDefault));
-                ctx->stats.host_bytes_pinned += ctx->store_bytes[f];
+                CKC(pinned_alloc(reinterpret_cast<void**>(&ctx->store[f]), std::max<size_t>(host_part(f), 1),
+                                 cudaHostAllocDefault));
+                ctx->stats.host_bytes_pinned += host_part(f);
             }
         }
     } else {
-        for (int f = 0; f < 3; f++) CKC(cudaMalloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1)));
+        for (int f = 0; f < 3; f++) {
+            CKC(cudaMalloc(&ctx->store[f], std::max<size_t>(ctx->store_bytes[f], 1)));
+            ctx->dstore[f] = ctx->store[f];
+        }
     }
     ctx->stats.device_bytes_used = need;
     CKC(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
@@ -642,9 +671,11 @@ extern "C" oocz_status oocz_create_ex(const oocz_config* cfg, int32_t rank, int3
 extern "C" size_t oocz_host_store_bytes(const oocz_config* cfg, int32_t world)
 {
     if (!cfg || world < 1 || cfg->nz % world) return 0;
+    const int S = cfg->nz / world;
+    const int zres = cfg->resident_blocks > 0 ? std::min(cfg->resident_blocks * cfg->block_planes, S) : 0;
     size_t t = 0;
     for (int f = 0; f < 3; f++)
-        t += arena_field_bytes((size_t)(cfg->nz / world / 4) *
+        t += arena_field_bytes((size_t)((S - zres) / 4) *
                                row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], esz_of(cfg)));
     return t;
 }
@@ -769,6 +800,7 @@ extern "C" void oocz_destroy(oocz_ctx* ctx)
         if (f < 2) cudaFree(ctx->pcopy[f]);
         if (ctx->cfg.store == OOCZ_STORE_HOST) {
             if (!ctx->store_external) pinned_free(ctx->store[f]);
+            cudaFree(ctx->dstore[f]);
         }
         else cudaFree(ctx->store[f]);
     }
@@ -926,21 +958,20 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     ctx->field_set[field] = false;
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     const int chunk = ctx->P;                       // planes per pass, <= slab capacity
-    for (int z = z0; z < z0 + nplanes; z += chunk) {
-        const int np = std::min(chunk, z0 + nplanes - z);
+    for (int z = z0, np; z < z0 + nplanes; z += np) {
+        np = rows_chunk_end(ctx, z, std::min(z + chunk, z0 + nplanes)) - z;
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
         CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb, in_kind, s));
-        const size_t off = rows_off(ctx, field, z);
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         const uint8_t* coded;
-        if (host) {
+        if (!rows_on_device(ctx, z)) {
             uint8_t* dev = ctx->in_slot[0];         // device staging of the encoded rows
             CK(encode_or_copy(ctx, field, buf, np, dev, s));
-            CK(cudaMemcpyAsync(ctx->store[field] + off, dev, bytes, cudaMemcpyDeviceToHost, s));
+            CK(cudaMemcpyAsync(rows_ptr(ctx, field, z), dev, bytes, cudaMemcpyDeviceToHost, s));
             coded = dev;
         } else {
-            CK(encode_or_copy(ctx, field, buf, np, ctx->store[field] + off, s));
-            coded = ctx->store[field] + off;
+            CK(encode_or_copy(ctx, field, buf, np, rows_ptr(ctx, field, z), s));
+            coded = rows_ptr(ctx, field, z);
         }
         if (field == OOCZ_M && ctx->m_full)         // m_resident: keep the decoded RT(m)
             CK(decode_or_copy(ctx, field, coded, np, ctx->m_full + (size_t)(ctx->h + z) * ctx->pb, s));
@@ -1001,20 +1032,18 @@ static oocz_status get_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     if (!dst_v && nplanes) return fail(ctx, OOCZ_EINVAL, "null destination");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t s = ctx->s_comp;
-    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const int chunk = ctx->P;
     uint8_t* dst = static_cast<uint8_t*>(dst_v);
-    for (int z = z0; z < z0 + nplanes; z += chunk) {
-        const int np = std::min(chunk, z0 + nplanes - z);
-        const size_t off = rows_off(ctx, field, z);
+    for (int z = z0, np; z < z0 + nplanes; z += np) {
+        np = rows_chunk_end(ctx, z, std::min(z + chunk, z0 + nplanes)) - z;
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
-        if (host) {
+        if (!rows_on_device(ctx, z)) {
             uint8_t* dev = ctx->in_slot[0];
-            CK(cudaMemcpyAsync(dev, ctx->store[field] + off, bytes, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(dev, rows_ptr(ctx, field, z), bytes, cudaMemcpyHostToDevice, s));
             CK(decode_or_copy(ctx, field, dev, np, buf, s));
         } else {
-            CK(decode_or_copy(ctx, field, ctx->store[field] + off, np, buf, s));
+            CK(decode_or_copy(ctx, field, rows_ptr(ctx, field, z), np, buf, s));
         }
         CK(cudaMemcpyAsync(dst + (size_t)(z - z0) * ctx->pb, buf, (size_t)np * ctx->pb,
                            on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, s));
@@ -1061,8 +1090,9 @@ extern "C" oocz_status oocz_save_store(oocz_ctx* ctx, int32_t field, void* dst, 
     if (bytes != ctx->store_bytes[field] || (!dst && bytes))
         return fail(ctx, OOCZ_EINVAL, "bytes (%zu) != store size (%zu)", bytes, ctx->store_bytes[field]);
     CK(cudaSetDevice(ctx->device));
-    if (ctx->cfg.store == OOCZ_STORE_HOST) std::memcpy(dst, ctx->store[field], bytes);
-    else CK(cudaMemcpy(dst, ctx->store[field], bytes, cudaMemcpyDeviceToHost));
+    const size_t dev_bytes = rows_off(ctx, field, ctx->zres);     // the rows kept in HBM come first
+    if (dev_bytes) CK(cudaMemcpy(dst, ctx->dstore[field], dev_bytes, cudaMemcpyDeviceToHost));
+    if (bytes > dev_bytes) std::memcpy(static_cast<uint8_t*>(dst) + dev_bytes, ctx->store[field], bytes - dev_bytes);
     return OOCZ_OK;
 }
 
@@ -1079,14 +1109,17 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     ctx->field_set[field] = false;
     std::fill(ctx->rows_set[field].begin(), ctx->rows_set[field].end(), 0);
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
-    if (host) std::memcpy(ctx->store[field], src, bytes);
-    else CK(cudaMemcpy(ctx->store[field], src, bytes, cudaMemcpyHostToDevice));
+    {
+        const size_t dev_bytes = rows_off(ctx, field, ctx->zres);
+        if (dev_bytes) CK(cudaMemcpy(ctx->dstore[field], src, dev_bytes, cudaMemcpyHostToDevice));
+        if (bytes > dev_bytes)
+            std::memcpy(ctx->store[field], static_cast<const uint8_t*>(src) + dev_bytes, bytes - dev_bytes);
+    }
     if (field == OOCZ_M && ctx->m_full) {       // m_resident: decode the loaded stream once
         for (int z = 0; z < ctx->S; z += ctx->P) {
             const int np = std::min(ctx->P, ctx->S - z);
-            const size_t off = rows_off(ctx, field, z);
-            const uint8_t* coded = ctx->store[field] + off;
-            if (host) {
+            const uint8_t* coded = rows_ptr(ctx, field, z);
+            if (!rows_on_device(ctx, z)) {
                 CK(cudaMemcpyAsync(ctx->in_slot[0], coded, (size_t)(np / 4) * ctx->row_bytes[field],
                                    cudaMemcpyHostToDevice, s));
                 coded = ctx->in_slot[0];
@@ -1137,7 +1170,9 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const Geom& g = ctx->geom[i];
     const int h = ctx->h, P = ctx->P, D = ctx->D, S = ctx->S;
     const size_t pb = ctx->pb;
-    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
+    // this block's rows stream over the host link (not kept in HBM: device store or
+    // resident_blocks)
+    const bool host = !rows_on_device(ctx, g.own0);
     const int nslots = (int)ctx->ev_in_ready.size();
     const int slot = (int)(ctx->seq % nslots);
     // slab set: blocks rotate through nsets; with serpentine sweeps by block
@@ -1169,8 +1204,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         auto add = [&](int z0, int z1, int owner) {
             if (z1 <= z0) return;
             Part q{z0, z1, nullptr, false};
-            if (!host) {
-                q.src = ctx->store[f] + rows_off(ctx, f, z0);
+            if (rows_on_device(ctx, z0)) {
+                q.src = rows_ptr(ctx, f, z0);
             } else if (f != OOCZ_M && rows_in_slot(ctx, owner)) {
                 q.src = ctx->out_slot[ctx->last_slot[owner]] + ctx->out_off[f] +
                         (size_t)((z0 - owner * P) / 4) * ctx->row_bytes[f];
@@ -1205,7 +1240,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
             for (int k = 0; k < nparts[f]; k++) {
                 const Part& q = part[f][k];
                 if (!q.h2d) continue;
-                CK(cudaMemcpyAsync(const_cast<uint8_t*>(q.src), ctx->store[f] + rows_off(ctx, f, q.z0),
+                CK(cudaMemcpyAsync(const_cast<uint8_t*>(q.src), rows_ptr(ctx, f, q.z0),
                                    (size_t)((q.z1 - q.z0) / 4) * ctx->row_bytes[f], cudaMemcpyHostToDevice, sh));
             }
         prof_end(ctx, sh);
@@ -1366,7 +1401,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
             for (int f = 0; f < 2; f++) bytes += (uint64_t)(P / 4) * ctx->row_bytes[f];
             prof_begin(ctx, sweep, i, OOCZ_ST_D2H, 2, so, bytes);
             for (int f = 0; f < 2; f++)
-                CK(cudaMemcpyAsync(ctx->store[f] + rows_off(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
+                CK(cudaMemcpyAsync(rows_ptr(ctx, f, g.own0), ctx->out_slot[slot] + ctx->out_off[f],
                                    (size_t)(P / 4) * ctx->row_bytes[f], cudaMemcpyDeviceToHost, so));
             prof_end(ctx, so);
             ctx->stats.d2h_bytes += bytes;
@@ -1376,7 +1411,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     } else {
         for (int f = 0; f < 2; f++) {
             prof_begin(ctx, sweep, i, OOCZ_ST_ENCODE, 5, se, (uint64_t)P * pb + (uint64_t)(P / 4) * ctx->row_bytes[f]);
-            CK(encode_or_copy(ctx, f, own[f], P, ctx->store[f] + rows_off(ctx, f, g.own0), se));
+            CK(encode_or_copy(ctx, f, own[f], P, rows_ptr(ctx, f, g.own0), se));
             prof_end(ctx, se);
         }
         CK(cudaEventRecord(ctx->ev_slab_free[set], se));

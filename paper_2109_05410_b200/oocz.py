@@ -36,7 +36,8 @@ class oocz_config(C.Structure):
                 ("rate", C.c_int32 * 3), ("store", C.c_int32), ("slots", C.c_int32),
                 ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32),
                 ("precision", C.c_int32), ("c64", C.c_double * 5), ("serpentine", C.c_int32),
-                ("slab_sets", C.c_int32), ("graphs", C.c_int32), ("cone", C.c_int32)]
+                ("slab_sets", C.c_int32), ("graphs", C.c_int32), ("cone", C.c_int32),
+                ("resident_blocks", C.c_int32)]
 
 
 class oocz_stats(C.Structure):
@@ -109,7 +110,7 @@ for _name, (_res, _args) in _SIGS.items():
     _fn.restype = _res
     _fn.argtypes = _args
 
-ABI_VERSION = 5          # the oocz_config layout this binding marshals (include/oocz.h)
+ABI_VERSION = 6          # the oocz_config layout this binding marshals (include/oocz.h)
 if _lib.oocz_abi_version() != ABI_VERSION:
     raise ImportError(f"{LIB_PATH} has ABI {_lib.oocz_abi_version()}, the binding expects {ABI_VERSION}: rebuild")
 

@@ -27,7 +27,7 @@ def test_every_header_symbol_is_exported(z):
 
 
 def test_abi_version(z):
-    assert z.oocz_abi_version() == z.ABI_VERSION == 5
+    assert z.oocz_abi_version() == z.ABI_VERSION == 6
 
 
 def test_zfp_bytes_closed_form(z):
@@ -62,6 +62,12 @@ def test_cfl_limit_default_coefficients(z):
     (dict(graphs=2, block_planes=32), 1, -1, "graphs (2)"),
     (dict(cone=1, block_planes=32), 1, 0, ""),
     (dict(cone=2, block_planes=32), 1, -1, "cone (2)"),
+    (dict(resident_blocks=2, block_planes=32), 1, 0, ""),
+    (dict(resident_blocks=4, block_planes=32), 1, 0, ""),            # K = D
+    (dict(resident_blocks=5, block_planes=32), 1, -1, "resident_blocks (5) outside [0, D = 4]"),
+    (dict(resident_blocks=-1, block_planes=32), 1, -1, "resident_blocks (-1)"),
+    (dict(resident_blocks=1, block_planes=32, store=1), 1, -1, "needs store = OOCZ_STORE_HOST"),
+    (dict(resident_blocks=1, block_planes=32), 2, -1, "needs world = 1"),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)
@@ -70,6 +76,16 @@ def test_validate(z, kw, world, code, msg):
     rc, m = z.oocz_validate(cfg, world)
     assert rc == code, m
     assert msg in m
+
+
+def test_host_store_bytes_leave_out_the_resident_rows(z):
+    """resident_blocks = K: the host store holds only the rows of blocks K .. D-1
+    (each field's part rounded up to 4 KiB)."""
+    rows = 64 // 4 * 64 // 4 * 8 * 16                     # one 4-plane row of a 64 x 64 plane at rate 16
+    for k in range(5):
+        cfg = z.oocz_default_config(64, 64, 128, tb=4, block_planes=32, resident_blocks=k)
+        part = (128 - 32 * k) // 4 * rows
+        assert z.oocz_host_store_bytes(cfg, 1) == 3 * ((part + 4095) // 4096 * 4096)
 
 
 def test_default_config(z):

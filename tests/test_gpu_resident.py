@@ -1,0 +1,96 @@
+"""Resident blocks (cfg.resident_blocks = K): a host-store context keeps the
+compressed rows of z-blocks 0 .. K-1 in HBM and streams the rest.  The
+placement changes where bytes live, never what is computed, so every case is
+bit-exact against the oracle's reduced schedule; the host link carries only the
+streamed blocks' rows."""
+import numpy as np
+import pytest
+
+from gpu_util import Z, bits
+from test_gpu_engine import CASES, _fields, _run_oracle
+
+pytestmark = pytest.mark.gpu
+
+
+def _cfg(z, nx, ny, nz, T, P, rates, K, **kw):
+    return z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=z.OOCZ_STORE_HOST,
+                                 resident_blocks=K, **kw)
+
+
+def _ks(D):
+    return sorted({1, max(D - 1, 1), D})
+
+
+@pytest.mark.parametrize("serpentine,m_resident,slots", [(0, 0, 2), (1, 1, 3), (1, 0, 2), (0, 1, 3)])
+@pytest.mark.parametrize("nx,ny,nz,T,P,rates,calls", CASES)
+def test_resident_blocks_match_oracle(nx, ny, nz, T, P, rates, calls, serpentine, m_resident, slots):
+    z = Z()
+    u, up, m = _fields(nx, ny, nz, 5)
+    wa, wb = _run_oracle(u, up, m, T, rates, calls)
+    for K in _ks(nz // P):
+        cfg = _cfg(z, nx, ny, nz, T, P, rates, K, serpentine=serpentine, m_resident=m_resident, slots=slots)
+        with z.Stepper(cfg) as s:
+            s.set(u, up, m)
+            for n in calls:
+                s.step(n)
+            assert np.array_equal(bits(s.get(z.OOCZ_U)), bits(wa)), K
+            assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(wb)), K
+
+
+@pytest.mark.parametrize("K", [0, 1, 2, 3, 4])
+def test_resident_blocks_host_bytes(K):
+    """Ascending sweeps: per sweep the H2D bytes are the streamed fields' rows of
+    planes [K P, S) and the D2H bytes u's and u-'s rows of the same planes; the
+    pinned host store holds just those rows."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 32, 128, 2, 32, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz, 9)
+    cfg = _cfg(z, nx, ny, nz, T, P, rates, K)
+    row = [nx // 4 * ny // 4 * 8 * r for r in rates]          # bytes of one 4-plane row per field
+    streamed = (nz - K * P) // 4
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        st0 = s.stats()
+        s.step(3 * T)
+        st = s.stats()
+        assert st["sweeps"] - st0["sweeps"] == 3
+        assert st["h2d_bytes"] - st0["h2d_bytes"] == 3 * streamed * sum(row)
+        assert st["d2h_bytes"] - st0["d2h_bytes"] == 3 * streamed * (row[0] + row[1])
+        assert st["host_bytes_pinned"] == streamed * sum(row)
+        wa, wb = _run_oracle(u, up, m, T, rates, [3 * T])
+        assert np.array_equal(bits(s.get(z.OOCZ_U)), bits(wa))
+        assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(wb))
+
+
+def test_resident_blocks_planes_and_checkpoint_across_the_boundary():
+    """z-range set / get that straddle the resident / streamed boundary, and a
+    checkpoint (save_store / load_store) of a hybrid store restored into a
+    host-only context: the same stream bytes, the same steps."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 24, 20, 96, 2, 24, (16, 16, 16)
+    u, up, m = _fields(nx, ny, nz, 13)
+    cfg = _cfg(z, nx, ny, nz, T, P, rates, 2)                # rows of planes [0, 48) in HBM
+    ref = _cfg(z, nx, ny, nz, T, P, rates, 0)
+    with z.Stepper(cfg) as s, z.Stepper(ref) as r:
+        for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+            for z0, n in ((0, 40), (40, 16), (56, 40)):          # [40, 56) straddles plane 48
+                z.oocz_set_field_planes(s.ctx, f, z0, a[z0:z0 + n])
+            z.oocz_set_field(r.ctx, f, a)
+        for f in (z.OOCZ_U, z.OOCZ_UPREV, z.OOCZ_M):
+            assert np.array_equal(z.oocz_save_store(s.ctx, f), z.oocz_save_store(r.ctx, f))
+        s.step(5)
+        r.step(5)
+        got = np.empty((32, ny, nx), np.float32)
+        z.oocz_get_field_planes(s.ctx, z.OOCZ_U, 32, got)      # [32, 64) straddles plane 48
+        assert np.array_equal(bits(got), bits(r.get(z.OOCZ_U)[32:64]))
+        saved = [z.oocz_save_store(s.ctx, f) for f in (z.OOCZ_U, z.OOCZ_UPREV, z.OOCZ_M)]
+        for f, b in zip((z.OOCZ_U, z.OOCZ_UPREV, z.OOCZ_M), saved):
+            assert np.array_equal(b, z.oocz_save_store(r.ctx, f))
+    with z.Stepper(ref) as t, z.Stepper(_cfg(z, nx, ny, nz, T, P, rates, 3, m_resident=1)) as h:
+        for ctx in (t.ctx, h.ctx):
+            for f, b in zip((z.OOCZ_U, z.OOCZ_UPREV, z.OOCZ_M), saved):
+                z.oocz_load_store(ctx, f, b)
+        t.step(4)
+        h.step(4)
+        assert np.array_equal(bits(h.get(z.OOCZ_U)), bits(t.get(z.OOCZ_U)))
+        assert np.array_equal(bits(h.get(z.OOCZ_UPREV)), bits(t.get(z.OOCZ_UPREV)))
