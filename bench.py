@@ -357,16 +357,37 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     S = nz // world
     store = opt.get("store", 0)
     tb = opt.get("tb", T)
-    cfg = Z.oocz_default_config(nx, ny, nz, tb=tb, block_planes=opt["P"], rate=list(rates), store=store,
-                                m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
-                                slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile,
-                                cone=opt.get("cone", 0))
+    def make_cfg(k=0, budget=0):
+        return Z.oocz_default_config(nx, ny, nz, tb=tb, block_planes=opt["P"], rate=list(rates), store=store,
+                                     m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
+                                     slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile,
+                                     cone=opt.get("cone", 0), resident_blocks=k, device_bytes=budget)
+    cfg = make_cfg()
     if callable(nccl_id):
         nccl_id = nccl_id()
     torch.cuda.empty_cache()             # the generator's chunks: HBM for the context (C3 fills it)
     log(f"{label}: grid {nx}x{ny}x{nz} rates {list(rates)} {opt} W={warmup} K={steps}")
     t0 = time.perf_counter()
-    if store == 0:
+    resident = 0
+    if opt.get("resident_blocks") == "max":
+        # the most z-blocks whose compressed rows fit in HBM (8 GiB left for the
+        # field generator); the rest must fit the pinned arena
+        budget = torch.cuda.mem_get_info(device)[0] - (8 << 30)
+        ctx = None
+        for k in range(S // opt["P"], -1, -1):
+            cfg = make_cfg(k, budget)
+            if Z.oocz_host_store_bytes(cfg, world) > arena[1]:
+                break
+            try:
+                ctx = Z.oocz_create_ex(cfg, rank, world, nccl_id, device, arena[0], arena[1])
+                resident = k
+                break
+            except Z.OoczError as e:
+                if e.status != Z.OOCZ_ECAPACITY:
+                    raise
+        if ctx is None:
+            raise RuntimeError(f"{label}: no resident_blocks split fits HBM and the {arena[1] / 1e9:.1f} GB arena")
+    elif store == 0:
         ctx = Z.oocz_create_ex(cfg, rank, world, nccl_id, device, arena[0], arena[1])
     else:
         ctx = Z.oocz_create(cfg, rank, world, nccl_id, device)
@@ -403,7 +424,8 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
                "sweeps": steps, "warmup": warmup, "launches": launches,
                "h2d_per_sweep": h2d, "d2h_per_sweep": d2h, "halo_per_sweep": (st["halo_bytes"] - st0["halo_bytes"]) / max(sweeps, 1),
                "h2d_GBps": h2d * steps / dev_s / 1e9, "d2h_GBps": d2h * steps / dev_s / 1e9,
-               "device_bytes": st["device_bytes_used"], "create_s": round(t_create, 2), "set_fields_s": round(t_set, 2),
+               "device_bytes": st["device_bytes_used"], "host_store_bytes": Z.oocz_host_store_bytes(cfg, world) if store == 0 else 0,
+               "resident_blocks": resident, "create_s": round(t_create, 2), "set_fields_s": round(t_set, 2),
                "evs": Z.oocz_get_events(ctx) if profile else []}
         if sample_planes is not None:    # planes of u for the compressed-vs-raw error
             res["u_planes"] = np.concatenate([Z.oocz_get_field_planes(ctx, Z.OOCZ_U, z0, np.empty((4, ny, nx), np.float32))
@@ -455,6 +477,15 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
                                     ("half_zfp_pf", (RATE,) * 3, PFr), ("half_raw_pf", (0, 0, 0), PFr)):
                 out[key] = run_c3(Z, key, nx, ny, raw_nz, rates, opt, arena, rank, world, nccl_id, local, sw, wu,
                                   dist, sample_planes=planes)
+            # rate 24 on the full C3 grid: a 231.9 GB compressed store, more than this host's
+            # RAM (and the arena); the rows of the first K z-blocks stay in HBM
+            # (resident_blocks, the largest K that fits), the rest stream as usual
+            try:
+                out["r24_resident"] = run_c3(Z, "c3_r24_resident", nx, ny, nz, (24,) * 3,
+                                             dict(P=pick_P(S, 64), serpentine=1, slots=2, resident_blocks="max"),
+                                             arena, rank, world, nccl_id, local, sw, wu, dist)
+            except Exception as e:       # a secondary number: report, do not lose the headline
+                out["r24_resident"] = {"error": f"{type(e).__name__}: {e}"[:300]}
             clk.active = False
     finally:
         Z.oocz_host_free(arena_p)
@@ -524,6 +555,12 @@ def paper_problem(Z, device, sweeps: int = 2, warmup: int = 1) -> dict:
             row["mean_pointwise_rel_error"] = err["mean_pointwise_significant"]
         out[key] = row
     return out
+
+
+def Z_ROWS(grid, rate, esz=4):
+    """bytes of one field's fixed-rate stream on grid (nx, ny, nz): 8 * rate per 4^3 block"""
+    nx, ny, nz = grid
+    return (nx // 4) * (ny // 4) * (nz // 4) * 8 * rate if rate else nx * ny * nz * esz
 
 
 def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
@@ -597,6 +634,22 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
                          "P": z["P"], "steps": (z["sweeps"] + z["warmup"]) * T, "max_rel_error": err}
         zr["paper_context"] = "1.20x (fp64, mode 4, V100-PCIe 3.0, PAPER.md:227)"
         rep["zfp_vs_raw"] = zr
+    if "r24_resident" in c3:
+        r = c3["r24_resident"]
+        if "error" in r:
+            rep["c3_rate24_resident_blocks"] = r
+        else:
+            store = 3 * Z_ROWS(r["grid"], 24)
+            rep["c3_rate24_resident_blocks"] = {
+                "value": round(r["cups"], 1), "e2e": round(r["e2e_cups"], 1), "rates": r["rates"], "P": r["P"],
+                "D": r["D"], "resident_blocks": r["resident_blocks"], "compressed_store_bytes": store,
+                "host_store_bytes": r["host_store_bytes"], "host_mem_bytes": info.get("mem_total_bytes"),
+                "h2d_bytes_per_step": int(r["h2d_per_sweep"]), "d2h_bytes_per_step": int(r["d2h_per_sweep"]),
+                "h2d_GBps": round(r["h2d_GBps"], 2), "d2h_GBps": round(r["d2h_GBps"], 2), "sweeps": r["sweeps"],
+                "what": "C3 at rate 24 on all three fields: the compressed store exceeds this host's RAM, so it "
+                        "runs only with the rows of the first resident_blocks z-blocks kept in HBM "
+                        "(cfg.resident_blocks, the largest split that fits) and the rest streamed; serpentine, "
+                        "m streamed, 2 slots"}
     if "hbm_error" in c3:
         rep["c3_hbm_resident"] = {"error": c3["hbm_error"]}
     if "hbm" in c3:
@@ -914,6 +967,7 @@ def gpu_arm(args):
         "c3_paper_faithful": rep.get("c3_paper_faithful"),
         "c3_paper_T12": rep.get("c3_paper_T12"),
         "c3_hbm_resident": rep.get("c3_hbm_resident"),
+        "c3_rate24_resident_blocks": rep.get("c3_rate24_resident_blocks"),
         "c3_arena": c3["arena"],
         "headline_run": rep["headline_run"],
         "c2": c2,
