@@ -22,12 +22,12 @@ def _fields(nx, ny, nz, seed, kind="dense"):
 
 
 def _run_gpu(u, up, m, T, P, rates, store, calls, slots=2, profile=0, serpentine=0, m_resident=0, slab_sets=0,
-             cone=0):
+             cone=0, resident_blocks=0):
     z = Z()
     nz, ny, nx = u.shape
     cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=list(rates), store=store,
                                 slots=slots, profile=profile, serpentine=serpentine, m_resident=m_resident,
-                                slab_sets=slab_sets, cone=cone)
+                                slab_sets=slab_sets, cone=cone, resident_blocks=resident_blocks)
     with z.Stepper(cfg) as s:
         s.set(u, up, m)
         for n in calls:
@@ -345,8 +345,8 @@ def test_extreme_rates(store):
 def test_random_configurations_bit_exact(seed):
     """96 seeded random configurations of everything the stepper accepts --
     grid shape, T, P, per-field rates (raw to 64), store location, slots,
-    slab sets, serpentine, m resident, split calls -- against the oracle.
-    (This test found the separate-encode-stream race.)"""
+    slab sets, serpentine, m resident, resident blocks (host store), split calls --
+    against the oracle.  (This test found the separate-encode-stream race.)"""
     rng = np.random.default_rng(seed)
     for case in range(96):
         T = int(rng.integers(1, 4))
@@ -360,6 +360,8 @@ def test_random_configurations_bit_exact(seed):
         opts = dict(slots=int(rng.integers(2, 5)), slab_sets=int(rng.choice([0, 1, 2, 3, 4])),
                     serpentine=int(rng.integers(0, 2)), m_resident=int(rng.integers(0, 2)))
         calls = [int(x) for x in rng.integers(1, 3 * T + 2, size=int(rng.integers(1, 4)))]
+        if store == 0:      # (its own generator: the draws above stay those of earlier rounds)
+            opts["resident_blocks"] = int(np.random.default_rng(1000 * seed + case).integers(0, D + 1))
         u, up, m = _fields(nx, ny, nz, 100 + case)
         gu, gup, _, _ = _run_gpu(u, up, m, T, P, rates, store, calls, **opts)
         ou, oup = _run_oracle(u, up, m, T, rates, calls)
