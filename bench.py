@@ -221,7 +221,7 @@ def lanes_summary(evs) -> dict:
 
 # DRAM bytes / algorithmic bytes per launch of each hot kernel, from the committed
 # ncu --set full capture of the C3-wide launch shape (tools/ncu_r02.sh)
-TRAFFIC_JSON = "r02e_stencil_c3_traffic.json"
+TRAFFIC_JSON = "r02g_stencil_c3_traffic.json"
 TRAFFIC_KEY = {"stencil": "traffic_over_algorithmic", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}
 ALU_PEAK = 148 * 4 * 0.5 * 1.965   # G warp-instructions/s: ALU pipe, rt 2 cycles per SMSP (B300_MICROARCH)
 
@@ -276,9 +276,9 @@ def codec_alu_roofline(table) -> dict | None:
     not by HBM: their fraction is the ALU pipe's share of its peak issue rate
     (148 SMs x 4 sub-partitions x one warp-instruction per 2 cycles at 1965 MHz),
     measured by ncu (sm__inst_executed_pipe_alu) on the committed capture of the
-    C3-wide launch shape (profiles/r02e_ncu_kernels.json)."""
+    C3-wide launch shape (profiles/r02g_ncu_kernels.json)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r02e_ncu_kernels.json")) as fh:
+        with open(os.path.join(ROOT, "profiles", "r02g_ncu_kernels.json")) as fh:
             kj = json.load(fh)["c3_slab"]
     except Exception:
         return None
@@ -293,7 +293,7 @@ def codec_alu_roofline(table) -> dict | None:
                      "unit": "G ALU-pipe warp-instructions/s", "frac": round(frac, 4),
                      "issue_active": round(k["issue_active_pct"] / 100, 4), "isolated_us": k["us"],
                      "in_step_avg_ms": table[stage]["avg_launch_ms"] if stage in table else None,
-                     "source": "profiles/r02e_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16, round-2 codec)"}
+                     "source": "profiles/r02g_ncu_kernels.json (ncu --set full, 4096^2 x 96-plane C3 slab, rate 16, round-2 codec)"}
     return out or None
 
 

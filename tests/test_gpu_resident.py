@@ -94,3 +94,32 @@ def test_resident_blocks_planes_and_checkpoint_across_the_boundary():
         h.step(4)
         assert np.array_equal(bits(h.get(z.OOCZ_U)), bits(t.get(z.OOCZ_U)))
         assert np.array_equal(bits(h.get(z.OOCZ_UPREV)), bits(t.get(z.OOCZ_UPREV)))
+
+
+@pytest.mark.parametrize("precision,cone", [(32, 1), (64, 0), (64, 1)])
+def test_resident_blocks_fp64_and_trapezoid_cone(precision, cone):
+    """The paper's own schedule (trapezoid cone, ascending, m streamed) and the fp64
+    path with resident blocks: bit-exact against the matching oracle."""
+    import oracle
+    z = Z()
+    nx, ny, nz, T, P = 24, 20, 96, 2, 24
+    rates = (32, 24, 24) if precision == 64 else (16, 12, 16)
+    u, up, m = _fields(nx, ny, nz, 17)
+    calls = [5, 4]
+    if precision == 64:
+        u, up, m = (a.astype(np.float64) for a in (u, up, m))
+        a, b, mm = oracle.roundtrip64(u, rates[0]), oracle.roundtrip64(up, rates[1]), oracle.roundtrip64(m, rates[2])
+        for n in calls:
+            a, b = oracle.advance64(a, b, mm, T, rates, n)
+        view = np.uint64
+    else:
+        a, b = _run_oracle(u, up, m, T, rates, calls)
+        view = np.uint32
+    for K in (1, 3):
+        cfg = _cfg(z, nx, ny, nz, T, P, rates, K, precision=precision, cone=cone)
+        with z.Stepper(cfg) as s:
+            s.set(u, up, m)
+            for n in calls:
+                s.step(n)
+            assert np.array_equal(s.get(z.OOCZ_U).view(view), a.view(view)), K
+            assert np.array_equal(s.get(z.OOCZ_UPREV).view(view), b.view(view)), K
