@@ -107,8 +107,9 @@ typedef struct {
                               fits HBM (a hybrid of the two placements; the paper streams
                               everything, PAPER.md:254 names orchestration future work).
                               0 (default) = all rows on the host; K = D equals
-                              OOCZ_STORE_DEVICE.  Needs world = 1 and store = HOST for
-                              K > 0; 0 <= K <= D, else OOCZ_EINVAL.  Results identical. */
+                              OOCZ_STORE_DEVICE.  Per rank with world > 1 (D = nz / world
+                              / P).  Needs store = HOST for K > 0; 0 <= K <= D, else
+                              OOCZ_EINVAL.  Results identical. */
 } oocz_config;
 
 typedef struct {

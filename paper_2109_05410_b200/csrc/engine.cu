@@ -399,8 +399,6 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
             cfg->nz / world / cfg->block_planes);
     if (cfg->resident_blocks > 0 && cfg->store != OOCZ_STORE_HOST)
         BAD(OOCZ_EINVAL, "resident_blocks (%d) needs store = OOCZ_STORE_HOST", cfg->resident_blocks);
-    if (cfg->resident_blocks > 0 && world > 1)
-        BAD(OOCZ_EINVAL, "resident_blocks (%d) needs world = 1", cfg->resident_blocks);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
     for (int k = 0; k < 5; k++)
@@ -911,7 +909,6 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     cudaStream_t s = ctx->s_comp;
     const double mmax = ctx->esz == 8 ? cfl_limit(ctx->cfg.c64) : cfl_limit(ctx->cfg.c);
     const uint8_t* src = static_cast<const uint8_t*>(src_v);
-    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     const cudaMemcpyKind in_kind = on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     const int rate = ctx->cfg.rate[field];
     const bool check_rt = field == OOCZ_M && rate > 0;
@@ -983,14 +980,14 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     if (!ctx->field_set[field]) return OOCZ_OK;
     if (field != OOCZ_M && ctx->halo) {
         std::string herr;
-        if (!halo_capture_store(ctx->halo, field, ctx->store[field], host, ctx->S, ctx->row_bytes[field], s, &herr) ||
+        if (!halo_capture_store(ctx->halo, field, rows_ptr(ctx, field, 0), rows_ptr(ctx, field, ctx->S - ctx->h), s, &herr) ||
             cudaStreamSynchronize(s) != cudaSuccess)
             return fail(ctx, OOCZ_ENCCL, "halo capture: %s", herr.c_str());
     }
     if (field == OOCZ_M && ctx->halo) {
         // m halos are read-only: exchange them once (compressed form, reading R20)
         std::string herr;
-        if (!halo_exchange_m(ctx->halo, ctx->store[OOCZ_M], host, ctx->S, ctx->row_bytes[OOCZ_M], s, &herr))
+        if (!halo_exchange_m(ctx->halo, rows_ptr(ctx, OOCZ_M, 0), rows_ptr(ctx, OOCZ_M, ctx->S - ctx->h), s, &herr))
             return fail(ctx, OOCZ_ENCCL, "m halo exchange: %s", herr.c_str());
     }
     return OOCZ_OK;
@@ -1104,7 +1101,6 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     if (bytes != ctx->store_bytes[field] || (!src && bytes))
         return fail(ctx, OOCZ_EINVAL, "bytes (%zu) != store size (%zu)", bytes, ctx->store_bytes[field]);
     CK(cudaSetDevice(ctx->device));
-    const bool host = ctx->cfg.store == OOCZ_STORE_HOST;
     cudaStream_t s = ctx->s_comp;
     ctx->field_set[field] = false;
     std::fill(ctx->rows_set[field].begin(), ctx->rows_set[field].end(), 0);
@@ -1133,8 +1129,8 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     if (ctx->halo) {                            // the neighbours' halos come from the store
         std::string herr;
         const bool ok = field == OOCZ_M
-            ? halo_exchange_m(ctx->halo, ctx->store[OOCZ_M], host, ctx->S, ctx->row_bytes[OOCZ_M], s, &herr)
-            : halo_capture_store(ctx->halo, field, ctx->store[field], host, ctx->S, ctx->row_bytes[field], s, &herr);
+            ? halo_exchange_m(ctx->halo, rows_ptr(ctx, OOCZ_M, 0), rows_ptr(ctx, OOCZ_M, ctx->S - ctx->h), s, &herr)
+            : halo_capture_store(ctx->halo, field, rows_ptr(ctx, field, 0), rows_ptr(ctx, field, ctx->S - ctx->h), s, &herr);
         if (!ok || cudaStreamSynchronize(s) != cudaSuccess)
             return fail(ctx, OOCZ_ENCCL, "halo refresh: %s", herr.c_str());
     }

@@ -147,14 +147,12 @@ cudaError_t uncode(const HaloComm* hc, int f, const uint8_t* src, int nx, int ny
     return field_decode(src, hc->esz, nx, ny, hc->h, hc->rate[f], dst, s);
 }
 
-bool fill_from_store(HaloComm* hc, int f, const uint8_t* store, bool host_store, int S, size_t row_bytes,
-                     cudaStream_t s, std::string* err)
+bool fill_from_store(HaloComm* hc, int f, const uint8_t* top, const uint8_t* bot, cudaStream_t s, std::string* err)
 {
-    const cudaMemcpyKind k = host_store ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    // pinned host or device rows: unified addressing tells the copy which
     const size_t n = hc->bytes[f];
-    return cuda_ok(cudaMemcpyAsync(hc->send_top[f], store, n, k, s), err, "halo fill") &&
-           cuda_ok(cudaMemcpyAsync(hc->send_bot[f], store + (size_t)((S - hc->h) / 4) * row_bytes, n, k, s), err,
-                   "halo fill");
+    return cuda_ok(cudaMemcpyAsync(hc->send_top[f], top, n, cudaMemcpyDefault, s), err, "halo fill") &&
+           cuda_ok(cudaMemcpyAsync(hc->send_bot[f], bot, n, cudaMemcpyDefault, s), err, "halo fill");
 }
 
 // One NCCL group: send `snd` to peer `to`, receive `rcv` from peer `from` (either
@@ -273,23 +271,22 @@ void halo_destroy(HaloComm* hc)
     delete hc;
 }
 
-bool halo_capture_store(HaloComm* hc, int field, const uint8_t* store, bool host_store, int S, size_t row_bytes,
-                        cudaStream_t s, std::string* err)
+bool halo_capture_store(HaloComm* hc, int field, const uint8_t* top, const uint8_t* bot, cudaStream_t s,
+                        std::string* err)
 {
     // the previous transfers must be done reading the send buffers
     return cuda_ok(cudaStreamWaitEvent(s, hc->ev_dn, 0), err, "wait") &&
            cuda_ok(cudaStreamWaitEvent(s, hc->ev_up, 0), err, "wait") &&
-           fill_from_store(hc, field, store, host_store, S, row_bytes, s, err) &&
+           fill_from_store(hc, field, top, bot, s, err) &&
            cuda_ok(cudaEventRecord(hc->ev_capt_top, s), err, "event") &&
            cuda_ok(cudaEventRecord(hc->ev_capt_bot, s), err, "event");
 }
 
-bool halo_exchange_m(HaloComm* hc, const uint8_t* store_m, bool host_store, int S, size_t row_bytes,
-                     cudaStream_t s, std::string* err)
+bool halo_exchange_m(HaloComm* hc, const uint8_t* top, const uint8_t* bot, cudaStream_t s, std::string* err)
 {
     if (!cuda_ok(cudaStreamWaitEvent(s, hc->ev_dn, 0), err, "wait") ||
         !cuda_ok(cudaStreamWaitEvent(s, hc->ev_up, 0), err, "wait") ||
-        !fill_from_store(hc, 2, store_m, host_store, S, row_bytes, s, err))
+        !fill_from_store(hc, 2, top, bot, s, err))
         return false;
     if (!cuda_ok(cudaStreamSynchronize(s), err, "sync")) return false;
     hc->m_pending = true;

@@ -47,11 +47,12 @@ HaloComm** halo_create_local_group(int world, int device, size_t plane_elems, in
 void halo_destroy(HaloComm* hc);
 
 // copy the store's first / last h planes of a read-write field into the send buffers
-bool halo_capture_store(HaloComm* hc, int field, const uint8_t* store, bool host_store, int S,
-                        size_t row_bytes, cudaStream_t s, std::string* err);
+// (top / bot: the stored rows of planes [0, h) and [S - h, S), each in host or
+// device memory -- a store split by resident_blocks has one of each)
+bool halo_capture_store(HaloComm* hc, int field, const uint8_t* top, const uint8_t* bot, cudaStream_t s,
+                        std::string* err);
 // m: fill send buffers from the store and mark the m halos stale (exchanged at the next sweep)
-bool halo_exchange_m(HaloComm* hc, const uint8_t* store_m, bool host_store, int S, size_t row_bytes,
-                     cudaStream_t s, std::string* err);
+bool halo_exchange_m(HaloComm* hc, const uint8_t* top, const uint8_t* bot, cudaStream_t s, std::string* err);
 // start of an oocz_step call (resets the watchdog's progress markers)
 void halo_step_begin(HaloComm* hc);
 bool halo_sweep_begin(HaloComm* hc, std::string* err);
