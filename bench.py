@@ -370,23 +370,13 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     t0 = time.perf_counter()
     resident = 0
     if opt.get("resident_blocks") == "max":
-        # the most z-blocks whose compressed rows fit in HBM (8 GiB left for the
-        # field generator); the rest must fit the pinned arena
+        # resident_blocks = -1: the library keeps as many z-blocks' compressed rows in
+        # HBM as the budget allows (8 GiB left for the field generator); the rest must
+        # fit the pinned arena
         budget = torch.cuda.mem_get_info(device)[0] - (8 << 30)
-        ctx = None
-        for k in range(S // opt["P"], -1, -1):
-            cfg = make_cfg(k, budget)
-            if Z.oocz_host_store_bytes(cfg, world) > arena[1]:
-                break
-            try:
-                ctx = Z.oocz_create_ex(cfg, rank, world, nccl_id, device, arena[0], arena[1])
-                resident = k
-                break
-            except Z.OoczError as e:
-                if e.status != Z.OOCZ_ECAPACITY:
-                    raise
-        if ctx is None:
-            raise RuntimeError(f"{label}: no resident_blocks split fits HBM and the {arena[1] / 1e9:.1f} GB arena")
+        ctx = Z.oocz_create_ex(make_cfg(-1, budget), rank, world, nccl_id, device, arena[0], arena[1])
+        cfg = Z.oocz_get_config(ctx)
+        resident = cfg.resident_blocks
     elif store == 0:
         ctx = Z.oocz_create_ex(cfg, rank, world, nccl_id, device, arena[0], arena[1])
     else:
@@ -648,7 +638,7 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
                 "h2d_GBps": round(r["h2d_GBps"], 2), "d2h_GBps": round(r["d2h_GBps"], 2), "sweeps": r["sweeps"],
                 "what": "C3 at rate 24 on all three fields: the compressed store exceeds this host's RAM, so it "
                         "runs only with the rows of the first resident_blocks z-blocks kept in HBM "
-                        "(cfg.resident_blocks, the largest split that fits) and the rest streamed; serpentine, "
+                        "(cfg.resident_blocks = -1: the largest split that fits) and the rest streamed; serpentine, "
                         "m streamed, 2 slots"}
     if "hbm_error" in c3:
         rep["c3_hbm_resident"] = {"error": c3["hbm_error"]}

@@ -107,9 +107,13 @@ typedef struct {
                               fits HBM (a hybrid of the two placements; the paper streams
                               everything, PAPER.md:254 names orchestration future work).
                               0 (default) = all rows on the host; K = D equals
-                              OOCZ_STORE_DEVICE.  Per rank with world > 1 (D = nz / world
-                              / P).  Needs store = HOST for K > 0; 0 <= K <= D, else
-                              OOCZ_EINVAL.  Results identical. */
+                              OOCZ_STORE_DEVICE.  -1 = auto: the largest K whose rows fit
+                              the device budget (device_bytes, or the free memory) beside
+                              everything else; oocz_get_config reports the K chosen, and
+                              oocz_host_store_bytes the K = 0 size (an upper bound).  Per
+                              rank with world > 1 (D = nz / world / P).  Needs store =
+                              HOST when nonzero; -1 <= K <= D, else OOCZ_EINVAL.  Results
+                              identical. */
 } oocz_config;
 
 typedef struct {

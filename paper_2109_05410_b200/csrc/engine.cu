@@ -394,10 +394,10 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
         BAD(OOCZ_EINVAL, "slab_sets (%d) outside {0 (= 2), 1, 2, 3, 4}", cfg->slab_sets);
     if (cfg->graphs != 0 && cfg->graphs != 1) BAD(OOCZ_EINVAL, "graphs (%d) must be 0 or 1", cfg->graphs);
     if (cfg->cone != 0 && cfg->cone != 1) BAD(OOCZ_EINVAL, "cone (%d) must be 0 or 1", cfg->cone);
-    if (cfg->resident_blocks < 0 || cfg->resident_blocks > cfg->nz / world / cfg->block_planes)
-        BAD(OOCZ_EINVAL, "resident_blocks (%d) outside [0, D = %d]", cfg->resident_blocks,
+    if (cfg->resident_blocks < -1 || cfg->resident_blocks > cfg->nz / world / cfg->block_planes)
+        BAD(OOCZ_EINVAL, "resident_blocks (%d) outside [-1 (auto), D = %d]", cfg->resident_blocks,
             cfg->nz / world / cfg->block_planes);
-    if (cfg->resident_blocks > 0 && cfg->store != OOCZ_STORE_HOST)
+    if (cfg->resident_blocks != 0 && cfg->store != OOCZ_STORE_HOST)
         BAD(OOCZ_EINVAL, "resident_blocks (%d) needs store = OOCZ_STORE_HOST", cfg->resident_blocks);
     if (cfg->precision != 32 && cfg->precision != 64)
         BAD(OOCZ_EINVAL, "precision (%d) must be 32 or 64", cfg->precision);
@@ -512,14 +512,21 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         need += (size_t)cfg->slots * (ctx->in_slot_bytes + ctx->out_slot_bytes);
     }
     for (int f = 0; f < 3; f++) ctx->store_bytes[f] = (size_t)(S / 4) * ctx->row_bytes[f];
-    ctx->zres = host ? std::min(cfg->resident_blocks * P, S) : S;
-    for (int f = 0; f < 3; f++) need += rows_off(ctx, f, ctx->zres);   // the rows kept in HBM
     if (world > 1) need += halo_device_bytes(ctx->plane_elems, h, cfg->rate, ctx->row_bytes);
     if (cfg->m_resident) need += (size_t)(S + 2 * h) * pb;
     {
         size_t fr = 0, tot = 0;
         CKC(cudaMemGetInfo(&fr, &tot));
         const size_t budget = cfg->device_bytes ? cfg->device_bytes : fr;
+        int K = cfg->resident_blocks;
+        if (host && K < 0) {    // auto: as many leading blocks as the budget leaves room for
+            size_t per = 0;
+            for (int f = 0; f < 3; f++) per += rows_off(ctx, f, P);
+            K = budget > need ? (int)std::min<size_t>((size_t)D, (budget - need) / std::max<size_t>(per, 1)) : 0;
+            ctx->cfg.resident_blocks = K;
+        }
+        ctx->zres = host ? std::min(std::max(K, 0) * P, S) : S;
+        for (int f = 0; f < 3; f++) need += rows_off(ctx, f, ctx->zres);   // the rows kept in HBM
         if (need > budget) {
             fprintf(stderr, "oocz_create: device memory %zu B needed > budget %zu B\n", need, budget);
             return cleanup_fail(OOCZ_ECAPACITY);
@@ -670,6 +677,7 @@ extern "C" size_t oocz_host_store_bytes(const oocz_config* cfg, int32_t world)
 {
     if (!cfg || world < 1 || cfg->nz % world) return 0;
     const int S = cfg->nz / world;
+    // (auto, -1: the bytes for K = 0, an upper bound)
     const int zres = cfg->resident_blocks > 0 ? std::min(cfg->resident_blocks * cfg->block_planes, S) : 0;
     size_t t = 0;
     for (int f = 0; f < 3; f++)

@@ -64,11 +64,13 @@ def test_cfl_limit_default_coefficients(z):
     (dict(cone=2, block_planes=32), 1, -1, "cone (2)"),
     (dict(resident_blocks=2, block_planes=32), 1, 0, ""),
     (dict(resident_blocks=4, block_planes=32), 1, 0, ""),            # K = D
-    (dict(resident_blocks=5, block_planes=32), 1, -1, "resident_blocks (5) outside [0, D = 4]"),
-    (dict(resident_blocks=-1, block_planes=32), 1, -1, "resident_blocks (-1)"),
+    (dict(resident_blocks=5, block_planes=32), 1, -1, "resident_blocks (5) outside [-1 (auto), D = 4]"),
+    (dict(resident_blocks=-1, block_planes=32), 1, 0, ""),           # auto
+    (dict(resident_blocks=-2, block_planes=32), 1, -1, "resident_blocks (-2)"),
+    (dict(resident_blocks=-1, block_planes=32, store=1), 1, -1, "needs store = OOCZ_STORE_HOST"),
     (dict(resident_blocks=1, block_planes=32, store=1), 1, -1, "needs store = OOCZ_STORE_HOST"),
     (dict(resident_blocks=1, block_planes=32), 2, 0, ""),             # per rank: D = 2
-    (dict(resident_blocks=3, block_planes=32), 2, -1, "resident_blocks (3) outside [0, D = 2]"),
+    (dict(resident_blocks=3, block_planes=32), 2, -1, "resident_blocks (3) outside [-1 (auto), D = 2]"),
 ])
 def test_validate(z, kw, world, code, msg):
     base = dict(nx=64, ny=64, nz=128, tb=4, block_planes=32)

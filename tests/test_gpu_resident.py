@@ -149,3 +149,26 @@ def test_resident_blocks_partitioned_group(world, K):
     ou, oup = _run_oracle(u, up, m, T, rates, [7])
     assert np.array_equal(bits(gu), bits(ou))
     assert np.array_equal(bits(gup), bits(oup))
+
+
+def test_resident_blocks_auto_takes_what_the_budget_leaves():
+    """resident_blocks = -1: the largest K whose rows fit the device budget beside
+    everything else (here a budget of the K = 0 need plus 2.5 blocks of rows:
+    K = 2), reported by oocz_get_config; results unchanged."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 32, 128, 2, 32, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz, 29)
+    per_block = sum(nx // 4 * ny // 4 * 8 * r for r in rates) * (P // 4)
+    with z.Stepper(_cfg(z, nx, ny, nz, T, P, rates, 0)) as s0:
+        need0 = s0.stats()["device_bytes_used"]
+    cfg = _cfg(z, nx, ny, nz, T, P, rates, -1, device_bytes=need0 + per_block * 5 // 2)
+    with z.Stepper(cfg) as s:
+        assert z.oocz_get_config(s.ctx).resident_blocks == 2
+        assert s.stats()["device_bytes_used"] == need0 + 2 * per_block
+        s.set(u, up, m)
+        s.step(5)
+        wa, wb = _run_oracle(u, up, m, T, rates, [5])
+        assert np.array_equal(bits(s.get(z.OOCZ_U)), bits(wa))
+        assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(wb))
+    with z.Stepper(_cfg(z, nx, ny, nz, T, P, rates, -1)) as s:     # the whole free HBM: every block
+        assert z.oocz_get_config(s.ctx).resident_blocks == nz // P
