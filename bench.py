@@ -997,6 +997,26 @@ def _oracle_timed(planes: int, seconds: float, max_sweeps: int = 16) -> dict:
     return {"n": n_tot, "s": s_tot, "sweeps": k}
 
 
+def _oracle_c1_c2() -> dict:
+    """C1 whole (64^3, PULSE(4) + LAYERED, P = 32, T = 2, rate 16, 10 steps: the
+    oracle's reduced schedule) and one sweep of a 512 x 512 x 32 box of C2
+    (DENSE(1) + LAYERED, T = 4, rate 16), timed in this process."""
+    import oracle
+    from paper_2109_05410_b200 import synth
+    n = 64
+    u, m = synth.pulse(n, n, n, sigma=4.0), synth.layered(n, n, n)
+    t0 = time.perf_counter()
+    oracle.advance(u, u, m, 2, (RATE,) * 3, 10)
+    c1 = time.perf_counter() - t0
+    u = synth.dense(512, 512, 512, seed=1, z0=0, z1=32)
+    m = synth.layered(512, 512, 512, z0=0, z1=32)
+    t0 = time.perf_counter()
+    oracle.advance(u, u, m, T, (RATE,) * 3, T)
+    c2 = time.perf_counter() - t0
+    return {"c1": {"value": round(n ** 3 * 10 / c1, 1), "seconds": round(c1, 3)},
+            "c2_sample": {"value": round(512 * 512 * 32 * T / c2, 1), "seconds": round(c2, 3)}}
+
+
 def _oracle_subprocess(threads: int, seconds: float, planes: int) -> dict:
     """The oracle in a fresh process with OMP_NUM_THREADS = threads (its stencil
     loops are OpenMP; the codec round trips are serial C)."""
@@ -1021,12 +1041,21 @@ def cpu_baseline(seconds: float = 16.0, info: dict | None = None):
     ncpu = os.cpu_count() or 1
     allc = _oracle_subprocess(ncpu, seconds / 2, planes)
     one = _oracle_subprocess(1, seconds / 2, planes)
+    small = {}
+    for th in (1, ncpu):        # C1 and C2 also at one thread
+        r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-c1c2"], capture_output=True,
+                           text=True, env=dict(os.environ, OMP_NUM_THREADS=str(th)), timeout=600)
+        if r.returncode == 0:
+            small[f"threads_{th}"] = json.loads(r.stdout.strip().splitlines()[-1])
     return {"value": round(allc["n"] / allc["s"], 1), "unit": "cell-updates/s", "cores": ncpu, "kind": "oracle",
             "sample": f"{allc['sweeps']} sweep(s) (T={T} steps + rate-{RATE} round trips each) of a "
                       f"4096x64x{planes} box of the C3 workload (DENSE(2) + LAYERED), {allc['s']:.1f} s, "
                       f"OMP_NUM_THREADS={ncpu}",
             "single_thread": {"value": round(one["n"] / one["s"], 1), "sweeps": one["sweeps"],
                               "seconds": round(one["s"], 1)},
+            "c1_c2": dict(small, what="C1 whole (64^3, PULSE(4) + LAYERED, T = 2, rate 16, 10 steps) and one "
+                                      "sweep of a 512x512x32 box of C2 (DENSE(1) + LAYERED, T = 4, rate 16), "
+                                      "cell-updates/s at 1 thread and at all logical CPUs"),
             "host": {k: info.get(k) for k in ("model", "sockets", "physical_cores", "logical_cpus", "hypervisor")}}
 
 
@@ -1076,8 +1105,14 @@ def main():
     ap.add_argument("--no-paper", action="store_true", help="skip the paper's own 1152^3 fp64 problem")
     ap.add_argument("--quick", action="store_true", help="the C3 headline and C2 rate 16 / raw only")
     ap.add_argument("--oracle-sample", type=float, default=None, help=argparse.SUPPRESS)
+    ap.add_argument("--oracle-c1c2", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--oracle-planes", type=int, default=64, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.oracle_c1c2:                         # cpu_baseline's child process (C1 / C2 sample)
+        import oracle
+        oracle.build()
+        print(json.dumps(_oracle_c1_c2()))
+        return
     if args.oracle_sample is not None:           # cpu_baseline's child process
         import oracle
         oracle.build()
