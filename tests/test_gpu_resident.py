@@ -172,3 +172,32 @@ def test_resident_blocks_auto_takes_what_the_budget_leaves():
         assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(wb))
     with z.Stepper(_cfg(z, nx, ny, nz, T, P, rates, -1)) as s:     # the whole free HBM: every block
         assert z.oocz_get_config(s.ctx).resident_blocks == nz // P
+
+
+def test_resident_blocks_with_a_caller_arena():
+    """oocz_create_ex with resident blocks: the arena must hold only the streamed
+    rows (oocz_host_store_bytes of the config); one byte less is OOCZ_ECAPACITY and
+    leaves nothing behind; the exact size steps bit-exactly."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 24, 96, 2, 24, (16, 12, 16)
+    u, up, m = _fields(nx, ny, nz, 31)
+    cfg = _cfg(z, nx, ny, nz, T, P, rates, 2)
+    need = z.oocz_host_store_bytes(cfg, 1)
+    assert need < z.oocz_host_store_bytes(_cfg(z, nx, ny, nz, T, P, rates, 0), 1)
+    arena = z.oocz_host_alloc(need)
+    try:
+        with pytest.raises(z.OoczError) as e:
+            z.oocz_create_ex(cfg, 0, 1, None, 0, arena, need - 1)
+        assert e.value.status == z.OOCZ_ECAPACITY
+        ctx = z.oocz_create_ex(cfg, 0, 1, None, 0, arena, need)
+        try:
+            for f, a in ((z.OOCZ_U, u), (z.OOCZ_UPREV, up), (z.OOCZ_M, m)):
+                z.oocz_set_field(ctx, f, a)
+            z.oocz_step(ctx, 6)
+            wa, wb = _run_oracle(u, up, m, T, rates, [6])
+            assert np.array_equal(bits(z.oocz_get_field(ctx, z.OOCZ_U, np.empty_like(u))), bits(wa))
+            assert np.array_equal(bits(z.oocz_get_field(ctx, z.OOCZ_UPREV, np.empty_like(u))), bits(wb))
+        finally:
+            z.oocz_destroy(ctx)
+    finally:
+        z.oocz_host_free(arena)
