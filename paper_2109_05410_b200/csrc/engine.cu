@@ -1521,10 +1521,45 @@ static oocz_status step_end(oocz_ctx* ctx, int64_t nsteps, cudaEvent_t base)
 // chosen by block index.
 static constexpr int kGraphSweeps = 16;
 
+// In core: with every field raw and the store in HBM, the store IS the grid (the
+// [z][y][x] planes of each field), so a sweep is T whole-grid steps in place, the
+// two time levels swapping roles by pointer -- what the block schedule computes
+// with raw round trips (the schedule equals the in-core leapfrog),
+// without its slab copies.  The paper-faithful schedule (cone = 1) keeps its blocks.
+static bool in_core_eligible(const oocz_ctx* c)
+{
+    return c->cfg.store == OOCZ_STORE_DEVICE && c->world == 1 && !c->halo && c->cfg.cone == 0 &&
+           c->cfg.rate[0] == 0 && c->cfg.rate[1] == 0 && c->cfg.rate[2] == 0;
+}
+
+static oocz_status in_core_sweep(oocz_ctx* ctx, int sweep, int ts)
+{
+    for (int s = 0; s < ts; s++) {
+        uint8_t* u = ctx->store[OOCZ_U];
+        uint8_t* up = ctx->store[OOCZ_UPREV];
+        const uint8_t* m = ctx->store[OOCZ_M];
+        const int S = ctx->S;
+        prof_begin(ctx, sweep, 0, OOCZ_ST_STENCIL, 1, ctx->s_comp, 4ull * (uint64_t)S * ctx->pb);
+        cudaError_t e = ctx->esz == 8
+            ? launch_stencil_step(reinterpret_cast<const double*>(u), reinterpret_cast<double*>(up),
+                                  reinterpret_cast<const double*>(m), ctx->nx, ctx->ny, S, ctx->cfg.c64, 0, S, 0, S,
+                                  ctx->s_comp)
+            : launch_stencil_step(reinterpret_cast<const float*>(u), reinterpret_cast<float*>(up),
+                                  reinterpret_cast<const float*>(m), ctx->nx, ctx->ny, S, ctx->cfg.c, 0, S, 0, S,
+                                  ctx->s_comp);
+        CK(e);
+        prof_end(ctx, ctx->s_comp);
+        // u+ was written over u-: it is the new u, the old u the new u-
+        std::swap(ctx->store[OOCZ_U], ctx->store[OOCZ_UPREV]);
+        std::swap(ctx->dstore[OOCZ_U], ctx->dstore[OOCZ_UPREV]);
+    }
+    return OOCZ_OK;
+}
+
 static bool graph_eligible(const oocz_ctx* c)
 {
     return c->cfg.graphs && c->cfg.store == OOCZ_STORE_DEVICE && c->world == 1 && !c->halo && !c->cfg.profile &&
-           !c->cfg.serpentine;
+           !c->cfg.serpentine && !in_core_eligible(c);
 }
 
 static oocz_status capture_chunk(oocz_ctx* ctx, int64_t nsteps, int* sweeps)
@@ -1657,6 +1692,12 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
         const bool last_sweep = done + ts >= nsteps;
         for (int r = 0; r < n; r++) {
             oocz_ctx* ctx = ctxs[r];
+            if (in_core_eligible(ctx)) {
+                oocz_status st = in_core_sweep(ctx, sweep, ts);
+                if (st != OOCZ_OK) return st;
+                ctx->stats.sweeps++;
+                continue;
+            }
             const int D = ctx->D;
             // serpentine (reading R22): odd sweeps of the call descend, and the block
             // at each turn is processed twice in a row without leaving the device

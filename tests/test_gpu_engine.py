@@ -540,3 +540,40 @@ def test_random_configurations_cone_bit_exact(seed=77):
         ou, oup = _run_oracle(u, up, m, T, rates, calls)
         assert np.array_equal(bits(gu), bits(ou)) and np.array_equal(bits(gup), bits(oup)), \
             (nx, ny, nz, T, P, rates, store, opts, calls)
+
+
+@pytest.mark.parametrize("precision", [32, 64])
+@pytest.mark.parametrize("calls", [[8], [5, 2], [1, 1, 3]])
+def test_raw_device_store_steps_in_core(precision, calls):
+    """Raw fields with the store in HBM step in core: one whole-grid stencil
+    launch per step, the time levels swapping by pointer, no copies -- bit-exact
+    against the oracle (and so against the block schedule), with the stencil's
+    16 B per cell-update as the only recorded traffic."""
+    import oracle as O
+    z = Z()
+    nx, ny, nz, T, P = 40, 24, 96, 3, 24
+    u, up, m = _fields(nx, ny, nz, 41)
+    if precision == 64:
+        u, up, m = (a.astype(np.float64) for a in (u, up, m))
+        a, b = u, up
+        for n in calls:
+            a, b = O.advance64(a, b, m, T, (0, 0, 0), n)
+        view = np.uint64
+    else:
+        a, b = _run_oracle(u, up, m, T, (0, 0, 0), calls)
+        view = np.uint32
+    cfg = z.oocz_default_config(nx, ny, nz, tb=T, block_planes=P, rate=[0, 0, 0], store=1, profile=1,
+                                precision=precision, m_resident=1)
+    with z.Stepper(cfg) as s:
+        s.set(u, up, m)
+        l0 = s.stats()["kernel_launches"]
+        for n in calls:
+            s.step(n)
+        st = s.stats()
+        assert st["kernel_launches"] - l0 == sum(calls)
+        assert st["h2d_bytes"] == st["d2h_bytes"] == 0
+        evs = z.oocz_get_events(s.ctx)
+        assert {e["stage"] for e in evs} == {2}                          # stencil
+        assert sum(e["bytes"] for e in evs) == 4 * nz * nx * ny * (8 if precision == 64 else 4) * calls[-1]
+        assert np.array_equal(s.get(z.OOCZ_U).view(view), a.view(view))
+        assert np.array_equal(s.get(z.OOCZ_UPREV).view(view), b.view(view))
