@@ -62,7 +62,10 @@ typedef struct {
     int32_t  block_planes; /* P: z-planes per block; multiple of 4, P >= 2h, P | nz/world     */
     int32_t  rate[3];      /* bits per value for {U, UPREV, M}: 0 = raw fp32, 1..64 = fixed-rate
                               ZFP ("the number of bits to preserve a value") */
-    int32_t  store;        /* OOCZ_STORE_HOST or OOCZ_STORE_DEVICE                             */
+    int32_t  store;        /* OOCZ_STORE_HOST or OOCZ_STORE_DEVICE.  DEVICE with every rate 0,
+                              world = 1 and cone = 0 is the in-core problem: oocz_step then
+                              steps the store in place (one whole-grid launch per step, no
+                              blocks); results identical                                   */
     int32_t  slots;        /* staging slots per direction (>= 2); host store only             */
     int32_t  profile;      /* 1: record per-stage CUDA events (oocz_get_events)               */
     uint64_t device_bytes; /* device memory budget; 0 = whatever cudaMemGetInfo reports free  */
@@ -174,8 +177,9 @@ oocz_status oocz_create(const oocz_config* cfg, int32_t rank, int32_t world,
  * e.g. the benchmark's schedules over one 155 GB store: pinning takes ~0.45 s
  * per GiB, the allocation, not the stepping, would dominate).
  *  - oocz_host_store_bytes: arena bytes a host-store context for (cfg, world)
- *    needs on each rank (the three field stores, each rounded up to 4 KiB);
- *    0 if nz is not divisible by world.
+ *    needs on each rank (the three field stores, each rounded up to 4 KiB; with
+ *    resident_blocks K > 0 only the streamed rows); 0 if nz is not divisible by
+ *    world.
  *  - oocz_host_alloc / oocz_host_free: pinned, portable host memory
  *    (cudaHostAlloc); OOCZ_ECUDA if the allocation fails (oocz_last_error(NULL)).
  *  - oocz_create_ex: oocz_create, but with store = OOCZ_STORE_HOST the stores
