@@ -560,9 +560,12 @@ def Z_ROWS(grid, rate, esz=4):
 def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
     h = c3["headline"]
     roof, table = roofline(h["evs"], peak_gbs, peak_src)
-    busier = max(h["h2d_per_sweep"], h["d2h_per_sweep"])
-    # the busier direction against its own rate with both directions busy
-    link_peak = link["concurrent_d2h_GBps" if h["d2h_per_sweep"] >= h["h2d_per_sweep"] else "concurrent_h2d_GBps"]
+    # the binding direction: the one whose bytes per sweep take longest at its own
+    # measured rate with both directions busy (the roof is that time per sweep)
+    t_dir = {d: h[f"{d}_per_sweep"] / (link[f"concurrent_{d}_GBps"] * 1e9) for d in ("h2d", "d2h")}
+    bound_dir = max(t_dir, key=t_dir.get)
+    busier = h[f"{bound_dir}_per_sweep"]
+    link_peak = link[f"concurrent_{bound_dir}_GBps"]
     rep = {
         "value": round(h["cups"], 1),
         "ms_per_step": round(h["device_s"] * 1e3 / args.steps, 3),
@@ -574,13 +577,15 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
                 "ms_per_step": round(h["host_s"] * 1e3 / args.steps, 3)},
         "roofline": roof,
         "roofline_host_link": {
-            "bound": "host-link", "achieved": round(busier * args.steps / h["device_s"] / 1e9, 2),
+            "bound": "host-link", "direction": bound_dir,
+            "achieved": round(busier * args.steps / h["device_s"] / 1e9, 2),
             "peak": link_peak, "unit": "GB/s",
             "frac": round(busier * args.steps / h["device_s"] / 1e9 / link_peak, 4),
             "h2d_GBps": round(h["h2d_GBps"], 2), "d2h_GBps": round(h["d2h_GBps"], 2),
             "peak_source": "measured in this run: pinned H2D and D2H at once on two streams (host_link_probe)",
-            "what": "the out-of-core roofline (SURVEY 8(d)): bytes the busier direction must move per sweep / "
-                    "time, over that direction's measured bandwidth with both directions busy",
+            "what": "the out-of-core roofline (SURVEY 8(d)): of H2D and D2H, the direction whose bytes per "
+                    "sweep take longest at its measured rate with both directions busy binds; achieved = its "
+                    "bytes per sweep / sweep time, peak = its measured rate",
             "host_link_probe": link},
         "kernels_in_step": table,
         "codec_alu_roofline": codec_alu_roofline(table),
@@ -835,9 +840,8 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
            "steps": steps, "warmup": warmup,
            "value_hbm_resident": round(v["cups"], 1),
            "e2e_out_of_core": round(e["cups"], 1),
-           "e2e_host_link_frac": round(max(e["h2d_per_sweep"], e["d2h_per_sweep"]) / (e["s"] / steps) / 1e9 /
-                                       link["concurrent_d2h_GBps" if e["d2h_per_sweep"] >= e["h2d_per_sweep"]
-                                            else "concurrent_h2d_GBps"], 4),
+           "e2e_host_link_frac": round(max(e[f"{d}_per_sweep"] / (link[f"concurrent_{d}_GBps"] * 1e9)
+                                           for d in ("h2d", "d2h")) / (e["s"] / steps), 4),
            "e2e_h2d_bytes_per_step": int(e["h2d_per_sweep"]), "e2e_d2h_bytes_per_step": int(e["d2h_per_sweep"]),
            "raw": {"value_hbm_resident": round(out["raw_dev"]["cups"], 1), "e2e": round(out["raw_host"]["cups"], 1)},
            "speedup_zfp_vs_raw": {"hbm_resident": round(v["cups"] / out["raw_dev"]["cups"], 3),
