@@ -673,12 +673,12 @@ def make_fields_c2():
 
 
 def run_mode_c2(Z, store, rates, fields, device, steps, warmup, profile, m_resident=0, tb=T, precision=32,
-                serpentine=0, slots=2, slab_sets=0, cone=0):
+                serpentine=0, slots=2, slab_sets=0, cone=0, block_planes=P, graphs=0):
     """Returns (device seconds for `steps` sweeps, stats, events, launches, ctx)."""
     import torch
-    cfg = Z.oocz_default_config(NX, NY, NZ, tb=tb, block_planes=P, rate=list(rates), store=store,
+    cfg = Z.oocz_default_config(NX, NY, NZ, tb=tb, block_planes=block_planes, rate=list(rates), store=store,
                                 m_resident=m_resident, precision=precision, serpentine=serpentine,
-                                slots=slots, profile=profile, slab_sets=slab_sets, cone=cone)
+                                slots=slots, profile=profile, slab_sets=slab_sets, cone=cone, graphs=graphs)
     ctx = Z.oocz_create(cfg, 0, 1, None, device)
     try:
         for f, a in zip((Z.OOCZ_U, Z.OOCZ_UPREV, Z.OOCZ_M), fields):

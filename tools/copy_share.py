@@ -9,8 +9,8 @@ import bench  # noqa: E402
 from paper_2109_05410_b200 import oocz as Z  # noqa: E402
 
 torch.cuda.set_device(0)
-fields = bench.make_fields(0, bench.NZ)
-dev_s, st, evs, launches, ctx = bench.run_mode(Z, 1, (16,) * 3, fields, 0, 1, None, 0, 10, 3, None, 1, m_resident=1)
+fields = bench.make_fields_c2()
+dev_s, st, evs, launches, ctx = bench.run_mode_c2(Z, 1, (16,) * 3, fields, 0, 10, 3, 1, m_resident=1)
 Z.oocz_destroy(ctx)
 lanes = {0: "h2d", 1: "compute", 2: "d2h", 3: "comm", 4: "decode", 5: "encode"}
 agg = collections.Counter()

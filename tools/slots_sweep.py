@@ -7,11 +7,11 @@ import bench  # noqa: E402
 from paper_2109_05410_b200 import oocz as Z  # noqa: E402
 
 torch.cuda.set_device(0)
-fields = bench.make_fields(0, bench.NZ)
+fields = bench.make_fields_c2()
 cells = bench.NX * bench.NY * bench.NZ * bench.T * 10
 for serp, mres in ((0, 0), (1, 0), (0, 1), (1, 1)):
     for slots in (2, 3, 4):
-        dev_s, st, evs, launches, ctx = bench.run_mode(Z, 0, (16, 16, 16), fields, 0, 1, None, 0, 10, 3, None, 0,
+        dev_s, st, evs, launches, ctx = bench.run_mode_c2(Z, 0, (16, 16, 16), fields, 0, 10, 3, 0,
                                                       m_resident=mres, serpentine=serp, slots=slots)
         Z.oocz_destroy(ctx)
         sw = st["sweeps"]
