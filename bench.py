@@ -791,7 +791,7 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
     steps, warmup = args.c2_steps, 3
     cells = NX * NY * NZ * T * steps
     OD = dict(m_resident=1)
-    OH = dict(serpentine=1, m_resident=1, slots=3)
+    OH = dict(serpentine=1, m_resident=1, slots=4)   # (4 slots: 67 vs 64 G, profiles/r02_c2_slots.txt)
     PF = dict(serpentine=0, m_resident=0, cone=1)
     modes = [("zfp_dev", 1, (RATE,) * 3, OD), ("zfp_host", 0, (RATE,) * 3, OH),
              ("raw_dev", 1, (0, 0, 0), OD), ("raw_host", 0, (0, 0, 0), OH)]
@@ -849,7 +849,7 @@ def c2_arm(args, Z, device, peak_gbs, peak_src, link, clk):
            "max_rel_error": err,
            "in_core": in_core_c2(Z, fields, steps, warmup, out["raw_dev"]["u"], peak_gbs),
            "roofline_in_step": roof, "kernels_in_step": table, "lanes": lanes_summary(v["evs"]),
-           "schedule": "HBM-resident: m_resident=1; out of core: serpentine=1, m_resident=1, slots=3"}
+           "schedule": "HBM-resident: m_resident=1; out of core: serpentine=1, m_resident=1, slots=4"}
     if "pf_raw_host" in out:
         rep["paper_faithful"] = {"value_hbm_resident": round(out["pf_zfp_dev"]["cups"], 1),
                                  "e2e_out_of_core": round(out["pf_zfp_host"]["cups"], 1),
