@@ -194,6 +194,7 @@ struct oocz_ctx {
     long long seq = 0;                      // global block sequence number
     std::vector<int> last_slot;             // staging slot of each block's latest encode (host store)
     std::vector<long long> last_seq;        // ... and its block sequence number (-1: not in a slot)
+    std::vector<uint8_t> kept;              // its latest rows are only in that slot (D2H skipped, R22)
     // halo exchange (world > 1)
     HaloComm* halo = nullptr;
     // profiling
@@ -639,6 +640,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
     CKC(mk(ctx->ev_encoded, D));
     ctx->last_slot.assign(D, 0);
     ctx->last_seq.assign(D, -1);
+    ctx->kept.assign(D, 0);
     CKC(cudaEventCreate(&ctx->ev_t0));
     CKC(cudaEventCreate(&ctx->ev_t1));
     CKC(cudaEventCreateWithFlags(&ctx->ev_join_h2d, cudaEventDisableTiming));
@@ -1310,7 +1312,14 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     }
     (void)rd_planes;
     if (any_h2d) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
-    if (host && turn) CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[i]], sd));   // the kept slot is read
+    // a kept block's slot (its rows were never written back) is free once the
+    // decodes that read it are done: the encode that reuses it waits on this
+    for (int f = 0; f < nf; f++)
+        for (int k = 0; k < nparts[f]; k++) {
+            const int o = owner_of(part[f][k]);
+            if (!part[f][k].h2d && ctx->kept[o] && !rows_on_device(ctx, part[f][k].z0))
+                CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[o]], sd));
+        }
     // keep the time-t shared region for the next block (reading R14):
     // ascending C_i = slab [P, P+2h), descending C_{i-1} = slab [0, 2h)
     if (has_next) {
@@ -1392,6 +1401,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         CK(cudaEventRecord(ctx->ev_slab_free[set], se));
         ctx->last_slot[i] = slot;
         ctx->last_seq[i] = ctx->seq;
+        ctx->kept[i] = keep;
         CK(cudaEventRecord(ctx->ev_encoded[i], se));
         if (keep) {
             // rows stay in the slot for the turnaround; its decode frees the slot
@@ -1706,7 +1716,11 @@ static oocz_status step_group(oocz_ctx* const* ctxs, int n, int64_t nsteps)
             for (int k = 0; k < D; k++) {
                 const int i = dir > 0 ? k : D - 1 - k;
                 const bool turn = serp && sweep > 0 && k == 0;
-                const bool keep = serp && !last_sweep && k == D - 1;
+                // the last nkeep blocks before a turnaround keep their rows in their slots
+                // (no D2H): the first nkeep blocks after it read them from there before
+                // re-encoding them, which needs slots >= 2 nkeep - 1 (R22)
+                const int nkeep = std::min(D, ((int)ctx->out_slot.size() + 1) / 2);
+                const bool keep = serp && !last_sweep && k >= D - nkeep;
                 oocz_status st = enqueue_block(ctx, sweep, i, ts, dir, turn, keep);
                 if (st != OOCZ_OK) return st;
             }

@@ -214,9 +214,12 @@ def test_m_resident_partitioned_group(world):
 def _serpentine_bytes(D, P, h, T, calls, slots, nf, row):
     """Host-link bytes of serpentine sweeps, modelled from the rule (DESIGN.md
     R22): a read-unit part is decoded from a staging slot when the block that
-    encoded it is at most `slots` blocks back in the sequence; the kept block
-    at each turn skips its D2H; m rows (nf == 3) always cross, except at a turn."""
+    encoded it is at most `slots` blocks back in the sequence; the last
+    nkeep = min(D, (slots + 1) // 2) blocks before each turn skip their D2H (their
+    rows are read from their slots after the turn); m rows (nf == 3) always
+    cross, except at a turn."""
     S = D * P
+    nkeep = min(D, (slots + 1) // 2)
     h2d = d2h = 0
     seq, last = 0, [-1] * D
     for n in calls:
@@ -226,7 +229,7 @@ def _serpentine_bytes(D, P, h, T, calls, slots, nf, row):
             for kk in range(D):
                 i = kk if asc else D - 1 - kk
                 turn = s_ > 0 and kk == 0
-                keep = s_ < k - 1 and kk == D - 1
+                keep = s_ < k - 1 and kk >= D - nkeep
                 if asc:
                     rd0, rd1 = (0 if i == 0 else i * P + h), min((i + 1) * P + h, S)
                     nb = min(i + 1, D - 1)
@@ -254,8 +257,8 @@ def _serpentine_bytes(D, P, h, T, calls, slots, nf, row):
 
 @pytest.mark.parametrize("slab_sets", [1, 2, 3, 4])
 @pytest.mark.parametrize("m_resident", [0, 1])
-@pytest.mark.parametrize("slots", [2, 3])
-@pytest.mark.parametrize("D,calls", [(4, [12]), (3, [5, 7]), (1, [9]), (2, [4, 4, 1])])
+@pytest.mark.parametrize("slots", [2, 3, 5])
+@pytest.mark.parametrize("D,calls", [(4, [12]), (3, [5, 7]), (1, [9]), (2, [4, 4, 1]), (6, [14, 3])])
 def test_serpentine_bit_exact_and_bytes(D, calls, slots, m_resident, slab_sets):
     """Serpentine sweeps (R22): same bits as the oracle, and exactly the
     host-link bytes of the schedule's model: the block at each turn never crosses
