@@ -444,7 +444,7 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     t_arena = time.perf_counter() - t0
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
-        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=3)
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=4)
         PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
         out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id, local,
@@ -952,7 +952,7 @@ def gpu_arm(args):
                                f"three fields (154.6 GB pinned host store), T={T}, P={h['P']} ({h['D']} z-blocks"
                                f"{' per GPU' if world > 1 else ''})",
                    "grid": [C3N, C3N, C3Z], "tb": T, "block_planes": h["P"], "rate": RATE,
-                   "schedule": "serpentine sweeps + m decoded once into HBM + 3 staging slots (the library's fastest "
+                   "schedule": "serpentine sweeps + m decoded once into HBM + 4 staging slots (the library's fastest "
                                "schedule of the same computation, bit-identical to the paper's; the paper's own: "
                                "c3_paper_faithful)",
                    "step": "one sweep = T leapfrog steps over the whole grid",

@@ -315,7 +315,7 @@ def c2_state():
 @pytest.mark.parametrize("store,opts", [
     (1, dict(m_resident=1)),                                  # bench value path
     (0, dict(serpentine=1, m_resident=1, slots=4)),           # bench e2e path (C2)
-    (0, dict(serpentine=1, m_resident=1, slots=3)),           # the C3 headline schedule
+    (0, dict(serpentine=1, m_resident=1, slots=3)),           # 3 slots: 2 kept blocks per turn
     (0, dict()),                                              # the paper-faithful schedule
 ])
 def test_c2_full_size_bench_configs_bit_exact(c2_state, store, opts):
