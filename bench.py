@@ -384,7 +384,7 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
     t_create = time.perf_counter() - t0
     try:
         # a compressed store in HBM leaves little room for the generator's fp64 chunks
-        t_set = set_fields_gpu(Z, ctx, nx, ny, nz, rank * S, S, C3SEED, chunk=16 if store == 0 else 4)
+        t_set = set_fields_gpu(Z, ctx, nx, ny, nz, rank * S, S, C3SEED, chunk=opt.get("gen_chunk", 16 if store == 0 else 4))
         Z.oocz_step(ctx, warmup * tb)
         if dist:
             dist.barrier()
@@ -444,11 +444,24 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     t_arena = time.perf_counter() - t0
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
-        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=4)
+        # 5 staging slots: 3 kept blocks per serpentine turn; they fill HBM
+        # to ~186 GB, so the field generator works in 4-plane chunks, and a box with less
+        # free HBM falls back to 4 slots (2 kept blocks)
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=5, gen_chunk=4)
         PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
-        out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id, local,
-                                 args.steps, args.warmup, dist, profile=1)
+        try:
+            out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id,
+                                     local, args.steps, args.warmup, dist, profile=1)
+        except Exception as e:
+            if world > 1:
+                raise
+            log(f"c3_zfp_host with 5 slots failed ({type(e).__name__}: {str(e)[:120]}); 4 slots")
+            torch.cuda.empty_cache()
+            HS = dict(HS, slots=4, gen_chunk=16)
+            out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id,
+                                     local, args.steps, args.warmup, dist, profile=1)
+            out["headline"]["fallback"] = f"5 slots: {type(e).__name__}: {str(e)[:160]}"
         clk.active = False
         if world == 1 and not args.quick:
             sw, wu = args.sec_steps, 1
@@ -461,7 +474,7 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
                                 arena, rank, world, nccl_id, local, sw, wu, dist)
             # ZFP vs raw on the largest C3-shaped grid whose raw store fits this host
             planes = [0, raw_nz // 4, raw_nz // 2, 3 * raw_nz // 4 - 4, raw_nz - 4]
-            HSr = dict(HS, P=pick_P(raw_nz, 64))
+            HSr = dict(HS, P=pick_P(raw_nz, 64), slots=4, gen_chunk=16)   # (raw slots are twice the size)
             PFr = dict(PF, P=pick_P(raw_nz, 96))
             for key, rates, opt in (("half_zfp_hs", (RATE,) * 3, HSr), ("half_raw_hs", (0, 0, 0), HSr),
                                     ("half_zfp_pf", (RATE,) * 3, PFr), ("half_raw_pf", (0, 0, 0), PFr)):
@@ -952,7 +965,8 @@ def gpu_arm(args):
                                f"three fields (154.6 GB pinned host store), T={T}, P={h['P']} ({h['D']} z-blocks"
                                f"{' per GPU' if world > 1 else ''})",
                    "grid": [C3N, C3N, C3Z], "tb": T, "block_planes": h["P"], "rate": RATE,
-                   "schedule": "serpentine sweeps + m decoded once into HBM + 4 staging slots (the library's fastest "
+                   "schedule": f"serpentine sweeps + m decoded once into HBM + {h['schedule'].get('slots')} staging "
+                               "slots, kept blocks at the turns (the library's fastest "
                                "schedule of the same computation, bit-identical to the paper's; the paper's own: "
                                "c3_paper_faithful)",
                    "step": "one sweep = T leapfrog steps over the whole grid",

@@ -21,7 +21,7 @@ try:
     for slots in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3,4,5,6").split(",")]:
         try:
             r = bench.run_c3(Z, f"slots{slots}", nx, ny, nz, (16,) * 3,
-                             dict(P=64, serpentine=1, m_resident=1, slots=slots), (arena_p, need), 0, 1, None, 0,
+                             dict(P=64, serpentine=1, m_resident=1, slots=slots, gen_chunk=4 if slots >= 5 else 16), (arena_p, need), 0, 1, None, 0,
                              4, 2, None)
             print(json.dumps({"slots": slots, "G": round(r["cups"] / 1e9, 2), "h2d_GB": round(r["h2d_per_sweep"] / 1e9, 2),
                               "d2h_GB": round(r["d2h_per_sweep"] / 1e9, 2), "h2d_GBps": round(r["h2d_GBps"], 2),
