@@ -444,10 +444,10 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     t_arena = time.perf_counter() - t0
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
-        # 5 staging slots: 3 kept blocks per serpentine turn; they fill HBM
-        # to ~186 GB, so the field generator works in 4-plane chunks, and a box with less
-        # free HBM falls back to 4 slots (2 kept blocks)
-        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=5, gen_chunk=4)
+        # 7 output staging slots: 4 kept blocks per serpentine turn; they fill
+        # HBM to ~184 GB, so the field generator works in 4-plane chunks, and a box with
+        # less free HBM falls back to 4 slots (2 kept blocks)
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=7, gen_chunk=4)
         PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
         try:
@@ -456,12 +456,12 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
         except Exception as e:
             if world > 1:
                 raise
-            log(f"c3_zfp_host with 5 slots failed ({type(e).__name__}: {str(e)[:120]}); 4 slots")
+            log(f"c3_zfp_host with 7 slots failed ({type(e).__name__}: {str(e)[:120]}); 4 slots")
             torch.cuda.empty_cache()
             HS = dict(HS, slots=4, gen_chunk=16)
             out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id,
                                      local, args.steps, args.warmup, dist, profile=1)
-            out["headline"]["fallback"] = f"5 slots: {type(e).__name__}: {str(e)[:160]}"
+            out["headline"]["fallback"] = f"7 slots: {type(e).__name__}: {str(e)[:160]}"
         clk.active = False
         if world == 1 and not args.quick:
             sw, wu = args.sec_steps, 1

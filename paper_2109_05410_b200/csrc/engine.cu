@@ -141,6 +141,11 @@ cudaError_t launch_scan_field(const float* in, size_t n, unsigned int* flags, cu
 using namespace oocz;
 
 // ------------------------------------------------------------------ context
+#ifndef OOCZ_IN_SLOTS
+#define OOCZ_IN_SLOTS 3
+#endif
+static constexpr int kInSlots = OOCZ_IN_SLOTS;   // input staging slots at most (host store)
+
 struct Geom {
     int rd0, rd1;      // read unit, rank-local planes
     int own0, own1;    // write unit
@@ -510,7 +515,10 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             ctx->out_off[f] = ctx->out_slot_bytes;
             ctx->out_slot_bytes += (size_t)(P / 4) * ctx->row_bytes[f];
         }
-        need += (size_t)cfg->slots * (ctx->in_slot_bytes + ctx->out_slot_bytes);
+        // staging: `slots` output slots (their depth is what keeps recently encoded
+        // rows on the device, R22) and at most kInSlots input slots (H2D runs that far
+        // ahead of the decode)
+        need += (size_t)std::min(cfg->slots, kInSlots) * ctx->in_slot_bytes + (size_t)cfg->slots * ctx->out_slot_bytes;
     }
     for (int f = 0; f < 3; f++) ctx->store_bytes[f] = (size_t)(S / 4) * ctx->row_bytes[f];
     if (world > 1) need += halo_device_bytes(ctx->plane_elems, h, cfg->rate, ctx->row_bytes);
@@ -551,9 +559,11 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         for (int s = 0; s < cfg->slots; s++) {
             uint8_t* a = nullptr;
             uint8_t* b = nullptr;
-            CKC(cudaMalloc(&a, ctx->in_slot_bytes));
+            if (s < kInSlots) {
+                CKC(cudaMalloc(&a, ctx->in_slot_bytes));
+                ctx->in_slot.push_back(a);
+            }
             CKC(cudaMalloc(&b, ctx->out_slot_bytes));
-            ctx->in_slot.push_back(a);
             ctx->out_slot.push_back(b);
         }
         if (ctx->zres > 0)
@@ -632,8 +642,8 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         }
         return cudaSuccess;
     };
-    CKC(mk(ctx->ev_in_ready, nslots));
-    CKC(mk(ctx->ev_in_free, nslots));
+    CKC(mk(ctx->ev_in_ready, std::min(nslots, kInSlots)));
+    CKC(mk(ctx->ev_in_free, std::min(nslots, kInSlots)));
     CKC(mk(ctx->ev_out_ready, nslots));
     CKC(mk(ctx->ev_out_free, nslots));
     CKC(mk(ctx->ev_written, D));
@@ -1179,8 +1189,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     // this block's rows stream over the host link (not kept in HBM: device store or
     // resident_blocks)
     const bool host = !rows_on_device(ctx, g.own0);
-    const int nslots = (int)ctx->ev_in_ready.size();
-    const int slot = (int)(ctx->seq % nslots);
+    const int islot = (int)(ctx->seq % (long long)ctx->ev_in_ready.size());    // input staging slot
+    const int slot = (int)(ctx->seq % (long long)ctx->ev_out_ready.size());    // output staging slot
     // slab set: blocks rotate through nsets; with serpentine sweeps by block
     // index, so a turnaround block finds its own slab (and its decoded m) again;
     // in a graph capture by block
@@ -1216,7 +1226,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
                 q.src = ctx->out_slot[ctx->last_slot[owner]] + ctx->out_off[f] +
                         (size_t)((z0 - owner * P) / 4) * ctx->row_bytes[f];
             } else {
-                q.src = ctx->in_slot[slot] + ctx->in_off[f] + (size_t)((z0 - rd0) / 4) * ctx->row_bytes[f];
+                q.src = ctx->in_slot[islot] + ctx->in_off[f] + (size_t)((z0 - rd0) / 4) * ctx->row_bytes[f];
                 q.h2d = true;
             }
             part[f][nparts[f]++] = q;
@@ -1233,7 +1243,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     auto owner_of = [&](const Part& q) { return q.z0 >= g.own0 && q.z0 < g.own1 ? i : nb; };
     if (any_h2d) {
         cudaStream_t sh = ctx->s_h2d;
-        CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[slot], 0));
+        CK(cudaStreamWaitEvent(sh, ctx->ev_in_free[islot], 0));
         for (int f = 0; f < nf; f++)
             for (int k = 0; k < nparts[f]; k++)
                 if (part[f][k].h2d) CK(cudaStreamWaitEvent(sh, ctx->ev_written[owner_of(part[f][k])], 0));
@@ -1251,8 +1261,8 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
             }
         prof_end(ctx, sh);
         ctx->stats.h2d_bytes += bytes;
-        CK(cudaEventRecord(ctx->ev_in_ready[slot], sh));
-        CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[slot], 0));
+        CK(cudaEventRecord(ctx->ev_in_ready[islot], sh));
+        CK(cudaStreamWaitEvent(sd, ctx->ev_in_ready[islot], 0));
     }
     // rows read from the device: the encodes that wrote them must be done
     for (int f = 0; f < nf; f++)
@@ -1311,7 +1321,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         prof_end(ctx, sd);
     }
     (void)rd_planes;
-    if (any_h2d) CK(cudaEventRecord(ctx->ev_in_free[slot], sd));
+    if (any_h2d) CK(cudaEventRecord(ctx->ev_in_free[islot], sd));
     // a kept block's slot (its rows were never written back) is free once the
     // decodes that read it are done: the encode that reuses it waits on this
     for (int f = 0; f < nf; f++)
