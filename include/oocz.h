@@ -66,7 +66,11 @@ typedef struct {
                               world = 1 and cone = 0 is the in-core problem: oocz_step then
                               steps the store in place (one whole-grid launch per step, no
                               blocks); results identical                                   */
-    int32_t  slots;        /* staging slots per direction (>= 2); host store only             */
+    int32_t  slots;        /* staging slots (>= 2), host store only: `slots` output slots for
+                              encoded rows (with serpentine, the last (slots + 1) / 2 blocks
+                              before a turnaround keep their rows there instead of writing
+                              them back) and min(slots, 3) input slots for the H2D of read
+                              units.  Results identical.                                     */
     int32_t  profile;      /* 1: record per-stage CUDA events (oocz_get_events)               */
     uint64_t device_bytes; /* device memory budget; 0 = whatever cudaMemGetInfo reports free  */
     int32_t  m_resident;   /* 1: decode the read-only m ONCE into HBM (nx*ny*(nz/world + 8T)
