@@ -361,7 +361,8 @@ def run_c3(Z, label, nx, ny, nz, rates, opt, arena, rank, world, nccl_id, device
         return Z.oocz_default_config(nx, ny, nz, tb=tb, block_planes=opt["P"], rate=list(rates), store=store,
                                      m_resident=opt.get("m_resident", 0), serpentine=opt.get("serpentine", 0),
                                      slots=opt.get("slots", 2), slab_sets=opt.get("slab_sets", 0), profile=profile,
-                                     cone=opt.get("cone", 0), resident_blocks=k, device_bytes=budget)
+                                     cone=opt.get("cone", 0), resident_blocks=k, device_bytes=budget,
+                                     m_hbm=opt.get("m_hbm", 0))
     cfg = make_cfg()
     if callable(nccl_id):
         nccl_id = nccl_id()
@@ -444,24 +445,28 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     t_arena = time.perf_counter() - t0
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
-        # 7 output staging slots: 4 kept blocks per serpentine turn; they fill
-        # HBM to ~184 GB, so the field generator works in 4-plane chunks, and a box with
-        # less free HBM falls back to 4 slots (2 kept blocks)
-        HS = dict(P=pick_P(S, 64), serpentine=1, m_resident=1, slots=7, gen_chunk=4)
+        # m's compressed stream in HBM (m_hbm, decoded per block) instead of a decoded m, and
+        # the HBM that frees as 16 output staging slots: 8 kept blocks per serpentine turn
+        # (DESIGN.md §7).  They fill HBM to ~184 GB, so the field generator works in 4-plane
+        # chunks; a box with less free HBM falls back to 12 slots, then to 4 with m resident
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_hbm=1, slots=16, gen_chunk=4)
         PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
-        try:
-            out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id,
-                                     local, args.steps, args.warmup, dist, profile=1)
-        except Exception as e:
-            if world > 1:
-                raise
-            log(f"c3_zfp_host with 7 slots failed ({type(e).__name__}: {str(e)[:120]}); 4 slots")
-            torch.cuda.empty_cache()
-            HS = dict(HS, slots=4, gen_chunk=16)
-            out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, HS, arena, rank, world, nccl_id,
-                                     local, args.steps, args.warmup, dist, profile=1)
-            out["headline"]["fallback"] = f"7 slots: {type(e).__name__}: {str(e)[:160]}"
+        fallbacks = []
+        for hs in (HS, dict(HS, slots=12), dict(P=HS["P"], serpentine=1, m_resident=1, slots=4)):
+            try:
+                out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, hs, arena, rank, world,
+                                         nccl_id, local, args.steps, args.warmup, dist, profile=1)
+                HS = hs
+                break
+            except Exception as e:
+                if world > 1 or hs.get("slots") == 4:
+                    raise
+                log(f"c3_zfp_host {hs} failed ({type(e).__name__}: {str(e)[:120]}); next schedule")
+                fallbacks.append(f"{hs}: {type(e).__name__}: {str(e)[:120]}")
+                torch.cuda.empty_cache()
+        if fallbacks:
+            out["headline"]["fallback"] = fallbacks
         clk.active = False
         if world == 1 and not args.quick:
             sw, wu = args.sec_steps, 1
@@ -474,7 +479,7 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
                                 arena, rank, world, nccl_id, local, sw, wu, dist)
             # ZFP vs raw on the largest C3-shaped grid whose raw store fits this host
             planes = [0, raw_nz // 4, raw_nz // 2, 3 * raw_nz // 4 - 4, raw_nz - 4]
-            HSr = dict(HS, P=pick_P(raw_nz, 64), slots=4, gen_chunk=16)   # (raw slots are twice the size)
+            HSr = dict(P=pick_P(raw_nz, 64), serpentine=1, m_resident=1, slots=4)   # (raw slots are twice the size)
             PFr = dict(PF, P=pick_P(raw_nz, 96))
             for key, rates, opt in (("half_zfp_hs", (RATE,) * 3, HSr), ("half_raw_hs", (0, 0, 0), HSr),
                                     ("half_zfp_pf", (RATE,) * 3, PFr), ("half_raw_pf", (0, 0, 0), PFr)):
@@ -965,8 +970,8 @@ def gpu_arm(args):
                                f"three fields (154.6 GB pinned host store), T={T}, P={h['P']} ({h['D']} z-blocks"
                                f"{' per GPU' if world > 1 else ''})",
                    "grid": [C3N, C3N, C3Z], "tb": T, "block_planes": h["P"], "rate": RATE,
-                   "schedule": f"serpentine sweeps + m decoded once into HBM + {h['schedule'].get('slots')} staging "
-                               "slots, kept blocks at the turns (the library's fastest "
+                   "schedule": f"serpentine sweeps + m {'compressed in HBM' if h['schedule'].get('m_hbm') else 'decoded once into HBM'}"
+                               f" + {h['schedule'].get('slots')} output staging slots, kept blocks at the turns (the library's fastest "
                                "schedule of the same computation, bit-identical to the paper's; the paper's own: "
                                "c3_paper_faithful)",
                    "step": "one sweep = T leapfrog steps over the whole grid",

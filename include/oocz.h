@@ -121,6 +121,12 @@ typedef struct {
                               rank with world > 1 (D = nz / world / P).  Needs store =
                               HOST when nonzero; -1 <= K <= D, else OOCZ_EINVAL.  Results
                               identical. */
+    int32_t  m_hbm;        /* 1: with store = OOCZ_STORE_HOST, the read-only m's compressed
+                              stream lives in HBM whole (decoded per block, never crossing the
+                              host link), whatever resident_blocks says for u and u-.  Half
+                              the HBM of m_resident's decoded m at rate 16, for more output
+                              slots.  0 or 1 (1 needs store = HOST), else OOCZ_EINVAL.
+                              Results identical. */
 } oocz_config;
 
 typedef struct {

@@ -187,7 +187,7 @@ struct oocz_ctx {
     // resident_blocks = K on a host store (a hybrid), 0 otherwise.  rows_ptr() maps.
     uint8_t* store[3] = {nullptr, nullptr, nullptr};
     uint8_t* dstore[3] = {nullptr, nullptr, nullptr};
-    int zres = 0;
+    int zres[3] = {0, 0, 0};                // per field (m_hbm: m's whole stream in HBM)
     size_t store_bytes[3] = {0, 0, 0};
     bool store_external = false;            // host store carved from a caller-owned arena (oocz_create_ex)
     // streams / events
@@ -267,14 +267,17 @@ double cfl_limit(const C c[5])
 // one 4-aligned plane range of a field's store as a byte range
 inline size_t rows_off(const oocz_ctx* c, int f, int plane) { return (size_t)(plane / 4) * c->row_bytes[f]; }
 // where the stored rows from `plane` on live (a block's rows are all in one place)
-inline bool rows_on_device(const oocz_ctx* c, int plane) { return plane < c->zres; }
+inline bool rows_on_device(const oocz_ctx* c, int f, int plane) { return plane < c->zres[f]; }
 inline uint8_t* rows_ptr(const oocz_ctx* c, int f, int plane)
 {
-    return plane < c->zres ? c->dstore[f] + rows_off(c, f, plane)
-                           : c->store[f] + (rows_off(c, f, plane) - rows_off(c, f, c->zres));
+    return plane < c->zres[f] ? c->dstore[f] + rows_off(c, f, plane)
+                              : c->store[f] + (rows_off(c, f, plane) - rows_off(c, f, c->zres[f]));
 }
 // the end of a chunk of stored rows starting at plane z that stays in one place
-inline int rows_chunk_end(const oocz_ctx* c, int z, int end) { return z < c->zres ? std::min(end, c->zres) : end; }
+inline int rows_chunk_end(const oocz_ctx* c, int f, int z, int end)
+{
+    return z < c->zres[f] ? std::min(end, c->zres[f]) : end;
+}
 
 cudaError_t encode_or_copy(oocz_ctx* c, int f, const uint8_t* src, int nplanes, uint8_t* dst, cudaStream_t s)
 {
@@ -403,6 +406,8 @@ extern "C" oocz_status oocz_validate(const oocz_config* cfg, int32_t world, char
     if (cfg->resident_blocks < -1 || cfg->resident_blocks > cfg->nz / world / cfg->block_planes)
         BAD(OOCZ_EINVAL, "resident_blocks (%d) outside [-1 (auto), D = %d]", cfg->resident_blocks,
             cfg->nz / world / cfg->block_planes);
+    if (cfg->m_hbm != 0 && cfg->m_hbm != 1) BAD(OOCZ_EINVAL, "m_hbm (%d) must be 0 or 1", cfg->m_hbm);
+    if (cfg->m_hbm && cfg->store != OOCZ_STORE_HOST) BAD(OOCZ_EINVAL, "m_hbm needs store = OOCZ_STORE_HOST");
     if (cfg->resident_blocks != 0 && cfg->store != OOCZ_STORE_HOST)
         BAD(OOCZ_EINVAL, "resident_blocks (%d) needs store = OOCZ_STORE_HOST", cfg->resident_blocks);
     if (cfg->precision != 32 && cfg->precision != 64)
@@ -506,6 +511,7 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         // get_field also stage P planes of any one field through slot 0
         size_t one_field = 0;
         for (int f = 0; f < slab_fields; f++) {
+            if (f == OOCZ_M && cfg->m_hbm) continue;          // m's rows are read in HBM
             ctx->in_off[f] = ctx->in_slot_bytes;
             ctx->in_slot_bytes += (size_t)(rd_max_planes / 4) * ctx->row_bytes[f];
         }
@@ -528,14 +534,20 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
         CKC(cudaMemGetInfo(&fr, &tot));
         const size_t budget = cfg->device_bytes ? cfg->device_bytes : fr;
         int K = cfg->resident_blocks;
+        const bool m_hbm = host && cfg->m_hbm;
+        if (m_hbm) need += rows_off(ctx, OOCZ_M, S);        // m's whole compressed stream in HBM
         if (host && K < 0) {    // auto: as many leading blocks as the budget leaves room for
             size_t per = 0;
-            for (int f = 0; f < 3; f++) per += rows_off(ctx, f, P);
+            for (int f = 0; f < 3; f++)
+                if (!(m_hbm && f == OOCZ_M)) per += rows_off(ctx, f, P);
             K = budget > need ? (int)std::min<size_t>((size_t)D, (budget - need) / std::max<size_t>(per, 1)) : 0;
             ctx->cfg.resident_blocks = K;
         }
-        ctx->zres = host ? std::min(std::max(K, 0) * P, S) : S;
-        for (int f = 0; f < 3; f++) need += rows_off(ctx, f, ctx->zres);   // the rows kept in HBM
+        for (int f = 0; f < 3; f++) {
+            ctx->zres[f] = host ? std::min(std::max(K, 0) * P, S) : S;
+            if (m_hbm && f == OOCZ_M) ctx->zres[f] = S;
+            else need += rows_off(ctx, f, ctx->zres[f]);   // the rows kept in HBM
+        }
         if (need > budget) {
             fprintf(stderr, "oocz_create: device memory %zu B needed > budget %zu B\n", need, budget);
             return cleanup_fail(OOCZ_ECAPACITY);
@@ -566,9 +578,9 @@ static oocz_status create_impl(const oocz_config* cfg, int32_t rank, int32_t wor
             CKC(cudaMalloc(&b, ctx->out_slot_bytes));
             ctx->out_slot.push_back(b);
         }
-        if (ctx->zres > 0)
-            for (int f = 0; f < 3; f++) CKC(cudaMalloc(&ctx->dstore[f], std::max<size_t>(rows_off(ctx, f, ctx->zres), 1)));
-        auto host_part = [&](int f) { return ctx->store_bytes[f] - rows_off(ctx, f, ctx->zres); };
+        for (int f = 0; f < 3; f++)
+            if (ctx->zres[f] > 0) CKC(cudaMalloc(&ctx->dstore[f], std::max<size_t>(rows_off(ctx, f, ctx->zres[f]), 1)));
+        auto host_part = [&](int f) { return ctx->store_bytes[f] - rows_off(ctx, f, ctx->zres[f]); };
         if (arena) {
             size_t want = 0;
             for (int f = 0; f < 3; f++) want += arena_field_bytes(host_part(f));
@@ -693,7 +705,7 @@ extern "C" size_t oocz_host_store_bytes(const oocz_config* cfg, int32_t world)
     const int zres = cfg->resident_blocks > 0 ? std::min(cfg->resident_blocks * cfg->block_planes, S) : 0;
     size_t t = 0;
     for (int f = 0; f < 3; f++)
-        t += arena_field_bytes((size_t)((S - zres) / 4) *
+        t += arena_field_bytes((size_t)((S - (cfg->m_hbm && f == OOCZ_M ? S : zres)) / 4) *
                                row_bytes_for(cfg->nx, cfg->ny, cfg->rate[f], esz_of(cfg)));
     return t;
 }
@@ -976,12 +988,12 @@ static oocz_status set_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     const int chunk = ctx->P;                       // planes per pass, <= slab capacity
     for (int z = z0, np; z < z0 + nplanes; z += np) {
-        np = rows_chunk_end(ctx, z, std::min(z + chunk, z0 + nplanes)) - z;
+        np = rows_chunk_end(ctx, field, z, std::min(z + chunk, z0 + nplanes)) - z;
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
         CK(cudaMemcpyAsync(buf, src + (size_t)(z - z0) * ctx->pb, (size_t)np * ctx->pb, in_kind, s));
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         const uint8_t* coded;
-        if (!rows_on_device(ctx, z)) {
+        if (!rows_on_device(ctx, field, z)) {
             uint8_t* dev = ctx->in_slot[0];         // device staging of the encoded rows
             CK(encode_or_copy(ctx, field, buf, np, dev, s));
             CK(cudaMemcpyAsync(rows_ptr(ctx, field, z), dev, bytes, cudaMemcpyDeviceToHost, s));
@@ -1052,10 +1064,10 @@ static oocz_status get_planes_impl(oocz_ctx* ctx, int32_t field, int32_t z0, int
     const int chunk = ctx->P;
     uint8_t* dst = static_cast<uint8_t*>(dst_v);
     for (int z = z0, np; z < z0 + nplanes; z += np) {
-        np = rows_chunk_end(ctx, z, std::min(z + chunk, z0 + nplanes)) - z;
+        np = rows_chunk_end(ctx, field, z, std::min(z + chunk, z0 + nplanes)) - z;
         const size_t bytes = (size_t)(np / 4) * ctx->row_bytes[field];
         uint8_t* buf = ctx->slab[0][0];              // scratch between steps
-        if (!rows_on_device(ctx, z)) {
+        if (!rows_on_device(ctx, field, z)) {
             uint8_t* dev = ctx->in_slot[0];
             CK(cudaMemcpyAsync(dev, rows_ptr(ctx, field, z), bytes, cudaMemcpyHostToDevice, s));
             CK(decode_or_copy(ctx, field, dev, np, buf, s));
@@ -1107,7 +1119,7 @@ extern "C" oocz_status oocz_save_store(oocz_ctx* ctx, int32_t field, void* dst, 
     if (bytes != ctx->store_bytes[field] || (!dst && bytes))
         return fail(ctx, OOCZ_EINVAL, "bytes (%zu) != store size (%zu)", bytes, ctx->store_bytes[field]);
     CK(cudaSetDevice(ctx->device));
-    const size_t dev_bytes = rows_off(ctx, field, ctx->zres);     // the rows kept in HBM come first
+    const size_t dev_bytes = rows_off(ctx, field, ctx->zres[field]);   // the rows kept in HBM come first
     if (dev_bytes) CK(cudaMemcpy(dst, ctx->dstore[field], dev_bytes, cudaMemcpyDeviceToHost));
     if (bytes > dev_bytes) std::memcpy(static_cast<uint8_t*>(dst) + dev_bytes, ctx->store[field], bytes - dev_bytes);
     return OOCZ_OK;
@@ -1126,7 +1138,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
     std::fill(ctx->rows_set[field].begin(), ctx->rows_set[field].end(), 0);
     std::fill(ctx->last_seq.begin(), ctx->last_seq.end(), -1LL);   // the store changes outside the slots
     {
-        const size_t dev_bytes = rows_off(ctx, field, ctx->zres);
+        const size_t dev_bytes = rows_off(ctx, field, ctx->zres[field]);
         if (dev_bytes) CK(cudaMemcpy(ctx->dstore[field], src, dev_bytes, cudaMemcpyHostToDevice));
         if (bytes > dev_bytes)
             std::memcpy(ctx->store[field], static_cast<const uint8_t*>(src) + dev_bytes, bytes - dev_bytes);
@@ -1135,7 +1147,7 @@ extern "C" oocz_status oocz_load_store(oocz_ctx* ctx, int32_t field, const void*
         for (int z = 0; z < ctx->S; z += ctx->P) {
             const int np = std::min(ctx->P, ctx->S - z);
             const uint8_t* coded = rows_ptr(ctx, field, z);
-            if (!rows_on_device(ctx, z)) {
+            if (!rows_on_device(ctx, field, z)) {
                 CK(cudaMemcpyAsync(ctx->in_slot[0], coded, (size_t)(np / 4) * ctx->row_bytes[field],
                                    cudaMemcpyHostToDevice, s));
                 coded = ctx->in_slot[0];
@@ -1188,7 +1200,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     const size_t pb = ctx->pb;
     // this block's rows stream over the host link (not kept in HBM: device store or
     // resident_blocks)
-    const bool host = !rows_on_device(ctx, g.own0);
+    const bool host = !rows_on_device(ctx, OOCZ_U, g.own0);
     const int islot = (int)(ctx->seq % (long long)ctx->ev_in_ready.size());    // input staging slot
     const int slot = (int)(ctx->seq % (long long)ctx->ev_out_ready.size());    // output staging slot
     // slab set: blocks rotate through nsets; with serpentine sweeps by block
@@ -1220,7 +1232,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
         auto add = [&](int z0, int z1, int owner) {
             if (z1 <= z0) return;
             Part q{z0, z1, nullptr, false};
-            if (rows_on_device(ctx, z0)) {
+            if (rows_on_device(ctx, f, z0)) {
                 q.src = rows_ptr(ctx, f, z0);
             } else if (f != OOCZ_M && rows_in_slot(ctx, owner)) {
                 q.src = ctx->out_slot[ctx->last_slot[owner]] + ctx->out_off[f] +
@@ -1327,7 +1339,7 @@ static oocz_status enqueue_block(oocz_ctx* ctx, int sweep, int i, int ts, int di
     for (int f = 0; f < nf; f++)
         for (int k = 0; k < nparts[f]; k++) {
             const int o = owner_of(part[f][k]);
-            if (!part[f][k].h2d && ctx->kept[o] && !rows_on_device(ctx, part[f][k].z0))
+            if (!part[f][k].h2d && ctx->kept[o] && !rows_on_device(ctx, f, part[f][k].z0))
                 CK(cudaEventRecord(ctx->ev_out_free[ctx->last_slot[o]], sd));
         }
     // keep the time-t shared region for the next block (reading R14):

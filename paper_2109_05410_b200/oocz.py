@@ -37,7 +37,7 @@ class oocz_config(C.Structure):
                 ("profile", C.c_int32), ("device_bytes", C.c_uint64), ("m_resident", C.c_int32),
                 ("precision", C.c_int32), ("c64", C.c_double * 5), ("serpentine", C.c_int32),
                 ("slab_sets", C.c_int32), ("graphs", C.c_int32), ("cone", C.c_int32),
-                ("resident_blocks", C.c_int32)]
+                ("resident_blocks", C.c_int32), ("m_hbm", C.c_int32)]
 
 
 class oocz_stats(C.Structure):

@@ -201,3 +201,28 @@ def test_resident_blocks_with_a_caller_arena():
             z.oocz_destroy(ctx)
     finally:
         z.oocz_host_free(arena)
+
+
+@pytest.mark.parametrize("K,serpentine,slots", [(0, 1, 5), (1, 1, 3), (0, 0, 2), (2, 1, 7)])
+def test_m_hbm_matches_oracle_and_moves_no_m_bytes(K, serpentine, slots):
+    """m_hbm = 1: m's compressed stream lives in HBM whole and is decoded per block
+    (never crossing the host link), u and u- placed as resident_blocks says:
+    bit-exact, and the H2D bytes carry no m rows."""
+    z = Z()
+    nx, ny, nz, T, P, rates = 32, 24, 96, 2, 16, (16, 12, 8)
+    u, up, m = _fields(nx, ny, nz, 37)
+    calls = [7, 4]
+    cfg = _cfg(z, nx, ny, nz, T, P, rates, K, serpentine=serpentine, slots=slots, m_hbm=1)
+    ref = _cfg(z, nx, ny, nz, T, P, rates, K, serpentine=serpentine, slots=slots, m_resident=1)
+    with z.Stepper(cfg) as s, z.Stepper(ref) as r:
+        for st in (s, r):
+            st.set(u, up, m)
+            for n in calls:
+                st.step(n)
+        wa, wb = _run_oracle(u, up, m, T, rates, calls)
+        assert np.array_equal(bits(s.get(z.OOCZ_U)), bits(wa))
+        assert np.array_equal(bits(s.get(z.OOCZ_UPREV)), bits(wb))
+        # m decoded once (m_resident) or read in HBM (m_hbm): the same host traffic
+        assert s.stats()["h2d_bytes"] == r.stats()["h2d_bytes"]
+        assert s.stats()["d2h_bytes"] == r.stats()["d2h_bytes"]
+        assert np.array_equal(bits(s.get(z.OOCZ_M)), bits(r.get(z.OOCZ_M)))

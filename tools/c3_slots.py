@@ -20,10 +20,12 @@ arena_p = Z.oocz_host_alloc(need)
 try:
     for slots in [int(x) for x in (sys.argv[1] if len(sys.argv) > 1 else "3,4,5,6").split(",")]:
         try:
-            r = bench.run_c3(Z, f"slots{slots}", nx, ny, nz, (16,) * 3,
-                             dict(P=64, serpentine=1, m_resident=1, slots=slots, gen_chunk=4 if slots >= 5 else 16), (arena_p, need), 0, 1, None, 0,
+            mode = sys.argv[2] if len(sys.argv) > 2 else "mres"
+            opt = (dict(P=64, serpentine=1, m_hbm=1, slots=slots, gen_chunk=4) if mode == "mhbm" else
+                   dict(P=64, serpentine=1, m_resident=1, slots=slots, gen_chunk=4 if slots >= 5 else 16))
+            r = bench.run_c3(Z, f"slots{slots}_{mode}", nx, ny, nz, (16,) * 3, opt, (arena_p, need), 0, 1, None, 0,
                              4, 2, None)
-            print(json.dumps({"slots": slots, "G": round(r["cups"] / 1e9, 2), "h2d_GB": round(r["h2d_per_sweep"] / 1e9, 2),
+            print(json.dumps({"slots": slots, "mode": mode, "G": round(r["cups"] / 1e9, 2), "h2d_GB": round(r["h2d_per_sweep"] / 1e9, 2),
                               "d2h_GB": round(r["d2h_per_sweep"] / 1e9, 2), "h2d_GBps": round(r["h2d_GBps"], 2),
                               "d2h_GBps": round(r["d2h_GBps"], 2), "device_GB": round(r["device_bytes"] / 1e9, 1)}),
                   flush=True)
