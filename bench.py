@@ -240,19 +240,23 @@ def kernel_table(evs) -> dict:
     return per
 
 
-def roofline(evs, peak_gbs, peak_src):
+def roofline(evs, peak_gbs, peak_src, force=None):
     """Dominant kernel of the timed region from its per-launch CUDA events
     (recorded on the stream each kernel is launched on): achieved =
     algorithmic bytes of all its launches / their summed duration."""
     per = kernel_table(evs)
     if not per:
         return None, {}
-    dom = max(per, key=lambda k: per[k][0])
+    dom = force if force in per else max(per, key=lambda k: per[k][0])
     ms, nbytes, n = per[dom]
     achieved = nbytes / (ms / 1e3) / 1e9
     table = {k: {"ms": round(v[0], 4), "launches": v[2], "GB/s": round(v[1] / (v[0] / 1e3) / 1e9, 1),
                  "avg_launch_ms": round(v[0] / v[2], 4)}
              for k, v in per.items()}
+    if dom != "stencil" and not force:
+        alu = _alu_roofline(dom, per[dom])
+        if alu:
+            return alu, table
     kern = {"stencil": "stencil25_kernel", "decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[dom]
     traffic, tsrc = None, None
     try:   # DRAM bytes per launch from a committed ncu capture of the same kind of launch
@@ -269,6 +273,39 @@ def roofline(evs, peak_gbs, peak_src):
             "launches": n, "algorithmic_bytes_per_launch": int(nbytes / n),
             "algorithmic_bytes": "stencil: 16 B per updated cell (read u, u-, m; write u+); decode / encode: "
                                  "compressed bytes + 4 B per value (DESIGN.md section 6)"}, table
+
+
+def _alu_roofline(stage: str, rec) -> dict | None:
+    """The dominant kernel is a codec kernel (with m decoded per block the decode
+    leads the device time): it is bound by the integer ALU pipe, so its roofline is
+    ALU-pipe warp-instructions per second.  Instructions per value come from the
+    committed ncu capture of the C3-wide launch (profiles/r02g_ncu_kernels.json:
+    ALU-pipe share x peak x duration / values); values per in-step launch from the
+    launch's algorithmic bytes (compressed + 4 B per value at rate 16: 6 B/value)."""
+    name = {"decode": "zfp_decode_kernel", "encode": "zfp_encode_kernel"}[stage]
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02g_ncu_kernels.json")) as fh:
+            ks = [k for k in json.load(fh)["c3_slab"]["kernels"] if k["kernel"].endswith(name)]
+    except Exception:
+        return None
+    if not ks:
+        return None
+    k = ks[0]
+    values = C3N * C3N * 96
+    alu_per_value = k["alu_pipe_pct"] / 100.0 * ALU_PEAK * 1e9 * k["us"] * 1e-6 / values
+    ms, nbytes, n = rec
+    per_launch_values = nbytes / n / (4 + RATE / 8)
+    achieved = alu_per_value * per_launch_values / (ms / n / 1e3) / 1e9
+    return {"bound": "alu", "kernel": name, "achieved": round(achieved, 1), "peak": round(ALU_PEAK, 1),
+            "peak_source": "148 SMs x 4 sub-partitions x one ALU-pipe warp-instruction per 2 cycles x 1.965 GHz "
+                           "(B300_MICROARCH pipe rates; DESIGN.md section 6)",
+            "unit": "G ALU-pipe warp-instructions/s", "frac": round(achieved / ALU_PEAK, 4),
+            "traffic": None, "avg_launch_ms": round(ms / n, 4), "launches": n,
+            "alu_instructions_per_value": round(alu_per_value * 32, 2),
+            "what": "the dominant kernel of the step (most device time) is the decoder, bound by the integer "
+                    "ALU pipe: ALU-pipe warp-instructions per value from ncu on the C3-wide launch "
+                    "(profiles/r02g_ncu_kernels.json) x values per in-step launch / the in-step launch time "
+                    "(CUDA events on the decode stream); the HBM-bound stencil's roofline is roofline_stencil"}
 
 
 def codec_alu_roofline(table) -> dict | None:
@@ -594,6 +631,7 @@ def c3_report(c3, args, world, link, peak_gbs, peak_src, info):
                         "of the updated read-write fields are inside the call",
                 "ms_per_step": round(h["host_s"] * 1e3 / args.steps, 3)},
         "roofline": roof,
+        "roofline_stencil": roofline(h["evs"], peak_gbs, peak_src, force="stencil")[0],
         "roofline_host_link": {
             "bound": "host-link", "direction": bound_dir,
             "achieved": round(busier * args.steps / h["device_s"] / 1e9, 2),
@@ -979,6 +1017,7 @@ def gpu_arm(args):
                    "parallelism": f"z-slabs x{world}, NCCL compressed halos" if world > 1 else "single GPU"},
         "e2e": rep["e2e"],
         "roofline": rep["roofline"],
+        "roofline_stencil": rep["roofline_stencil"],
         "roofline_host_link": rep["roofline_host_link"],
         "gpu_launches": rep["gpu_launches"],
         "kernels_in_step": rep["kernels_in_step"],
