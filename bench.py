@@ -482,15 +482,18 @@ def c3_arm(args, Z, rank, world, local, dist, nccl_id, peak_gbs, peak_src, link,
     t_arena = time.perf_counter() - t0
     out = {"arena": {"bytes": need, "alloc_s": round(t_arena, 1)}}
     try:
-        # m's compressed stream in HBM (m_hbm, decoded per block) instead of a decoded m, and
-        # the HBM that frees as 16 output staging slots: 8 kept blocks per serpentine turn
-        # (DESIGN.md §7).  They fill HBM to ~184 GB, so the field generator works in 4-plane
-        # chunks; a box with less free HBM falls back to 12 slots, then to 4 with m resident
-        HS = dict(P=pick_P(S, 64), serpentine=1, m_hbm=1, slots=16, gen_chunk=4)
+        # m's compressed stream in HBM (m_hbm, decoded per block) instead of a decoded m, one
+        # slab set (the device work, decode -> stencil -> encode in series, still fits in
+        # the link time), and the HBM that frees as 20 output staging slots: 10 kept blocks
+        # per serpentine turn.  They fill HBM to ~182 GB, so the field
+        # generator works in 4-plane chunks; a box with less free HBM falls back to 16 slots
+        # and two slab sets, then 12, then 4 with m decoded in HBM
+        HS = dict(P=pick_P(S, 64), serpentine=1, m_hbm=1, slots=20, slab_sets=1, gen_chunk=4)
         PF = dict(P=pick_P(S, 192), serpentine=0, m_resident=0, slots=2, cone=1)
         clk.active = True
         fallbacks = []
-        for hs in (HS, dict(HS, slots=12), dict(P=HS["P"], serpentine=1, m_resident=1, slots=4)):
+        for hs in (HS, dict(HS, slots=16, slab_sets=0), dict(HS, slots=12, slab_sets=0),
+                   dict(P=HS["P"], serpentine=1, m_resident=1, slots=4)):
             try:
                 out["headline"] = run_c3(Z, "c3_zfp_host", nx, ny, nz, (RATE,) * 3, hs, arena, rank, world,
                                          nccl_id, local, args.steps, args.warmup, dist, profile=1)

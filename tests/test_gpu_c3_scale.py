@@ -88,7 +88,7 @@ def test_gpu_generators_match_synth_at_4096():
 @pytest.mark.parametrize("name,opts", [
     ("paper_faithful", dict(block_planes=128)),                                   # D = 2, slab 2.68e9 values
     ("serpentine_m_resident", dict(block_planes=64, serpentine=1, m_resident=1, slots=7)),   # m_full 4.8e9 values
-    ("serpentine_m_hbm", dict(block_planes=64, serpentine=1, m_hbm=1, slots=16)),              # the headline schedule
+    ("serpentine_m_hbm", dict(block_planes=64, serpentine=1, m_hbm=1, slots=20, slab_sets=1)),  # the headline schedule
     ("hbm_store_one_set", dict(block_planes=128, store=1, slab_sets=1)),
 ])
 def test_c3_scale_sampled_parity(name, opts, expected, arena):

@@ -22,6 +22,7 @@ try:
         try:
             mode = sys.argv[2] if len(sys.argv) > 2 else "mres"
             opt = (dict(P=64, serpentine=1, m_hbm=1, slots=slots, gen_chunk=4) if mode == "mhbm" else
+                   dict(P=64, serpentine=1, m_hbm=1, slots=slots, gen_chunk=4, slab_sets=1) if mode == "mhbm1" else
                    dict(P=64, serpentine=1, m_resident=1, slots=slots, gen_chunk=4 if slots >= 5 else 16))
             r = bench.run_c3(Z, f"slots{slots}_{mode}", nx, ny, nz, (16,) * 3, opt, (arena_p, need), 0, 1, None, 0,
                              4, 2, None)
